@@ -1,0 +1,316 @@
+"""Pins for the CPU oracle (-m "not gpu").  Each test ties an oracle function to
+something other than itself: values derived in SPEC/SURVEY from the paper's
+equations, closed forms, textbook special cases, brute force, and an
+independent event-driven evaluator (tests/brute.py)."""
+import numpy as np
+import pytest
+from scipy.sparse import csr_matrix
+from scipy.sparse.csgraph import shortest_path
+
+import brute
+import oracle as O
+from fixtures import load_golden, random_instance, undirected_to_directed
+
+INF = 0xFF
+
+
+# ----------------------------------------------------------------- coarsening
+def test_coarsen_worked_values():
+    # SPEC S:142-144, derived from Eq. 1-3
+    assert O.coarsen(0.5, 0.5, 4.0) == 4          # w = alpha -> Rounding(A)
+    assert O.coarsen(0.0, 0.5, 4.0) == 0          # reward A
+    assert O.coarsen(1.0, 0.5, 4.0) == 8          # penalty A
+    assert O.coarsen(0.75, 0.5, 4.0) == 6         # 4 + 4*(0.25/0.5)
+    assert O.coarsen(0.25, 0.5, 4.0) == 2         # consistency witness S:152
+
+
+def test_bound_worked_values():
+    # SPEC S:151-153 from Theorem boundEdgeWeight
+    assert O.bound(2, 0.5, 4.0) == pytest.approx((0.1875, 0.3125))
+    assert O.bound(4, 0.5, 4.0) == pytest.approx((0.4375, 0.5625))
+
+
+def test_coarsen_bound_roundtrip_and_invariants():
+    # SPEC acceptance 1: 1e4 random triples, w in bound(coarsen(w)); monotone; range.
+    rng = np.random.default_rng(7)
+    for _ in range(10000):
+        w = float(rng.random())
+        alpha = float(rng.choice([0.2, 0.5, 0.8]))
+        A = float(rng.uniform(2, 6))
+        a = O.coarsen(w, alpha, A)
+        lo, hi = O.bound(a, alpha, A)
+        assert lo - 1e-12 <= w < hi + 1e-12, (w, alpha, A, a, lo, hi)
+        assert 0 <= a <= int(np.floor(2 * A + 0.5))
+        # closed form of case 1: A - A(alpha-w)/alpha = A w / alpha (away from .5 ties)
+        if w <= alpha:
+            x = A * w / alpha
+            if abs(x - np.floor(x) - 0.5) > 1e-9:
+                assert a == int(np.floor(x + 0.5))
+    ws = np.sort(rng.random(2000))
+    a = O.coarsen_all(ws, 0.5, 3.87)
+    assert (np.diff(a.astype(int)) >= 0).all()
+
+
+def test_fine_weights_hand_fixtures():
+    # lone edge -> log 2; 3 same-label out-edges into single-in targets -> log 4;
+    # uniform graph -> all 0 (degenerate rescale, R2).
+    # star v->a,v->b,v->c (label 0) + lone x->y (label 1); reverse edges class 2L+1.
+    src = np.array([0, 1, 0, 2, 0, 3, 4, 5], np.uint32)
+    dst = np.array([1, 0, 2, 0, 3, 0, 5, 4], np.uint32)
+    cls = np.array([0, 1, 0, 1, 0, 1, 2, 3], np.uint32)
+    w = O.fine_weights(6, src, dst, cls)
+    # raw: star edges ln(3+1), their reverses ln(1+3), lone edges ln(1+1); min ln2, max ln4
+    assert np.allclose(w, [1, 1, 1, 1, 1, 1, 0, 0])
+    # mixed: a 2-edge fan (raw ln 3) sits halfway between ln2 and ln4 in log space? no:
+    # (ln3 - ln2)/(ln4 - ln2) = log2(1.5)
+    src2 = np.concatenate([src, np.array([6, 7, 6, 8], np.uint32)])
+    dst2 = np.concatenate([dst, np.array([7, 6, 8, 6], np.uint32)])
+    cls2 = np.concatenate([cls, np.array([4, 5, 4, 5], np.uint32)])
+    w2 = O.fine_weights(9, src2, dst2, cls2)
+    assert np.allclose(w2[8:], np.log2(1.5))
+    u = O.fine_weights(2, np.array([0, 1], np.uint32), np.array([1, 0], np.uint32), np.array([0, 1], np.uint32))
+    assert (u == 0).all()
+
+
+def test_fine_weights_bruteforce_counts():
+    rng = np.random.default_rng(3)
+    V, E = 30, 200
+    src = rng.integers(0, V, E).astype(np.uint32)
+    dst = rng.integers(0, V, E).astype(np.uint32)
+    cls = rng.integers(0, 4, E).astype(np.uint32)
+    w = O.fine_weights(V, src, dst, cls)
+    raw = np.array([np.log(np.sum((src == src[e]) & (cls == cls[e])) + np.sum((dst == dst[e]) & (cls == cls[e])))
+                    for e in range(E)])
+    ref = (raw - raw.min()) / (raw.max() - raw.min())
+    assert np.allclose(w, ref, rtol=0, atol=1e-15)
+
+
+# ----------------------------------------------------------------- path scoring
+def test_path_score_examples_and_closed_form():
+    assert O.path_score([]) == 0 and O.path_score([2, 1]) == 4 and O.path_score([1, 5]) == 6
+    rng = np.random.default_rng(11)
+    for _ in range(3000):
+        seq = rng.integers(0, 10, int(rng.integers(0, 12))).tolist()
+        assert O.path_score(seq) == brute.path_score_closed(seq)
+
+
+def test_rpg_score_examples():
+    assert O.rpg_score(0.5, 2, 4) == 3.0
+    assert O.rpg_score(1.0, 2, 7) == 2.0 and O.rpg_score(0.0, 2, 7) == 7.0  # endpoints S:234
+    assert O.rpg_score(0.3, 2, 2) == pytest.approx(2.0)
+
+
+# ----------------------------------------------------------------- hitting levels (Alg. 1)
+def test_known_answer_levels():
+    d = load_golden("two_node.json")
+    for case in d["cases"]:
+        s, t, a = undirected_to_directed(case["undirected_edges"])
+        g = O.Graph(case["nodes"], s, t, a)
+        H, blk, L, _ = O.phase(g, [np.array(x, np.uint32) for x in case["terms"]], case["depth"], 0)
+        assert H.tolist() == case["expect_H"]
+
+
+def _bfs_levels(V, src, dst, sources):
+    A = csr_matrix((np.ones(len(src)), (src.astype(np.int64), dst.astype(np.int64))), shape=(V, V))
+    d = shortest_path(A, unweighted=True, directed=True, indices=np.asarray(sources, np.int64))
+    return d.min(axis=0) if d.ndim == 2 else d
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_levels_special_cases_and_dijkstra(seed):
+    rng = np.random.default_rng(100 + seed)
+    V, src, dst, act, terms = random_instance(rng, 5, 40, T_hi=3)
+    D = int(rng.choice([3, 5, 8, 20]))
+    # textbook case: all a = 0, no blocking -> multi-source BFS hops (capped at D)
+    g0 = O.Graph(V, src, dst, np.zeros_like(act))
+    H0, _, _, _ = O.phase(g0, terms, D, 0)
+    for j, t in enumerate(terms):
+        bfs = _bfs_levels(V, src, dst, t)
+        ref = np.where(np.isfinite(bfs) & (bfs <= D), bfs, INF).astype(np.int64)
+        assert (H0[:, j].astype(np.int64) == ref).all()
+    # a == c everywhere -> h = c + hops for hops >= 1
+    c = int(rng.integers(1, 4))
+    gc = O.Graph(V, src, dst, np.full_like(act, c))
+    Hc, _, _, _ = O.phase(gc, terms, 40, 0)
+    for j, t in enumerate(terms):
+        bfs = _bfs_levels(V, src, dst, t)
+        ref = np.where(np.isfinite(bfs), np.where(bfs >= 1, bfs + c, 0), INF)
+        assert (Hc[:, j].astype(np.int64) == ref.astype(np.int64)).all()
+    # general activations, no blocking: label-correcting Dijkstra on Def. pathScoring
+    g = O.Graph(V, src, dst, act)
+    H, _, _, _ = O.phase(g, terms, D, 0)
+    for j, t in enumerate(terms):
+        dj = brute.dijkstra_levels(V, src, dst, act, t)
+        ref = np.where(dj <= D, dj, INF)
+        assert (H[:, j].astype(np.int64) == ref).all()
+        # north-star invariant: finite h >= unweighted BFS distance
+        bfs = _bfs_levels(V, src, dst, t)
+        fin = H[:, j] != INF
+        assert (H[fin, j] >= bfs[fin]).all()
+    # with central blocking the invariant still holds
+    Hb, _, _, _ = O.phase(g, terms, D, 1)
+    for j, t in enumerate(terms):
+        bfs = _bfs_levels(V, src, dst, t)
+        fin = Hb[:, j] != INF
+        assert (Hb[fin, j] >= bfs[fin]).all()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_levels_bruteforce_paths(seed):
+    rng = np.random.default_rng(500 + seed)
+    V, src, dst, act, terms = random_instance(rng, 4, 9, deg=2.0, T_hi=2)
+    g = O.Graph(V, src, dst, act)
+    H, _, _, _ = O.phase(g, terms, 40, 0)
+    for j, t in enumerate(terms):
+        bp = brute.brute_levels(V, src, dst, act, t)
+        assert (H[:, j].astype(np.int64) == bp).all()
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_levels_match_event_driven_with_blocking(seed):
+    # O1 (literal level-synchronous Alg. 1 with CF) == O2 (event buckets, closed-form blocking)
+    rng = np.random.default_rng(900 + seed)
+    V, src, dst, act, terms = random_instance(rng, 5, 40, T_hi=4)
+    D = int(rng.choice([3, 5, 8, 20]))
+    g = O.Graph(V, src, dst, act)
+    for mode in (0, 1, 2):
+        H, blk, L, _ = O.phase(g, terms, D, mode)
+        blocking = mode == 1 or (mode == 2 and len(terms) >= 2)
+        H2 = brute.o2_levels(V, src, dst, act, terms, D, blocking)
+        assert (H.astype(np.int64) == H2).all(), mode
+        # R10 closed form: block = max row if complete, else inf (only when blocking)
+        comp = (H != INF).all(axis=1)
+        ref = np.where(comp, H.max(axis=1), INF) if blocking else np.full(V, INF)
+        assert (blk.astype(np.int64) == ref.astype(np.int64)).all()
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_levels_depth_truncation_and_permutation(seed):
+    rng = np.random.default_rng(1300 + seed)
+    V, src, dst, act, terms = random_instance(rng, 5, 40, T_hi=3)
+    g = O.Graph(V, src, dst, act)
+    for mode in (0, 1):
+        Hd, _, _, _ = O.phase(g, terms, 4, mode)
+        Hf, _, _, _ = O.phase(g, terms, 30, mode)
+        assert (Hd == np.where(Hf <= 4, Hf, INF)).all()
+        perm = rng.permutation(len(src))
+        gp = O.Graph(V, src[perm], dst[perm], act[perm])
+        Hp, bp, _, _ = O.phase(gp, terms, 30, mode)
+        assert (Hp == Hf).all()
+
+
+def test_alpha_monotonicity():
+    # smaller alpha -> pointwise larger-or-equal a -> pointwise larger-or-equal H (no blocking)
+    rng = np.random.default_rng(5)
+    for _ in range(30):
+        V, src, dst, _, terms = random_instance(rng, 5, 30)
+        w = rng.random(len(src))
+        a3 = O.coarsen_all(w, 0.3, 3.87)
+        a7 = O.coarsen_all(w, 0.7, 3.87)
+        assert (a3 >= a7).all()
+        H3, _, _, _ = O.phase(O.Graph(V, src, dst, a3), terms, 30, 0)
+        H7, _, _, _ = O.phase(O.Graph(V, src, dst, a7), terms, 30, 0)
+        assert (H3 >= H7).all()
+
+
+# ----------------------------------------------------------------- end-to-end fixtures
+def _run_fixture(name, **kw):
+    d = load_golden(name)
+    s, t, a = undirected_to_directed(d["undirected_edges"])
+    g = O.Graph(d["nodes"], s, t, a)
+    C = [np.array(x, np.uint32) for x in d["central"]]
+    M = [np.array(x, np.uint32) for x in d["marginal"]]
+    r = O.search(g, C, M, d["k"], d["depth"], gamma=d["gamma"], **kw)
+    return d, s, t, r
+
+
+@pytest.mark.parametrize("name", ["five_node.json", "diamond.json", "r16_blocked_relay.json",
+                                  "ptc_fail_m2.json", "ptc_fail_m3.json", "ptc_pass_vc_marginal.json"])
+def test_golden_end_to_end(name):
+    d, s, t, r = _run_fixture(name)
+    assert len(r.rpgs) == len(d["expect"])
+    for got, exp in zip(r.rpgs, d["expect"]):
+        assert got.central_node == exp["central_node"]
+        assert got.sc == exp["sc"] and got.sm == exp["sm"] and got.score == exp["score"]
+        assert got.nodes.tolist() == exp["nodes"]
+        de = sorted((int(s[e]), int(t[e])) for e in got.edge_ids)
+        assert de == sorted(tuple(x) for x in exp["directed_edges"])
+    if "expect_ptc_fail" in d:
+        assert r.n_ptc_fail == d["expect_ptc_fail"]
+
+
+def test_ptc_modes_on_vc_marginal():
+    # exclusive form rejects what the inclusive reading (R19) accepts
+    _, _, _, r3 = _run_fixture("ptc_pass_vc_marginal.json", ptc_mode=3)
+    assert len(r3.rpgs) == 0
+    # flag-only keeps the PTC failure, flagged
+    _, _, _, r1 = _run_fixture("ptc_fail_m2.json", ptc_mode=1)
+    assert len(r1.rpgs) == 1 and r1.rpgs[0].ptc == 0
+
+
+# ----------------------------------------------------------------- whole search vs plain definition
+def _random_query(rng, V, src, dst, act):
+    nc = int(rng.integers(1, 4))
+    nm = int(rng.integers(0, 4))
+    terms = [np.unique(rng.integers(0, V, int(rng.integers(1, 4)))).astype(np.uint32) for _ in range(nc + nm)]
+    return terms[:nc], terms[nc:]
+
+
+@pytest.mark.parametrize("seed", range(80))
+def test_search_matches_plain_definition(seed):
+    # early-terminated O1 == exhaustive plain-definition form built from
+    # O2 + path enumeration + brute PTC (tests/brute.py)
+    rng = np.random.default_rng(2000 + seed)
+    V, src, dst, act, _ = random_instance(rng, 6, 18, deg=2.2, amax=4)
+    C, M = _random_query(rng, V, src, dst, act)
+    k = int(rng.choice([1, 3, 5]))
+    D = int(rng.choice([3, 6, 20]))
+    g = O.Graph(V, src, dst, act)
+    r = O.search(g, C, M, k, D)
+    ref, cands = brute.search_plain(V, src, dst, act, C, M, k, D)
+    assert [(c.sc, c.v) for c in r.candidates] == cands
+    got = [(x.score, x.sc, x.central_node, x.sm, x.nodes.tolist(), sorted(int(e) for e in x.edge_ids))
+           for x in r.rpgs]
+    exp = [(x[0], x[1], x[2], x[3], x[4], x[5]) for x in ref]
+    assert got == exp
+    # exhaustive mode gives the same answer (early termination must not change it)
+    r2 = O.search(g, C, M, k, D, early_term=2)
+    assert [(x.score, x.central_node, x.edge_ids.tolist()) for x in r2.rpgs] == \
+           [(x.score, x.central_node, x.edge_ids.tolist()) for x in r.rpgs]
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_search_degenerate_cases(seed):
+    rng = np.random.default_rng(4000 + seed)
+    V, src, dst, act, _ = random_instance(rng, 8, 30, amax=4)
+    g = O.Graph(V, src, dst, act)
+    t0 = np.unique(rng.integers(0, V, 4)).astype(np.uint32)
+    # |C| = 1: every central keyword node is a score-0 CG at level 0
+    r = O.search(g, [t0], [], 2, 20)
+    assert [(c.sc, c.v) for c in r.candidates] == [(0, int(v)) for v in t0]
+    assert r.Lc == 0
+    # M = empty: top-k CGs by (S^c, v), S^r = S^c
+    t1 = np.unique(rng.integers(0, V, 3)).astype(np.uint32)
+    r = O.search(g, [t0, t1], [], 3, 20)
+    exp = sorted((c.sc, c.v) for c in r.candidates)[:3]
+    assert [(x.sc, x.central_node) for x in r.rpgs] == exp
+    assert all(x.score == x.sc for x in r.rpgs)
+    # level-score law: identified CG scores never exceed the terminating level
+    assert all(c.sc <= r.Lc for c in r.candidates)
+
+
+@pytest.mark.parametrize("seed", range(150))
+def test_search_plain_definition_marginal_heavy(seed):
+    # |M| in {2,3}, low activations: exercises the stop rule, attach and PTC failures (R20)
+    rng = np.random.default_rng(7000 + seed)
+    V, src, dst, act, _ = random_instance(rng, 8, 20, deg=2.5, amax=3)
+    nc = int(rng.integers(1, 3))
+    nm = int(rng.integers(2, 4))
+    terms = [np.unique(rng.integers(0, V, int(rng.integers(1, 3)))).astype(np.uint32) for _ in range(nc + nm)]
+    C, M = terms[:nc], terms[nc:]
+    k = int(rng.choice([1, 3, 5]))
+    r = O.search(O.Graph(V, src, dst, act), C, M, k, 20)
+    ref, _ = brute.search_plain(V, src, dst, act, C, M, k, 20)
+    got = [(x.score, x.sc, x.central_node, x.sm, x.nodes.tolist(), sorted(int(e) for e in x.edge_ids))
+           for x in r.rpgs]
+    assert got == [(x[0], x[1], x[2], x[3], x[4], x[5]) for x in ref]
