@@ -1,0 +1,302 @@
+"""Benchmark of the RIKI hot path on B200.
+
+python bench.py [--gpus N --steps K --warmup W] [--impl riki|reference] [--config 2]
+
+A step = one batch of the config's synthetic RPQ workload (config 2: 200 queries, 2 central +
+2 marginal keywords, k = 10, depth 20, on a 1M-node / 5M-edge power-law KG) through the
+whole hot path (both runs, recovery, PTC, top-k) with inputs resident in HBM.  Under
+torchrun every rank runs its own batch on its own GPU (query-sharded replicas, weak
+scaling, no collective on the data path); the time is the max over ranks.
+--impl reference times the CPU oracle (oracle/, the only reference this paper has) on a
+bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RPQ queries/sec"
+UNIT = "queries/s"
+
+
+def _workload_name(cfg, spec):
+    return (f"C{cfg} {spec.name}: synthetic power-law KG {spec.n_nodes} nodes / {spec.n_edges} directed edges, "
+            f"{spec.n_central} central + {spec.n_marginal} marginal keywords, k={spec.k}, depth {spec.depth}")
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = max(mx, float(p[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws <= 1:
+        return 0, 1, None
+    import torch
+    import torch.distributed as dist
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, ws, dist
+
+
+def oracle_sample(kg, qs, idx, og=None):
+    """Times the CPU oracle (as it stands, single thread) on queries idx; returns (seconds, og)."""
+    import oracle as O
+    if og is None:
+        w = O.fine_weights(kg.n_nodes, kg.src, kg.dst, kg.label_class)
+        og = O.Graph(kg.n_nodes, kg.src, kg.dst, O.coarsen_all(w, 0.5, kg.avg_hops))
+    t0 = time.perf_counter()
+    for i in idx:
+        O.search(og, [kg.posting(t) for t in qs.central[i]], [kg.posting(t) for t in qs.marginal[i]], qs.k,
+                 qs.depth, want_matrices=False, want_candidates=False)
+    return time.perf_counter() - t0, og
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import synth
+    spec = synth.CONFIGS[args.config]
+    kg = synth.make_kg(args.config)
+    qs = synth.config_queries(kg, args.config)
+    per = args.ref_queries
+    og = None
+    for s in range(args.warmup):
+        _, og = oracle_sample(kg, qs, range(s * per, (s + 1) * per), og)
+    times = []
+    for s in range(args.steps):
+        i0 = ((args.warmup + s) * per) % len(qs.central)
+        dt, og = oracle_sample(kg, qs, [(i0 + j) % len(qs.central) for j in range(per)], og)
+        times.append(dt)
+    tot = sum(times)
+    v = per * args.steps / tot
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": _workload_name(args.config, spec), "queries_per_step": per},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{per} queries of the config-{args.config} query set per step, "
+                                       f"single-threaded oracle/riki_oracle.c"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="riki", choices=["riki", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--queries", type=int, default=0, help="queries per step (default: the config's query set)")
+    ap.add_argument("--cpu-sample", type=int, default=16, help="oracle queries for cpu_baseline")
+    ap.add_argument("--ref-queries", type=int, default=4, help="oracle queries per step for --impl reference")
+    ap.add_argument("--latency-queries", type=int, default=40)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+
+    import paper_2001_06770_b200 as P
+    import synth
+
+    rank, world, dist = _dist()
+    dev = torch.cuda.current_device()
+    spec = synth.CONFIGS[args.config]
+    kg = synth.make_kg(args.config)
+    nq = args.queries or spec.n_queries
+    if world == 1:
+        qs = synth.config_queries(kg, args.config, nq)
+    else:  # weak scaling: each rank its own query batch of the same shape
+        qs = synth.make_queries(kg, nq, spec.n_central, spec.n_marginal, spec.k, spec.depth,
+                                2000 + args.config + 7919 * rank)
+    g = P.Graph(kg.n_nodes, kg.src, kg.dst, kg.label_class, kg.term_ptr, kg.postings, device=dev)
+    g.set_label_weights(0.5, kg.avg_hops)
+    g.set_batch_slots(min(nq, 1024))
+    cp, ct = P.Graph._csr(qs.central)
+    mp, mt = P.Graph._csr(qs.marginal)
+    d_cp, d_ct, d_mp, d_mt = [torch.from_numpy(x.view(np.int64) if x.dtype == np.uint64 else x.view(np.int32))
+                              .to(f"cuda:{dev}") for x in (cp, ct, mp, mt)]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")  # > 126 MB L2
+
+    def step_device():
+        g.search_batch_device(nq, d_cp.data_ptr(), d_ct.data_ptr(), d_mp.data_ptr(), d_mt.data_ptr(), qs.k, qs.depth)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+    # ---------------- timed region (device-resident inputs and results)
+    g.reset_stats()
+    g.set_profiling(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    with Clocks(dev) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            ev[i][0].record()
+            step_device()
+            ev[i][1].record()
+        torch.cuda.synchronize()
+    barrier()
+    g.set_profiling(False)
+    st = g.stats()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(step_ms)
+    if dist:
+        t = torch.tensor([tot_ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = nq * world * args.steps / (tot_ms / 1000.0)
+    res = g.fetch(nq, [len(c) for c in qs.central], [len(m) for m in qs.marginal])
+    relax = sum(r.stats["relax_central"] + r.stats["relax_marginal"] for r in res)
+    n_rpg = sum(len(r.rpgs) for r in res)
+
+    # ---------------- e2e through the host C-ABI (H2D of queries, D2H of results inside)
+    h2d = cp.nbytes + ct.nbytes + mp.nbytes + mt.nbytes
+    e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    d2h = 0
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        e2e_ev[i][0].record()
+        rr = g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)
+        e2e_ev[i][1].record()
+        d2h = sum(4 * (len(x.nodes) + len(x.vc)) + 4 * len(x.edge_ids) + 64 for r in rr for x in r.rpgs)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
+    if dist:
+        t = torch.tensor([e2e_ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = nq * world * args.steps / (e2e_ms / 1000.0)
+
+    # ---------------- single-query latency (one query in flight, host API incl. D2H)
+    lat = []
+    for i in range(min(args.latency_queries, nq)):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        g.search(qs.central[i], qs.marginal[i], qs.k, qs.depth)
+        b.record()
+        torch.cuda.synchronize()
+        lat.append(a.elapsed_time(b))
+    lat.sort()
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    peak, peak_src = _peaks()
+    achieved = (st["expand_bytes"] / 1e9) / (st["expand_ms"] / 1e3) if st["expand_ms"] > 0 else 0.0
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u8", "data": "synthetic",
+        "config": {"workload": _workload_name(args.config, spec), "queries_per_step_per_gpu": nq,
+                   "l2": "flushed between steps (256 MiB write)", "parallelism": f"query-sharded replicas x{world}",
+                   "graph_seed": 1000 + args.config, "query_seed": 2000 + args.config},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "kernel": "k_expand + k_expand_heavy (Alg. 1 expansion), CUDA events on the library stream",
+                     "peak_source": peak_src, "expand_share_of_step": st["expand_ms"] / tot_ms if tot_ms else None},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(st["kernel_launches"]),
+        "latency_ms": {"p50": lat[len(lat) // 2] if lat else None,
+                       "p99": lat[min(len(lat) - 1, int(0.99 * len(lat)))] if lat else None, "n": len(lat)},
+        "gteps": relax / (tot_ms / args.steps / 1000.0) / 1e9,
+        "relaxations_per_step": relax, "rpgs_per_step": n_rpg,
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu:
+        n = min(args.cpu_sample, nq)
+        dt, _ = oracle_sample(kg, qs, range(n))
+        line["cpu_baseline"] = {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": f"first {n} queries of the same batch, single-threaded oracle"}
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

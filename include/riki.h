@@ -1,0 +1,213 @@
+/*
+ * riki.h -- C-ABI of libriki.so, the B200 (sm_100a) hot path of RIKI radial-pattern
+ * keyword search (Yang & Tung, "Efficient Radial Pattern Keyword Search on Knowledge
+ * Graphs in Parallel", arXiv 2001.06770).  "P:n" cites PAPER.md line n; "R<n>" the
+ * readings listed in DESIGN.md §3.
+ *
+ * Conventions (all entry points)
+ *   - Return riki_status: 0 = RIKI_OK, < 0 = error.  Never throw, never abort; a
+ *     thread-local message is available from riki_last_error().
+ *   - Node ids are dense uint32 in [0, n_nodes); edge ids are the caller's indices into
+ *     the directed edge list given to riki_load_graph (multi-edges stay distinct, R24).
+ *   - "host" pointers are ordinary CPU memory, "device" pointers are CUDA global memory
+ *     on the graph's device.  Inputs are only read; the library copies what it keeps.
+ *   - There is no CPU fallback: every step of the search runs in CUDA kernels; without a
+ *     usable sm_100 device the calls return RIKI_ECUDA.
+ *   - Infinity for a hitting level is 0xFF; finite levels are <= depth <= 254 (R8).
+ */
+#ifndef RIKI_H
+#define RIKI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RIKI_OK = 0,
+    RIKI_EINVAL = -1,          /* bad argument (null pointer, id out of range, k == 0, ...)     */
+    RIKI_ENOMEM = -2,          /* device or host allocation failed / workspace overflow          */
+    RIKI_ECUDA = -3,           /* CUDA runtime error (message has the CUDA error string)         */
+    RIKI_EEMPTY_CENTRAL = -4,  /* C = empty set; Def. RPQ requires C != empty            */
+    RIKI_EUNRESOLVED = -5,     /* a query term has an empty posting list (message names it)      */
+    RIKI_ENOWEIGHTS = -6,      /* search before activation levels were set                       */
+    RIKI_EDEPTH = -7,          /* depth > 254                                                    */
+    RIKI_ENCCL = -8,           /* reserved for distributed mode                                  */
+    RIKI_ENOSYS = -9           /* not implemented in this build                                  */
+} riki_status;
+
+#define RIKI_MAX_TERMS 8       /* keywords per phase (central or marginal), T <= 8              */
+#define RIKI_MAX_DEPTH 254
+
+typedef struct riki_graph riki_graph;     /* opaque, device-resident, owned by the library */
+typedef struct riki_results riki_results; /* opaque, host-resident, owned by the library   */
+
+/* ---------------------------------------------------------------------------------------
+ * Graph residency (CSR "pre-stored in the main memory of ... a GPU").
+ * The caller's edge list is directed and ALREADY bidirected: one reverse edge per original
+ * triple.  label_class[e] identifies the edge's label class (label, inverse flag;
+ * R3) and is used only by riki_set_label_weights.  term_ptr/postings is the keyword ->
+ * node inverted index (replaces MongoDB; R28): the posting list of term t is
+ * postings[term_ptr[t] .. term_ptr[t+1]), sorted ascending, unique.  All inputs are host
+ * pointers and are copied; the caller keeps ownership.  n_edges must be < 2^32.
+ * Errors: RIKI_EINVAL (null/out of range ids, unsorted postings), RIKI_ENOMEM, RIKI_ECUDA.
+ * ------------------------------------------------------------------------------------- */
+riki_status riki_load_graph(int device, uint32_t n_nodes, uint64_t n_edges,
+                            const uint32_t *src, const uint32_t *dst, const uint32_t *label_class,
+                            uint32_t n_terms, const uint64_t *term_ptr, const uint32_t *postings,
+                            riki_graph **out);
+void riki_free_graph(riki_graph *g);
+
+/* ---------------------------------------------------------------------------------------
+ * Edge activation levels a_e.  Each setter computes a_e on the device and
+ * re-sorts every CSR row by activation (rows are stored activation-ascending so that the
+ * gate a_e <= l of Alg. 1 line 9 reads only a row prefix).  Not on the query path.
+ *
+ * riki_set_edge_weights: w01[n_edges] (host, fine weights already rescaled to [0,1],
+ *   P:194) -> a_e = Rounding(A - A(alpha-w)/alpha) if w <= alpha else
+ *   Rounding(A + A(w-alpha)/(1-alpha)) (Eq. 1-3, half-up rounding R1, fp64 in exactly that
+ *   operation order R5).  0 < alpha < 1, avg_hops > 0 (the raw average A, R4).
+ * riki_set_node_weights: w01[n_nodes] (host); node-weighted special case
+ *   a(f->n) = coarsen(w[n]) (north star "set_node_weights"; P:196 contrasts node weighting).
+ * riki_set_label_weights: computes the fine weights on the device from label classes,
+ *   w_ij = ln(#out-edges of v_i in class(e) + #in-edges of v_j in class(e)) (both
+ *   counts include e, R3), min-max rescaled (all 0 if max == min, R2), then Eq. 1-3.
+ * riki_set_activation_levels: a[n_edges] (host) given directly (exact control, tests).
+ * riki_get_activation_levels: copies a_e (by caller edge id) to host a[n_edges].
+ * Errors: RIKI_EINVAL (alpha/avg out of range, null), RIKI_ENOMEM, RIKI_ECUDA.
+ * ------------------------------------------------------------------------------------- */
+riki_status riki_set_edge_weights(riki_graph *g, const double *w01, double alpha, double avg_hops);
+riki_status riki_set_node_weights(riki_graph *g, const double *w01, double alpha, double avg_hops);
+riki_status riki_set_label_weights(riki_graph *g, double alpha, double avg_hops);
+riki_status riki_set_activation_levels(riki_graph *g, const uint8_t *a);
+riki_status riki_get_activation_levels(const riki_graph *g, uint8_t *a);
+
+/* ---------------------------------------------------------------------------------------
+ * Search parameters (defaults in brackets; riki_params_default fills them).
+ *   gamma      Eq. 6 weight [0.5, R22]
+ *   beam_w     beam width w of the first level [0 -> w = k]
+ *   beam_mode  0 = keep every CG identified by the terminating level (ties, R13) [0];
+ *              1 = truncate the candidate CGs to the first w by (S^c, v)
+ *   tie_break  0 = (S^r, S^c, v) ascending (R23) [0]; others RIKI_ENOSYS
+ *   ptc_mode   0 = filter PTC failures, RPG-wide endpoint-inclusive (R19) [0];
+ *              1 = keep failures, flagged ptc = 0
+ *   early_term 0 = exact bound (R21) [0]; 2 = none (exhaustive marginal run to depth)
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+    double gamma;
+    uint32_t beam_w;
+    int beam_mode;
+    int tie_break;
+    int ptc_mode;
+    int early_term;
+} riki_params;
+void riki_params_default(riki_params *p);
+
+/* ---------------------------------------------------------------------------------------
+ * Radial Pattern Query search (Def. RPQ, Def. RPKSP).
+ * central[n_central] / marginal[n_marginal] are TERM ids (host).  1 <= n_central <= 8,
+ * 0 <= n_marginal <= 8 (M = empty returns the top-k CGs).  k >= 1 results;
+ * depth = maximum Glevel D (<= 254; paper default 20).  Runs, on the device:
+ * central run (seed, level loop of enqueue / identification / Alg. 1 expansion with CF
+ * blocking, termination at >= w CGs) -> candidate CGs -> Alg. 2 recovery of each CG ->
+ * marginal run (fresh H, stop rule for |M| >= 2, attach, RPG recovery + PTC, exact early
+ * termination) -> top-k by (S^r, S^c, v).  p == NULL uses defaults.  cuda_stream == NULL
+ * uses the library's stream; otherwise a cudaStream_t on the graph's device.
+ * *out receives a host result set (count may be 0: success with no result).
+ * Errors: RIKI_EEMPTY_CENTRAL, RIKI_EUNRESOLVED, RIKI_ENOWEIGHTS, RIKI_EDEPTH, RIKI_EINVAL,
+ *         RIKI_ENOMEM (workspace overflow, message says which), RIKI_ECUDA.
+ * ------------------------------------------------------------------------------------- */
+riki_status riki_rpq_search(riki_graph *g, const uint32_t *central, uint32_t n_central,
+                            const uint32_t *marginal, uint32_t n_marginal, uint32_t k, uint32_t depth,
+                            const riki_params *p, void *cuda_stream, riki_results **out);
+
+/* Batch of independent queries (host arrays): query q has central terms
+ * c_terms[c_ptr[q] .. c_ptr[q+1]) and marginal terms m_terms[m_ptr[q] .. m_ptr[q+1]).
+ * Queries run concurrently on the device in level-synchronous lock-step.  out[q] receives
+ * query q's results (n_queries handles).  On error no handle is returned. */
+riki_status riki_rpq_search_batch(riki_graph *g, uint32_t n_queries,
+                                  const uint64_t *c_ptr, const uint32_t *c_terms,
+                                  const uint64_t *m_ptr, const uint32_t *m_terms,
+                                  uint32_t k, uint32_t depth, const riki_params *p,
+                                  riki_results **out);
+
+/* Device-resident batch (benchmark / pipeline path): identical computation, but the query
+ * arrays are DEVICE pointers and results stay on the device (no D2H); results are
+ * retrievable afterwards with riki_batch_fetch (which performs the D2H).  Returns after
+ * the work has been enqueued and completed on the library stream. */
+riki_status riki_rpq_search_batch_device(riki_graph *g, uint32_t n_queries,
+                                         const uint64_t *d_c_ptr, const uint32_t *d_c_terms,
+                                         const uint64_t *d_m_ptr, const uint32_t *d_m_terms,
+                                         uint32_t k, uint32_t depth, const riki_params *p);
+riki_status riki_batch_fetch(riki_graph *g, uint32_t n_queries, riki_results **out);
+
+/* One result RPG (CG when M = empty).  Pointers stay valid until riki_results_free. */
+typedef struct {
+    uint32_t central_node;     /* v~ (Def. CG)                                       */
+    uint32_t sc, sm;           /* S^c (Eq. 4) and S^m (Eq. 5); sm = 0 when M = empty        */
+    double score;              /* S^r (Eq. 6); = S^c when M = empty                          */
+    uint8_t ptc;               /* 1 = PTC holds (always 1 unless ptc_mode = 1)               */
+    uint32_t n_nodes; const uint32_t *nodes;     /* sorted node ids of G^r                   */
+    uint32_t n_edges; const uint64_t *edge_ids;  /* sorted caller edge ids, CG u G^m         */
+    uint32_t n_vc; const uint32_t *vc;           /* sorted V_C                       */
+    const uint8_t *cdist;      /* [n_central] h_c[v~][j] = D(c_j, v~)                      */
+    const uint8_t *mdist;      /* [n_marginal] D(m_i, V_C) (Def. distKeyword2NodeSet)       */
+} riki_rpg;
+
+uint32_t riki_results_count(const riki_results *r);
+riki_status riki_results_get(const riki_results *r, uint32_t i, riki_rpg *out);
+/* per-query statistics: terminating levels of the two runs (-1 = not run), number of
+ * candidate CGs, attached candidates, PTC rejects, (edge, keyword) relaxations per run */
+typedef struct {
+    int32_t L_central, L_marginal;
+    uint32_t n_candidates, n_attached, n_ptc_fail;
+    uint64_t relax_central, relax_marginal;
+} riki_query_stats;
+riki_status riki_results_stats(const riki_results *r, riki_query_stats *out);
+/* candidate CGs in (S^c, v) order (only when riki_set_debug(g, 1) was on for the search) */
+uint32_t riki_results_ncand(const riki_results *r);
+riki_status riki_results_cand(const riki_results *r, uint32_t i, uint32_t *v, uint32_t *sc);
+void riki_results_free(riki_results *r);
+
+/* ---------------------------------------------------------------------------------------
+ * Debug / parity boundary (minimum slice): one exploration run with no termination other
+ * than depth or an empty frontier.  terms[n_terms] term ids (1..8); block_mode 0 = none,
+ * 1 = central CF (node identified when reached by all terms),
+ * 2 = marginal stop rule (only when n_terms >= 2, R11).  H_out (host, V*n_terms
+ * bytes, node-major) receives h; block_out (host, V bytes) the level at which the node was
+ * blocked (0xFF if never; closed form R10).  relax_out (may be NULL) the relaxation count.
+ * ------------------------------------------------------------------------------------- */
+riki_status riki_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t n_terms, uint32_t depth,
+                                int block_mode, uint8_t *H_out, uint8_t *block_out, uint64_t *relax_out,
+                                int32_t *L_end_out);
+
+/* ---------------------------------------------------------------------------------------
+ * Instrumentation: when enabled, every expansion launch is bracketed by CUDA events on the
+ * launching stream and its algorithmic bytes accumulated.
+ * ------------------------------------------------------------------------------------- */
+typedef struct {
+    uint64_t expand_launches;      /* expansion kernel launches (light + heavy)            */
+    double expand_ms;              /* summed CUDA-event time of those launches             */
+    uint64_t expand_bytes;         /* algorithmic bytes of those launches                  */
+    uint64_t relaxations;          /* (edge, keyword) relaxations                          */
+    uint64_t kernel_launches;      /* all library kernel launches                          */
+    uint64_t queries;              /* queries completed                                    */
+} riki_stats;
+riki_status riki_set_profiling(riki_graph *g, int on);
+riki_status riki_get_stats(const riki_graph *g, riki_stats *out);
+riki_status riki_reset_stats(riki_graph *g);
+riki_status riki_set_debug(riki_graph *g, int on);
+/* Batch slots (queries in flight per launch); 0 = automatic from free device memory. */
+riki_status riki_set_batch_slots(riki_graph *g, uint32_t slots);
+/* device memory footprint of the resident graph and of the search workspace (bytes) */
+riki_status riki_memory_footprint(const riki_graph *g, uint64_t *graph_bytes, uint64_t *workspace_bytes);
+
+const char *riki_last_error(void);
+const char *riki_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RIKI_H */

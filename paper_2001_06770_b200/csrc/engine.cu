@@ -1,0 +1,1717 @@
+// engine.cu -- RIKI query engine on sm_100a: batched, level-synchronous two-run search.
+//
+//   run 1 (central keywords) and run 2 (marginal keywords), each:
+//     seed -> per level: [attach + decide (run 2)] -> plan/terminate
+//      -> Alg. 1 expansion with CF blocking
+//   between the runs: candidate CGs (R13) sorted by (S^c, v) and recovered (Alg. 2,
+//   P:503-561) by one CTA each; during run 2 every newly attached candidate is recovered
+//   as an RPG and PTC-checked (Def. RPG, R19); finally the top-k by
+//   (S^r, S^c, v) (Eq. 6, R23) are sorted and packed for the host.
+//
+// All queries of a batch advance in lock-step (one level per iteration), so every launch
+// covers the frontiers of all in-flight queries.  H rows are one 32- or 64-bit word per
+// node (byte = hitting level, 0xFF = inf); a relaxation is one atomicAnd that both writes
+// l+1 into every still-infinite selected byte and tells the caller whether it was the
+// first writer of the row at this level (enqueue) and whether it completed the row
+// (identification at level l+1, R10).  Lock-free by Theorem lockfree.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+typedef unsigned __int128 u128;
+
+namespace {
+
+constexpr uint32_t MAX_SLOTS = 1024;
+constexpr uint32_t HEAVY = 256;  // longer active ranges are split into CHUNK-edge work items
+constexpr uint32_t CHUNK = 256;
+constexpr uint32_t EMPTY = 0xFFFFFFFFu;
+// recovery fast path (shared memory) capacities
+constexpr uint32_t CAP_U = 4096, CAP_K = 4096, CAP_Q = 4096, CAP_E = 8192;
+constexpr uint32_t SORT_SMEM = 8192;  // u32 keys sorted in shared memory
+
+enum Ctr { C_NHEAVY = 0, C_NNEWATT, C_NOVF, C_ACTIVE, C_TOTAL, C_NCAND_TOTAL, C_NCTR = 16 };
+enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_NPROF = 8 };
+enum Err { E_CAND = 1, E_HEAVY = 2, E_ARENA = 4, E_EXTRACT = 8, E_OUT = 16, E_UNRESOLVED = 32 };
+
+struct SlotState {
+    uint32_t T[2];
+    uint32_t term[2][RIKI_MAX_TERMS];
+    uint32_t k, w, depth;
+    uint32_t beam_mode, ptc_mode, early_term;
+    double gamma;
+    uint32_t in_phase, level;
+    uint32_t nq[2];
+    uint32_t blocking, collect, stop_m;
+    uint32_t ncand, ncand_kept, n_extract;
+    int32_t L_end[2];
+    unsigned long long relax[2];
+    uint32_t n_attached, n_ptc_fail, nR, nres;
+    uint32_t err, active;
+};
+
+struct Cand {
+    uint32_t v, sc;
+    uint32_t nodes_off, n_nodes, edges_off, n_edges, vc_off, n_vc;
+    uint32_t attached, ptc, sm, flags;
+    double sr;
+    uint8_t mdist[RIKI_MAX_TERMS];
+};
+
+struct OutHdr {
+    uint32_t central, sc, sm, ptc;
+    double score;
+    uint32_t n_nodes, nodes_off, n_edges, edges_off, n_vc, vc_off;
+    uint8_t cdist[RIKI_MAX_TERMS], mdist[RIKI_MAX_TERMS];
+};
+
+// Device view of the workspace (passed by value to every kernel).
+struct WsDev {
+    SlotState *st;
+    uint32_t nslots, V, W, capc, kmax;
+    uint8_t *H[2];
+    uint32_t rb[2];
+    uint32_t *q, *bm;
+    uint64_t *ck;
+    Cand *cd;
+    u128 *rk;
+    uint32_t *offs, *coffs;
+    uint4 *heavy;
+    uint32_t heavy_cap;
+    uint32_t *ctr;
+    unsigned long long *prof;
+    uint32_t *arena;
+    unsigned long long *arena_used, arena_cap;
+    uint2 *newatt, *ovf;
+    uint32_t ovf_cap;
+    uint32_t *big;
+    unsigned long long big_words;
+    OutHdr *hdr;
+    uint32_t *resid;
+    uint32_t *out;
+    unsigned long long *out_used, out_cap;
+
+    __device__ __forceinline__ uint32_t *Q(uint32_t s, uint32_t b) const { return q + ((size_t)s * 2 + b) * V; }
+    __device__ __forceinline__ uint32_t *BM(uint32_t s, uint32_t b) const { return bm + ((size_t)s * 2 + b) * W; }
+    template <class RowT> __device__ __forceinline__ RowT *Hs(int ph, uint32_t s) const {
+        return (RowT *)(H[ph] + (size_t)s * V * rb[ph]);
+    }
+    __device__ __forceinline__ uint64_t *CK(uint32_t s) const { return ck + (size_t)s * capc; }
+    __device__ __forceinline__ Cand *CD(uint32_t s) const { return cd + (size_t)s * capc; }
+    __device__ __forceinline__ u128 *RK(uint32_t s) const { return rk + (size_t)s * capc; }
+};
+
+template <class RowT> __device__ __forceinline__ RowT used_mask(uint32_t T) {
+    return T >= sizeof(RowT) ? (RowT)~(RowT)0 : (((RowT)1 << (8 * T)) - 1);
+}
+template <class RowT> __device__ __forceinline__ RowT vmin(RowT a, RowT b);
+template <> __device__ __forceinline__ uint32_t vmin<uint32_t>(uint32_t a, uint32_t b) { return __vminu4(a, b); }
+template <> __device__ __forceinline__ uint64_t vmin<uint64_t>(uint64_t a, uint64_t b) {
+    return (uint64_t)__vminu4((uint32_t)(a >> 32), (uint32_t)(b >> 32)) << 32 |
+           __vminu4((uint32_t)a, (uint32_t)b);
+}
+template <class RowT> __device__ __forceinline__ RowT shfl(RowT v, int src) { return __shfl_sync(FULLMASK, v, src); }
+
+// Eq. 6 in the oracle's exact operation order (R5): gamma*sc + (1-gamma)*sm.
+__device__ __forceinline__ double rpg_score(double g, uint32_t sc, uint32_t sm) {
+    return __dadd_rn(__dmul_rn(g, (double)sc), __dmul_rn(__dsub_rn(1.0, g), (double)sm));
+}
+__device__ __forceinline__ u128 rkey(double sr, uint32_t sc, uint32_t v) {
+    return (u128)(unsigned long long)__double_as_longlong(sr) << 64 | (u128)sc << 32 | v;
+}
+
+__device__ __forceinline__ uint32_t find_slot(const uint32_t *offs, uint32_t n, uint32_t item) {
+    // largest s with offs[s] <= item (offs non-decreasing, offs[n] = total)
+    uint32_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+        uint32_t m = (lo + hi) >> 1;
+        if (offs[m] <= item) lo = m; else hi = m;
+    }
+    return lo;
+}
+
+// ====================================================================== run setup
+__global__ void k_phase_begin(WsDev w, int ph, int hitting_mode) {
+    uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= w.nslots) return;
+    SlotState &st = w.st[s];
+    uint32_t T = st.T[ph];
+    st.in_phase = st.active && T > 0 && !st.err;
+    st.level = 0;
+    st.nq[0] = st.nq[1] = 0;
+    st.stop_m = 0;
+    st.L_end[ph] = -1;
+    if (hitting_mode >= 0) {  // debug boundary: 0 none, 1 central CF, 2 marginal stop rule
+        st.blocking = hitting_mode == 1 || (hitting_mode == 2 && T >= 2);
+        st.collect = 0;
+    } else if (ph == 0) {
+        st.blocking = 1;  // CF: "stop expanding a node once it is identified"
+        st.collect = 1;
+        st.ncand = 0;
+    } else {
+        st.blocking = T >= 2;  // stop rule P:373, disabled for |M| = 1 (R11)
+        st.collect = 0;
+        st.nR = 0;
+        st.n_attached = 0;
+        st.n_ptc_fail = 0;
+    }
+}
+
+// H rows: used bytes = 0xFF (inf), padding bytes = 0 (P:344 static initialisation)
+template <class RowT> __global__ void k_fill_H(WsDev w, int ph) {
+    uint32_t s = blockIdx.y;
+    if (!w.st[s].in_phase) return;
+    RowT pat = used_mask<RowT>(w.st[s].T[ph]);
+    RowT *H = w.Hs<RowT>(ph, s);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < w.V; i += gridDim.x * blockDim.x) H[i] = pat;
+}
+
+// Seeds: h = 0 at keyword nodes, all keyword nodes are frontiers; level-0
+// identification of nodes holding every phase keyword (score 0).
+template <class RowT> __global__ void k_seed(GraphDev g, WsDev w, int ph) {
+    uint32_t s = blockIdx.y;
+    SlotState &st = w.st[s];
+    if (!st.in_phase) return;
+    RowT *H = w.Hs<RowT>(ph, s);
+    uint32_t T = st.T[ph];
+    for (uint32_t j = 0; j < T; j++) {
+        uint32_t t = st.term[ph][j];
+        uint64_t b = g.tptr[t], e = g.tptr[t + 1];
+        for (uint64_t i = b + blockIdx.x * blockDim.x + threadIdx.x; i < e; i += (uint64_t)gridDim.x * blockDim.x) {
+            uint32_t v = g.post[i];
+            RowT andm = ~((RowT)0xFF << (8 * j));
+            RowT old = Row<RowT>::atomic_and(H + v, andm);
+            RowT nw = old & andm;
+            uint32_t bit = 1u << (v & 31);
+            uint32_t ob = atomicOr(w.BM(s, 0) + (v >> 5), bit);
+            if (!(ob & bit)) {
+                uint32_t p = atomicAdd(&st.nq[0], 1u);
+                w.Q(s, 0)[p] = v;
+            }
+            if (st.collect && Row<RowT>::eq(nw, Row<RowT>::splat(0xFF)) == 0 &&
+                Row<RowT>::byte(old, j) == 0xFF) {
+                uint32_t p = atomicAdd(&st.ncand, 1u);
+                if (p < w.capc) w.CK(s)[p] = (uint64_t)v;  // score 0
+                else atomicOr(&st.err, (uint32_t)E_CAND);
+            }
+        }
+    }
+}
+
+// ====================================================================== plan / terminate
+// One block: per-slot termination check for level l, then an exclusive scan of the
+// frontier sizes of the slots that expand (flattened work index for k_expand).
+__global__ void k_plan(WsDev w, int ph, uint32_t l) {
+    __shared__ uint32_t sc[MAX_SLOTS];
+    __shared__ uint32_t nact;
+    uint32_t s = threadIdx.x;
+    if (s == 0) nact = 0;
+    __syncthreads();
+    uint32_t items = 0;
+    if (s < w.nslots) {
+        SlotState &st = w.st[s];
+        if (st.in_phase) {
+            st.level = l;
+            uint32_t cur = l & 1;
+            bool stop;
+            if (ph == 0)  // P:362 ">= w CGs", depth bound (R8), empty frontier
+                stop = st.ncand >= st.w || l >= st.depth || st.nq[cur] == 0;
+            else
+                stop = st.stop_m;
+            if (stop || st.err) {
+                st.in_phase = 0;
+                st.L_end[ph] = (int32_t)l;
+            } else {
+                items = st.nq[cur];
+                st.nq[cur ^ 1] = 0;
+                atomicAdd(&nact, 1u);
+            }
+        }
+    }
+    // block exclusive scan (Hillis-Steele) over MAX_SLOTS
+    sc[s] = items;
+    __syncthreads();
+    for (uint32_t o = 1; o < MAX_SLOTS; o <<= 1) {
+        uint32_t v = s >= o ? sc[s - o] : 0;
+        __syncthreads();
+        sc[s] += v;
+        __syncthreads();
+    }
+    if (s < w.nslots) w.offs[s] = sc[s] - items;
+    if (s == 0) {
+        w.offs[w.nslots] = sc[MAX_SLOTS - 1];
+        w.ctr[C_ACTIVE] = nact;
+        w.ctr[C_TOTAL] = sc[MAX_SLOTS - 1];
+        w.ctr[C_NHEAVY] = 0;
+    }
+}
+
+// ====================================================================== expansion (Alg. 1)
+template <class RowT> struct Relax {
+    bool enq;    // first writer of this row at this level -> next frontier
+    bool ident;  // completed the row -> identified at level l+1
+    int cells;   // cells turned from inf to l+1 by this thread
+};
+
+// Relaxation of edge (f -> n) for the byte-columns in `mask` at level l (Alg. 1 lines 12-17).
+template <class RowT> __device__ __forceinline__ Relax<RowT> relax(RowT *H, uint32_t n, RowT mask, uint32_t l) {
+    typedef Row<RowT> R;
+    Relax<RowT> r{false, false, 0};
+    const RowT FF = R::splat(0xFF);
+    RowT hn = R::load(H + n);
+    RowT need = mask & R::eq(hn, FF);
+    if (!need) return r;
+    RowT andm = ~need | (need & R::splat(l + 1));
+    RowT old = R::atomic_and(H + n, andm);
+    RowT changed = need & R::eq(old, FF);
+    if (!changed) return r;
+    r.cells = R::ones(changed);
+    r.enq = R::eq(old, R::splat(l + 1)) == 0;  // no cell of n was written at this level before
+    r.ident = R::eq(old & andm, FF) == 0;      // this write completed the row
+    return r;
+}
+
+// Enqueue n into the next frontier of slot s: bit-packed frontier dedups (P:347 shared F).
+__device__ __forceinline__ void frontier_push(const WsDev &w, bool want, uint32_t s, uint32_t n, uint32_t nxt) {
+    bool app = false;
+    if (want) {
+        uint32_t bit = 1u << (n & 31);
+        uint32_t ob = atomicOr(w.BM(s, nxt) + (n >> 5), bit);
+        app = !(ob & bit);
+    }
+    uint32_t pos = warp_append(app, s, &w.st[0].nq[nxt], sizeof(SlotState) / 4);
+    if (app) w.Q(s, nxt)[pos] = n;
+}
+
+__device__ __forceinline__ void cand_push(const WsDev &w, bool want, uint32_t s, uint32_t n, uint32_t level) {
+    uint32_t pos = warp_append(want, s, &w.st[0].ncand, sizeof(SlotState) / 4);
+    if (want) {
+        if (pos < w.capc) w.CK(s)[pos] = (uint64_t)level << 32 | n;
+        else atomicOr(&w.st[s].err, (uint32_t)E_CAND);
+    }
+}
+
+__device__ __forceinline__ uint32_t upper_bound_act(const uint8_t *act, uint32_t lo, uint32_t hi, uint32_t l) {
+    while (lo < hi) {  // first index with act > l
+        uint32_t m = (lo + hi) >> 1;
+        if (act[m] <= l) lo = m + 1; else hi = m;
+    }
+    return lo;
+}
+__device__ __forceinline__ uint32_t lower_bound_act(const uint8_t *act, uint32_t lo, uint32_t hi, uint32_t l) {
+    while (lo < hi) {  // first index with act >= l
+        uint32_t m = (lo + hi) >> 1;
+        if (act[m] < l) lo = m + 1; else hi = m;
+    }
+    return lo;
+}
+
+// Work item = one frontier node of one slot.  Each warp takes 32 items: lane i does the
+// per-node part (row bounds, CF check, retention, activation range by binary search in the
+// activation-sorted row), then the warp walks the concatenated active ranges edge-parallel.
+template <class RowT>
+__global__ void __launch_bounds__(256) k_expand(GraphDev g, WsDev w, int ph, uint32_t l) {
+    typedef Row<RowT> R;
+    __shared__ uint32_t s_offs[MAX_SLOTS + 1];
+    __shared__ uint32_t s_info[MAX_SLOTS];
+    const uint32_t ns = w.nslots;
+    for (uint32_t i = threadIdx.x; i <= ns; i += blockDim.x) s_offs[i] = w.offs[i];
+    for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {
+        const SlotState &st = w.st[i];
+        s_info[i] = st.blocking | st.collect << 1 | st.T[ph] << 8;
+    }
+    __syncthreads();
+    const uint32_t total = s_offs[ns];
+    const uint32_t lane = lane_id();
+    const uint32_t cur = l & 1, nxt = cur ^ 1;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    const RowT L = R::splat(l);
+    unsigned long long p_items = 0, p_edges = 0, p_cells = 0, p_enq = 0;
+
+    for (uint32_t base = gw * 32; base < total; base += nw * 32) {
+        uint32_t item = base + lane;
+        bool valid = item < total;
+        uint32_t s = 0, f = 0, lo = 0, len = 0, relaxn = 0;
+        RowT newc = 0, oldc = 0;
+        bool retain = false;
+        if (valid) {
+            s = find_slot(s_offs, ns, item);
+            uint32_t info = s_info[s];
+            f = w.Q(s, cur)[item - s_offs[s]];
+            RowT *H = w.Hs<RowT>(ph, s);
+            RowT Rf = R::load(H + f);
+            w.BM(s, cur)[f >> 5] = 0;  // every set bit of this word is a node of Q_l (cleared here)
+            bool blocked = (info & 1) && R::le(Rf, L) == (RowT)~(RowT)0;  // CF: row complete, max <= l
+            if (!blocked) {
+                RowT used = used_mask<RowT>(info >> 8);
+                newc = R::eq(Rf, L) & used;   // reached at level l (or seeds at l = 0)
+                oldc = R::lt(Rf, L) & used;   // reached earlier: only edges with a == l are due now
+                uint32_t rb = g.row[f], re = g.row[f + 1];
+                if (re > rb && (newc | oldc)) {
+                    retain = g.act[re - 1] > l;  // Alg. 1 lines 9-11: some a_fn > l keeps f a frontier
+                    uint32_t hi = upper_bound_act(g.act, rb, re, l);
+                    uint32_t eqlo = oldc ? lower_bound_act(g.act, rb, hi, l) : hi;
+                    lo = newc ? rb : eqlo;
+                    len = hi - lo;
+                    relaxn = (hi - rb) * R::ones(newc) + (hi - eqlo) * R::ones(oldc);
+                    if (len > HEAVY) {
+                        uint32_t nch = (len + CHUNK - 1) / CHUNK;
+                        uint32_t p = atomicAdd(&w.ctr[C_NHEAVY], nch);
+                        if (p + nch <= w.heavy_cap) {
+                            for (uint32_t c = 0; c < nch; c++)
+                                w.heavy[p + c] = make_uint4(s, f, lo + c * CHUNK, min(lo + (c + 1) * CHUNK, hi));
+                        } else {
+                            atomicOr(&w.st[s].err, (uint32_t)E_HEAVY);
+                        }
+                        p_edges += len;
+                        len = 0;
+                    }
+                }
+            }
+            p_items++;
+        }
+        // relaxation count per slot (aggregated)
+        {
+            uint32_t vm = __ballot_sync(FULLMASK, valid);
+            if (valid) {
+                uint32_t peers = __match_any_sync(vm, s);
+                uint32_t sum = __reduce_add_sync(peers, relaxn);
+                if (lane == __ffs(peers) - 1 && sum) atomicAdd(&w.st[s].relax[ph], (unsigned long long)sum);
+            }
+        }
+        frontier_push(w, retain, s, f, nxt);
+        p_enq += retain;
+        // edge-parallel walk over the 32 active ranges
+        uint32_t incl = warp_incl_scan(len);
+        uint32_t tot = __shfl_sync(FULLMASK, incl, 31);
+        uint32_t excl = incl - len;
+        p_edges += len;
+        for (uint32_t eb = 0; eb < tot; eb += 32) {
+            uint32_t idx = eb + lane;
+            bool ev = idx < tot;
+            // owner lane: largest i with excl_i <= idx
+            uint32_t own = 0;
+#pragma unroll
+            for (uint32_t step = 16; step > 0; step >>= 1) {
+                uint32_t cand = own + step;
+                uint32_t ex = __shfl_sync(FULLMASK, excl, cand);
+                if (ex <= idx) own = cand;
+            }
+            uint32_t o_lo = __shfl_sync(FULLMASK, lo, own);
+            uint32_t o_ex = __shfl_sync(FULLMASK, excl, own);
+            uint32_t o_s = __shfl_sync(FULLMASK, s, own);
+            RowT o_new = shfl(newc, own), o_old = shfl(oldc, own);
+            Relax<RowT> r{false, false, 0};
+            uint32_t n = 0;
+            if (ev) {
+                uint32_t e = o_lo + (idx - o_ex);
+                n = g.col[e];
+                uint32_t a = g.act[e];
+                RowT mask = o_new | (a == l ? o_old : (RowT)0);
+                r = relax<RowT>(w.Hs<RowT>(ph, o_s), n, mask, l);
+                p_cells += r.cells;
+                p_enq += r.enq;
+            }
+            frontier_push(w, r.enq, o_s, n, nxt);
+            bool id = r.ident && ((s_info[ev ? o_s : 0] >> 1) & 1);
+            cand_push(w, id, o_s, n, l + 1);
+        }
+    }
+    p_items = warp_sum(p_items);
+    p_edges = warp_sum(p_edges);
+    p_cells = warp_sum(p_cells);
+    p_enq = warp_sum(p_enq);
+    if (lane == 0 && (p_items | p_edges)) {
+        atomicAdd(&w.prof[P_ITEMS], p_items);
+        atomicAdd(&w.prof[P_EDGES], p_edges);
+        atomicAdd(&w.prof[P_NEWCELLS], p_cells);
+        atomicAdd(&w.prof[P_ENQ], p_enq);
+    }
+}
+
+// Heavy ranges (hub rows): one warp per CHUNK-edge piece.
+template <class RowT> __global__ void __launch_bounds__(256) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l) {
+    typedef Row<RowT> R;
+    const uint32_t lane = lane_id();
+    const uint32_t nxt = (l & 1) ^ 1;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    uint32_t nh = min(w.ctr[C_NHEAVY], w.heavy_cap);
+    const RowT L = R::splat(l);
+    unsigned long long p_cells = 0, p_enq = 0;
+    for (uint32_t it = gw; it < nh; it += nw) {
+        uint4 h = w.heavy[it];
+        uint32_t s = h.x;
+        const SlotState &st = w.st[s];
+        RowT used = used_mask<RowT>(st.T[ph]);
+        RowT *H = w.Hs<RowT>(ph, s);
+        RowT Rf = R::load(H + h.y);  // values <= l are final; concurrent l+1 writes don't change the masks
+        RowT newc = R::eq(Rf, L) & used, oldc = R::lt(Rf, L) & used;
+        bool collect = st.collect;
+        for (uint32_t e0 = h.z; e0 < h.w; e0 += 32) {
+            uint32_t e = e0 + lane;
+            Relax<RowT> r{false, false, 0};
+            uint32_t n = 0;
+            if (e < h.w) {
+                n = g.col[e];
+                uint32_t a = g.act[e];
+                RowT mask = newc | (a == l ? oldc : (RowT)0);
+                r = relax<RowT>(H, n, mask, l);
+                p_cells += r.cells;
+                p_enq += r.enq;
+            }
+            frontier_push(w, r.enq, s, n, nxt);
+            cand_push(w, r.ident && collect, s, n, l + 1);
+        }
+    }
+    p_cells = warp_sum(p_cells);
+    p_enq = warp_sum(p_enq);
+    if (lane == 0 && (p_cells | p_enq)) {
+        atomicAdd(&w.prof[P_NEWCELLS], p_cells);
+        atomicAdd(&w.prof[P_ENQ], p_enq);
+    }
+}
+
+// Clear the bits of the last (unexpanded) frontier so the bitmaps are zero for reuse.
+__global__ void k_clear_bm(WsDev w, int ph) {
+    uint32_t s = blockIdx.y;
+    const SlotState &st = w.st[s];
+    if (st.L_end[ph] < 0) return;
+    uint32_t b = (uint32_t)st.L_end[ph] & 1;
+    uint32_t n = st.nq[b];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        w.BM(s, b)[w.Q(s, b)[i] >> 5] = 0;
+}
+
+// ====================================================================== candidates
+__device__ void cta_sort_u64(uint64_t *keys, uint32_t n, uint64_t *smem, uint32_t smem_cap) {
+    if (n < 2) return;
+    if (next_pow2(n) <= smem_cap) {
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) smem[i] = keys[i];
+        __syncthreads();
+        cta_bitonic_sort(smem, n);
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) keys[i] = smem[i];
+        __syncthreads();
+    } else {
+        cta_bitonic_sort(keys, n);  // global buffer has capacity next_pow2(n) (capc is a power of 2)
+    }
+}
+
+// Candidate CGs: all CGs identified by the terminating level, ties kept (R13), ordered
+// by (S^c, v); beam_mode 1 truncates to the first w.
+__global__ void k_cand_sort(WsDev w) {
+    extern __shared__ uint64_t sm64[];
+    uint32_t s = blockIdx.x;
+    SlotState &st = w.st[s];
+    if (!st.active || st.err) {
+        if (threadIdx.x == 0) st.ncand_kept = st.n_extract = 0;
+        return;
+    }
+    uint32_t n = min(st.ncand, w.capc);
+    cta_sort_u64(w.CK(s), n, sm64, 4096);
+    uint32_t kept = st.beam_mode == 1 ? min(n, st.w) : n;
+    uint32_t nex = st.T[1] == 0 ? min(kept, st.k) : kept;
+    for (uint32_t i = threadIdx.x; i < nex; i += blockDim.x) {
+        uint64_t key = w.CK(s)[i];
+        Cand c;
+        memset(&c, 0, sizeof(c));
+        c.v = (uint32_t)key;
+        c.sc = (uint32_t)(key >> 32);
+        c.sr = (double)c.sc;
+        c.ptc = 1;
+        w.CD(s)[i] = c;
+    }
+    if (threadIdx.x == 0) {
+        st.ncand_kept = kept;
+        st.n_extract = nex;
+    }
+}
+
+__global__ void k_scan_cands(WsDev w) {
+    __shared__ uint32_t sc[MAX_SLOTS];
+    uint32_t s = threadIdx.x;
+    uint32_t v = s < w.nslots ? w.st[s].n_extract : 0;
+    sc[s] = v;
+    __syncthreads();
+    for (uint32_t o = 1; o < MAX_SLOTS; o <<= 1) {
+        uint32_t t = s >= o ? sc[s - o] : 0;
+        __syncthreads();
+        sc[s] += t;
+        __syncthreads();
+    }
+    if (s < w.nslots) w.coffs[s] = sc[s] - v;
+    if (s == 0) {
+        w.coffs[w.nslots] = sc[MAX_SLOTS - 1];
+        w.ctr[C_NCAND_TOTAL] = sc[MAX_SLOTS - 1];
+        w.ctr[C_NOVF] = 0;
+    }
+}
+
+// ====================================================================== recovery (Alg. 2)
+struct ExBuf {
+    uint32_t *hu, *hk, *queue, *edges, *uf;
+    uint8_t *flag;
+    uint32_t cap_u, cap_k, cap_q, cap_e;
+};
+struct ExShared {
+    uint32_t qtail, nedges, nnodes, ovf;
+    uint32_t cnt, off, off2, mnr, mxr, nx, xvc, pass;
+};
+
+__device__ __forceinline__ void hs_clear(uint32_t *h, uint32_t cap) {
+    for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) h[i] = EMPTY;
+}
+
+// Reverse BFS for keyword column j (Alg. 2 lines 4-10) over the in-CSR.  Edge (n -> q) is
+// recovered iff h_nj finite, h_qj = max(h_nj, a) + 1 (Lemma recover) and
+// max(h_nj, a) < block[n] (n really expanded over it, R16); n is continued from iff
+// h_nj != 0 and not yet visited (R17).  In-rows are activation-sorted, so a row is cut
+// at the first a > h_qj - 1.  queue[0..nsrc) holds the sources (already in hk and hu).
+template <class RowT>
+__device__ void bfs_column(const GraphDev &g, const RowT *H, bool blocking, int j, uint32_t nsrc, const ExBuf &b,
+                           ExShared &sh) {
+    typedef Row<RowT> R;
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    HashSet hu{b.hu, b.cap_u}, hk{b.hk, b.cap_k};
+    uint32_t head = 0, tail = nsrc;
+    while (head < tail) {
+        for (uint32_t it = head + warp; it < tail; it += nw) {
+            uint32_t q = b.queue[it];
+            uint32_t hq = R::byte(R::load(H + q), j);
+            if (hq == 0 || hq == 0xFF) continue;
+            uint32_t rb = g.irow[q], re = g.irow[q + 1];
+            for (uint32_t k0 = rb; k0 < re; k0 += 32) {
+                uint32_t k = k0 + lane;
+                uint32_t a = k < re ? g.iact[k] : 0xFFu;
+                if (__shfl_sync(FULLMASK, a, 0) > hq - 1) break;
+                bool ok = false;
+                uint32_t n = 0, hn = 0xFF;
+                if (a <= hq - 1) {
+                    n = g.isrc[k];
+                    RowT Rn = R::load(H + n);
+                    hn = R::byte(Rn, j);
+                    if (hn != 0xFF) {
+                        uint32_t Lr = max(hn, a);
+                        if (Lr + 1 == hq) {
+                            uint32_t blk = 0xFF;
+                            if (blocking && R::eq(Rn, R::splat(0xFF)) == 0) blk = R::maxb(Rn);
+                            ok = Lr < blk;
+                        }
+                    }
+                }
+                if (ok) {
+                    uint32_t pos = atomicAdd(&sh.nedges, 1u);
+                    if (pos < b.cap_e) b.edges[pos] = g.ieid[k]; else sh.ovf = 1;
+                    int r = hu.insert(n);
+                    if (r < 0) sh.ovf = 1; else if (r == 1) atomicAdd(&sh.nnodes, 1u);
+                    if (hn != 0) {
+                        int r2 = hk.insert(n);
+                        if (r2 < 0) sh.ovf = 1;
+                        else if (r2 == 1) {
+                            uint32_t p = atomicAdd(&sh.qtail, 1u);
+                            if (p < b.cap_q) b.queue[p] = n; else sh.ovf = 1;
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        head = tail;
+        tail = min(sh.qtail, b.cap_q);
+        bool stop = sh.ovf;
+        __syncthreads();
+        if (stop) break;
+    }
+}
+
+__device__ __forceinline__ uint32_t arena_alloc(const WsDev &w, uint32_t words, uint32_t s) {
+    unsigned long long p = atomicAdd(w.arena_used, (unsigned long long)words);
+    if (p + words > w.arena_cap) {
+        atomicOr(&w.st[s].err, (uint32_t)E_ARENA);
+        return EMPTY;
+    }
+    return (uint32_t)p;
+}
+
+// CG of candidate (s, c): union over central keywords of the recovered SP(c_j, v~).
+// Writes nodes, edge ids and V_C (nodes holding a central keyword) to the arena.
+template <class RowC> __device__ void extract_cg(const GraphDev &g, const WsDev &w, uint32_t s, uint32_t c,
+                                                 const ExBuf &b, ExShared &sh, bool *overflow) {
+    typedef Row<RowC> R;
+    const SlotState &st = w.st[s];
+    Cand &cd = w.CD(s)[c];
+    const RowC *H = w.Hs<RowC>(0, s);
+    uint32_t T = st.T[0];
+    hs_clear(b.hu, b.cap_u);
+    if (threadIdx.x == 0) { sh.nedges = 0; sh.nnodes = 0; sh.ovf = 0; }
+    __syncthreads();
+    if (threadIdx.x == 0) { HashSet{b.hu, b.cap_u}.insert(cd.v); sh.nnodes = 1; }
+    for (uint32_t j = 0; j < T; j++) {
+        hs_clear(b.hk, b.cap_k);
+        __syncthreads();
+        if (threadIdx.x == 0) { HashSet{b.hk, b.cap_k}.insert(cd.v); b.queue[0] = cd.v; sh.qtail = 1; }
+        __syncthreads();
+        bfs_column<RowC>(g, H, true, j, 1, b, sh);
+        __syncthreads();
+        if (sh.ovf) break;
+    }
+    __syncthreads();
+    if (sh.ovf) { *overflow = true; return; }
+    *overflow = false;
+    // V_C count
+    RowC used = used_mask<RowC>(T);
+    if (threadIdx.x == 0) sh.cnt = 0;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < b.cap_u; i += blockDim.x) {
+        uint32_t v = b.hu[i];
+        if (v != EMPTY && (R::eq(R::load(H + v), 0) & used)) atomicAdd(&sh.cnt, 1u);
+    }
+    __syncthreads();
+    uint32_t nn = sh.nnodes, ne = min(sh.nedges, b.cap_e), nvc = sh.cnt;
+    if (threadIdx.x == 0) {
+        sh.off = arena_alloc(w, nn + ne + nvc, s);
+        sh.nnodes = 0;
+        sh.cnt = 0;
+    }
+    __syncthreads();
+    uint32_t off = sh.off;
+    if (off == EMPTY) return;
+    for (uint32_t i = threadIdx.x; i < b.cap_u; i += blockDim.x) {
+        uint32_t v = b.hu[i];
+        if (v == EMPTY) continue;
+        uint32_t p = atomicAdd(&sh.nnodes, 1u);
+        w.arena[off + p] = v;
+        if (R::eq(R::load(H + v), 0) & used) {
+            uint32_t pv = atomicAdd(&sh.cnt, 1u);
+            w.arena[off + nn + ne + pv] = v;
+        }
+    }
+    for (uint32_t i = threadIdx.x; i < ne; i += blockDim.x) w.arena[off + nn + i] = b.edges[i];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        cd.nodes_off = off; cd.n_nodes = nn;
+        cd.edges_off = off + nn; cd.n_edges = ne;
+        cd.vc_off = off + nn + ne; cd.n_vc = nvc;
+    }
+}
+
+__device__ __forceinline__ ExBuf smem_buf(uint8_t *sm) {
+    ExBuf b;
+    b.hu = (uint32_t *)sm; b.cap_u = CAP_U;
+    b.hk = b.hu + CAP_U; b.cap_k = CAP_K;
+    b.queue = b.hk + CAP_K; b.cap_q = CAP_Q;
+    b.edges = b.queue + CAP_Q; b.cap_e = CAP_E;
+    b.uf = b.edges + CAP_E;
+    b.flag = (uint8_t *)(b.uf + CAP_U);
+    return b;
+}
+constexpr size_t SMEM_EX = (size_t)(CAP_U + CAP_K + CAP_Q + CAP_E + CAP_U) * 4 + CAP_U;
+
+__device__ __forceinline__ ExBuf big_buf(const WsDev &w, uint32_t cta) {
+    // global scratch for the overflow path; capacities scale with V
+    uint64_t per = w.big_words;
+    uint32_t *p = w.big + per * cta;
+    uint32_t cu = next_pow2(2 * w.V + 2);
+    ExBuf b;
+    b.hu = p; b.cap_u = cu;
+    b.hk = b.hu + cu; b.cap_k = cu;
+    b.queue = b.hk + cu; b.cap_q = w.V + 1;
+    b.uf = b.queue + (w.V + 1);
+    b.flag = (uint8_t *)(b.uf + cu);
+    b.edges = (uint32_t *)(b.flag + cu + 16);
+    b.edges = (uint32_t *)(((uintptr_t)b.edges + 15) & ~(uintptr_t)15);
+    unsigned long long rem = per - (unsigned long long)(b.edges - p);
+    b.cap_e = (uint32_t)(rem < 0xFFFFFFFFull ? rem : 0xFFFFFFFFull);
+    return b;
+}
+
+template <class RowC> __global__ void __launch_bounds__(256) k_extract_cg(GraphDev g, WsDev w) {
+    extern __shared__ __align__(16) uint8_t smx[];
+    __shared__ ExShared sh;
+    ExBuf b = smem_buf(smx);
+    uint32_t total = w.coffs[w.nslots];
+    for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
+        uint32_t s = find_slot(w.coffs, w.nslots, item);
+        uint32_t c = item - w.coffs[s];
+        bool ovf = false;
+        extract_cg<RowC>(g, w, s, c, b, sh, &ovf);
+        if (ovf && threadIdx.x == 0) {
+            uint32_t p = atomicAdd(&w.ctr[C_NOVF], 1u);
+            if (p < w.ovf_cap) w.ovf[p] = make_uint2(s, c); else atomicOr(&w.st[s].err, (uint32_t)E_EXTRACT);
+        }
+        __syncthreads();
+    }
+}
+
+template <class RowC> __global__ void __launch_bounds__(256) k_extract_cg_big(GraphDev g, WsDev w) {
+    __shared__ ExShared sh;
+    ExBuf b = big_buf(w, blockIdx.x);
+    uint32_t n = min(w.ctr[C_NOVF], w.ovf_cap);
+    for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+        uint2 sc = w.ovf[i];
+        bool ovf = false;
+        extract_cg<RowC>(g, w, sc.x, sc.y, b, sh, &ovf);
+        if (ovf && threadIdx.x == 0) atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && blockIdx.x == 0) {}  // counter reset by the next scan/attach
+}
+
+// ====================================================================== run 2: attach, RPG, PTC
+// Attach (R14): D_gi = min over V_C of h_m[v][i]; all finite -> RPG with S^m = max_i
+// D_gi (Eq. 5) and S^r (Eq. 6).  One warp per candidate, byte-SIMD min over the V_C rows.
+template <class RowM> __global__ void __launch_bounds__(256) k_attach(WsDev w) {
+    typedef Row<RowM> R;
+    const uint32_t lane = lane_id();
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    uint32_t total = w.coffs[w.nslots];
+    for (uint32_t item = gw; item < total; item += nw) {
+        uint32_t s = find_slot(w.coffs, w.nslots, item);
+        uint32_t c = item - w.coffs[s];
+        SlotState &st = w.st[s];
+        if (!st.in_phase) continue;
+        Cand &cd = w.CD(s)[c];
+        if (cd.attached) continue;
+        const RowM *H = w.Hs<RowM>(1, s);
+        RowM mn = (RowM)~(RowM)0;
+        for (uint32_t t = lane; t < cd.n_vc; t += 32) mn = vmin<RowM>(mn, R::load(H + w.arena[cd.vc_off + t]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mn = vmin<RowM>(mn, shfl(mn, lane ^ o));
+        RowM used = used_mask<RowM>(st.T[1]);
+        if ((R::eq(mn, R::splat(0xFF)) & used) == 0 && lane == 0) {
+            uint32_t sm = R::maxb(mn & used);
+            cd.sm = sm;
+            cd.sr = rpg_score(st.gamma, cd.sc, sm);
+            for (uint32_t i = 0; i < RIKI_MAX_TERMS; i++) cd.mdist[i] = i < st.T[1] ? R::byte(mn, i) : 0;
+            cd.attached = 1;
+            atomicAdd(&st.n_attached, 1u);
+            uint32_t p = atomicAdd(&w.ctr[C_NNEWATT], 1u);
+            w.newatt[p] = make_uint2(s, c);
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t uf_find(volatile uint32_t *uf, uint32_t x) {
+    while (true) {
+        uint32_t p = uf[x];
+        if (p == x) return x;
+        x = p;
+    }
+}
+__device__ __forceinline__ void uf_union(uint32_t *uf, uint32_t a, uint32_t b) {
+    while (true) {
+        a = uf_find(uf, a);
+        b = uf_find(uf, b);
+        if (a == b) return;
+        if (a < b) { uint32_t t = a; a = b; b = t; }
+        if (atomicCAS(&uf[a], a, b) == a) return;
+    }
+}
+
+// RPG of an attached candidate: G^r = CG u (u_i SP(m_i, V_C)) recovered from the V_C nodes
+// at distance D_gi (R18), then PTC (R19/R19').
+template <class RowM> __device__ void extract_rpg(const GraphDev &g, const WsDev &w, uint32_t s, uint32_t c,
+                                                  const ExBuf &b, ExShared &sh, bool *overflow) {
+    typedef Row<RowM> R;
+    SlotState &st = w.st[s];
+    Cand &cd = w.CD(s)[c];
+    const RowM *H = w.Hs<RowM>(1, s);
+    const uint32_t T = st.T[1];
+    const bool blocking = T >= 2;
+    HashSet hu{b.hu, b.cap_u};
+    hs_clear(b.hu, b.cap_u);
+    if (threadIdx.x == 0) { sh.nedges = 0; sh.nnodes = 0; sh.ovf = 0; }
+    __syncthreads();
+    if (cd.n_nodes > b.cap_u / 2 || cd.n_edges > b.cap_e) { *overflow = true; return; }
+    for (uint32_t i = threadIdx.x; i < cd.n_nodes; i += blockDim.x) {
+        int r = hu.insert(w.arena[cd.nodes_off + i]);
+        if (r == 1) atomicAdd(&sh.nnodes, 1u);
+    }
+    for (uint32_t i = threadIdx.x; i < cd.n_edges; i += blockDim.x) b.edges[i] = w.arena[cd.edges_off + i];
+    if (threadIdx.x == 0) sh.nedges = cd.n_edges;
+    __syncthreads();
+    for (uint32_t j = 0; j < T; j++) {
+        hs_clear(b.hk, b.cap_k);
+        if (threadIdx.x == 0) sh.qtail = 0;
+        __syncthreads();
+        uint32_t dj = cd.mdist[j];
+        for (uint32_t t = threadIdx.x; t < cd.n_vc; t += blockDim.x) {
+            uint32_t v = w.arena[cd.vc_off + t];
+            if (R::byte(R::load(H + v), j) == dj) {
+                if (HashSet{b.hk, b.cap_k}.insert(v) < 0) sh.ovf = 1;
+                uint32_t p = atomicAdd(&sh.qtail, 1u);
+                if (p < b.cap_q) b.queue[p] = v; else sh.ovf = 1;
+            }
+        }
+        __syncthreads();
+        uint32_t nsrc = min(sh.qtail, b.cap_q);
+        if (!sh.ovf) bfs_column<RowM>(g, H, blocking, j, nsrc, b, sh);
+        __syncthreads();
+        if (sh.ovf) break;
+    }
+    __syncthreads();
+    if (sh.ovf) { *overflow = true; return; }
+    *overflow = false;
+    const uint32_t ne = min(sh.nedges, b.cap_e);
+    // ---- PTC: |M| = 1 trivial; else two distinct marginal keyword nodes X whose
+    // every simple connection in G^r passes through V_C (endpoint-inclusive, R19').
+    uint32_t pass = 1;
+    if (T >= 2) {
+        RowM used = used_mask<RowM>(T);
+        for (uint32_t i = threadIdx.x; i < b.cap_u; i += blockDim.x) { b.flag[i] = 0; b.uf[i] = i; }
+        if (threadIdx.x == 0) { sh.nx = 0; sh.xvc = 0; sh.mnr = EMPTY; sh.mxr = 0; }
+        __syncthreads();
+        for (uint32_t t = threadIdx.x; t < cd.n_vc; t += blockDim.x) {
+            int sl = hu.find(w.arena[cd.vc_off + t]);
+            if (sl >= 0) b.flag[sl] = 1;
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < b.cap_u; i += blockDim.x) {
+            uint32_t v = b.hu[i];
+            if (v == EMPTY) continue;
+            if (R::eq(R::load(H + v), 0) & used) {
+                b.flag[i] |= 2;
+                atomicAdd(&sh.nx, 1u);
+                if (b.flag[i] & 1) sh.xvc = 1;
+            }
+        }
+        __syncthreads();
+        if (sh.nx < 2) pass = 0;
+        else if (sh.xvc) pass = 1;
+        else {
+            for (uint32_t i = threadIdx.x; i < ne; i += blockDim.x) {
+                uint32_t e = b.edges[i];
+                int sa = hu.find(g.src[e]), sb = hu.find(g.dst[e]);
+                if (sa < 0 || sb < 0 || (b.flag[sa] & 1) || (b.flag[sb] & 1)) continue;
+                uf_union(b.uf, (uint32_t)sa, (uint32_t)sb);
+            }
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < b.cap_u; i += blockDim.x) {
+                if ((b.flag[i] & 3) != 2) continue;  // X outside V_C
+                uint32_t r = uf_find(b.uf, i);
+                atomicMin(&sh.mnr, r);
+                atomicMax(&sh.mxr, r);
+            }
+            __syncthreads();
+            pass = sh.mnr != sh.mxr;
+        }
+    }
+    __syncthreads();
+    // ---- write G^r lists
+    uint32_t nn = sh.nnodes;
+    if (threadIdx.x == 0) { sh.off = arena_alloc(w, nn + ne, s); sh.cnt = 0; }
+    __syncthreads();
+    uint32_t off = sh.off;
+    if (off != EMPTY) {
+        for (uint32_t i = threadIdx.x; i < b.cap_u; i += blockDim.x) {
+            uint32_t v = b.hu[i];
+            if (v == EMPTY) continue;
+            w.arena[off + atomicAdd(&sh.cnt, 1u)] = v;
+        }
+        for (uint32_t i = threadIdx.x; i < ne; i += blockDim.x) w.arena[off + nn + i] = b.edges[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && off != EMPTY) {
+        cd.nodes_off = off; cd.n_nodes = nn;
+        cd.edges_off = off + nn; cd.n_edges = ne;
+        cd.ptc = pass;
+        if (!pass) atomicAdd(&st.n_ptc_fail, 1u);
+        if (pass || st.ptc_mode == 1) {
+            uint32_t p = atomicAdd(&st.nR, 1u);
+            if (p < w.capc) w.RK(s)[p] = rkey(cd.sr, cd.sc, cd.v);
+            else atomicOr(&st.err, (uint32_t)E_CAND);
+        }
+    }
+}
+
+template <class RowM> __global__ void __launch_bounds__(256) k_extract_rpg(GraphDev g, WsDev w) {
+    extern __shared__ __align__(16) uint8_t smx[];
+    __shared__ ExShared sh;
+    ExBuf b = smem_buf(smx);
+    uint32_t n = w.ctr[C_NNEWATT];
+    for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+        uint2 sc = w.newatt[i];
+        bool ovf = false;
+        extract_rpg<RowM>(g, w, sc.x, sc.y, b, sh, &ovf);
+        if (ovf && threadIdx.x == 0) {
+            uint32_t p = atomicAdd(&w.ctr[C_NOVF], 1u);
+            if (p < w.ovf_cap) w.ovf[p] = sc; else atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT);
+        }
+        __syncthreads();
+    }
+}
+
+template <class RowM> __global__ void __launch_bounds__(256) k_extract_rpg_big(GraphDev g, WsDev w) {
+    __shared__ ExShared sh;
+    ExBuf b = big_buf(w, blockIdx.x);
+    uint32_t n = min(w.ctr[C_NOVF], w.ovf_cap);
+    for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+        uint2 sc = w.ovf[i];
+        bool ovf = false;
+        extract_rpg<RowM>(g, w, sc.x, sc.y, b, sh, &ovf);
+        if (ovf && threadIdx.x == 0) atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT);
+        __syncthreads();
+    }
+}
+
+__global__ void k_reset_level_ctrs(WsDev w) {
+    w.ctr[C_NNEWATT] = 0;
+    w.ctr[C_NOVF] = 0;
+}
+
+__device__ void cta_sort_u128(u128 *keys, uint32_t n, u128 *smem, uint32_t smem_cap) {
+    if (n < 2) return;
+    if (next_pow2(n) <= smem_cap) {
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) smem[i] = keys[i];
+        __syncthreads();
+        cta_bitonic_sort(smem, n);
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) keys[i] = smem[i];
+        __syncthreads();
+    } else {
+        cta_bitonic_sort(keys, n);
+    }
+}
+
+// Termination of run 2 at level l (after attach): depth, empty frontier, all attached, or
+// the exact bound (R21): |R| >= k and the best key any unattached candidate can still
+// reach, (gamma*S^c + (1-gamma)*(l+1), S^c, v), is worse than the k-th key of R.
+__global__ void k_decide_m(WsDev w, uint32_t l) {
+    extern __shared__ __align__(16) u128 sm128[];
+    __shared__ uint32_t first;
+    uint32_t s = blockIdx.x;
+    SlotState &st = w.st[s];
+    if (!st.in_phase) return;
+    if (threadIdx.x == 0) first = EMPTY;
+    __syncthreads();
+    uint32_t nR = min(st.nR, w.capc);
+    cta_sort_u128(w.RK(s), nR, sm128, 1024);
+    for (uint32_t c = threadIdx.x; c < st.n_extract; c += blockDim.x)
+        if (!w.CD(s)[c].attached) atomicMin(&first, c);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        bool stop = l >= st.depth || st.nq[l & 1] == 0 || first == EMPTY;
+        if (!stop && st.early_term == 0 && nR >= st.k) {
+            const Cand &fu = w.CD(s)[first];
+            u128 best = rkey(rpg_score(st.gamma, fu.sc, l + 1), fu.sc, fu.v);
+            stop = w.RK(s)[st.k - 1] < best;
+        }
+        st.stop_m = stop;
+    }
+}
+
+// ====================================================================== finalize
+__global__ void k_final_select(WsDev w) {
+    extern __shared__ __align__(16) u128 sm128[];
+    uint32_t s = blockIdx.x;
+    SlotState &st = w.st[s];
+    if (!st.active || st.err) {
+        if (threadIdx.x == 0) st.nres = 0;
+        return;
+    }
+    if (st.T[1] == 0) {  // M = empty: top-k CGs by (S^c, v)
+        uint32_t n = min(st.k, st.n_extract);
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) w.resid[(size_t)s * w.kmax + i] = i;
+        if (threadIdx.x == 0) st.nres = n;
+        return;
+    }
+    uint32_t nR = min(st.nR, w.capc);
+    cta_sort_u128(w.RK(s), nR, sm128, 1024);
+    uint32_t n = min(st.k, nR);
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        u128 key = w.RK(s)[i];
+        uint64_t ck = (uint64_t)key;  // (sc << 32 | v)
+        uint32_t lo = 0, hi = st.n_extract;
+        const uint64_t *K = w.CK(s);
+        while (lo < hi) { uint32_t m = (lo + hi) >> 1; if (K[m] < ck) lo = m + 1; else hi = m; }
+        w.resid[(size_t)s * w.kmax + i] = lo;
+    }
+    if (threadIdx.x == 0) st.nres = n;
+}
+
+// sort + unique a u32 list into the output buffer; returns (offset, count) via sh
+__device__ void sort_unique_out(const WsDev &w, uint32_t s, const uint32_t *src, uint32_t n, uint32_t *smem,
+                                uint32_t *scan, uint32_t *res_off, uint32_t *res_n) {
+    __shared__ uint32_t s_off, s_buf;
+    uint32_t *buf = smem;
+    bool global = next_pow2(n) > SORT_SMEM;
+    if (global) {
+        if (threadIdx.x == 0) s_buf = arena_alloc(w, next_pow2(n), s);
+        __syncthreads();
+        if (s_buf == EMPTY) { *res_off = 0; *res_n = 0; return; }
+        buf = w.arena + s_buf;
+    }
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) buf[i] = src[i];
+    __syncthreads();
+    cta_bitonic_sort(buf, n);
+    // unique: per-thread contiguous chunk counts + block scan
+    uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+    uint32_t b0 = min(threadIdx.x * per, n), b1 = min(b0 + per, n);
+    uint32_t cnt = 0;
+    for (uint32_t i = b0; i < b1; i++) cnt += (i == 0 || buf[i] != buf[i - 1]);
+    scan[threadIdx.x] = cnt;
+    __syncthreads();
+    for (uint32_t o = 1; o < blockDim.x; o <<= 1) {
+        uint32_t v = threadIdx.x >= o ? scan[threadIdx.x - o] : 0;
+        __syncthreads();
+        scan[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t total = scan[blockDim.x - 1];
+    if (threadIdx.x == 0) {
+        unsigned long long p = atomicAdd(w.out_used, (unsigned long long)total);
+        if (p + total > w.out_cap) { atomicOr(&w.st[s].err, (uint32_t)E_OUT); s_off = EMPTY; }
+        else s_off = (uint32_t)p;
+    }
+    __syncthreads();
+    uint32_t off = s_off;
+    if (off != EMPTY) {
+        uint32_t pos = off + scan[threadIdx.x] - cnt;
+        for (uint32_t i = b0; i < b1; i++)
+            if (i == 0 || buf[i] != buf[i - 1]) w.out[pos++] = buf[i];
+    }
+    __syncthreads();
+    *res_off = off;
+    *res_n = total;
+}
+
+template <class RowC> __global__ void __launch_bounds__(256) k_final_lists(WsDev w) {
+    extern __shared__ __align__(16) uint32_t sm32[];
+    __shared__ uint32_t scan[256];
+    uint32_t r = blockIdx.x, s = blockIdx.y;
+    const SlotState &st = w.st[s];
+    if (r >= st.nres) return;
+    uint32_t c = w.resid[(size_t)s * w.kmax + r];
+    const Cand &cd = w.CD(s)[c];
+    OutHdr h;
+    memset(&h, 0, sizeof(h));
+    h.central = cd.v;
+    h.sc = cd.sc;
+    h.sm = st.T[1] ? cd.sm : 0;
+    h.ptc = cd.ptc;
+    h.score = st.T[1] ? cd.sr : (double)cd.sc;
+    sort_unique_out(w, s, w.arena + cd.nodes_off, cd.n_nodes, sm32, scan, &h.nodes_off, &h.n_nodes);
+    sort_unique_out(w, s, w.arena + cd.edges_off, cd.n_edges, sm32, scan, &h.edges_off, &h.n_edges);
+    sort_unique_out(w, s, w.arena + cd.vc_off, cd.n_vc, sm32, scan, &h.vc_off, &h.n_vc);
+    RowC hv = Row<RowC>::load(w.Hs<RowC>(0, s) + cd.v);
+    for (uint32_t j = 0; j < RIKI_MAX_TERMS; j++) {
+        h.cdist[j] = j < st.T[0] ? Row<RowC>::byte(hv, j) : 0;
+        h.mdist[j] = j < st.T[1] ? cd.mdist[j] : 0;
+    }
+    if (threadIdx.x == 0) w.hdr[(size_t)s * w.kmax + r] = h;
+}
+
+// ====================================================================== debug boundary
+template <class RowT> __global__ void k_pack_H(WsDev w, uint32_t T, uint8_t *Hout, uint8_t *blk, int blocking) {
+    const RowT *H = w.Hs<RowT>(0, 0);
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < w.V; v += gridDim.x * blockDim.x) {
+        RowT r = Row<RowT>::load(H + v);
+        for (uint32_t j = 0; j < T; j++) Hout[(size_t)v * T + j] = (uint8_t)Row<RowT>::byte(r, j);
+        blk[v] = (blocking && Row<RowT>::eq(r, Row<RowT>::splat(0xFF)) == 0) ? (uint8_t)Row<RowT>::maxb(r) : 0xFF;
+    }
+}
+
+}  // namespace
+
+// ====================================================================== host side
+struct Workspace {
+    uint32_t slots = 0, V = 0, W = 0, capc = 0, kmax = 0, heavy_cap = 0, ovf_cap = 0, big_ctas = 0;
+    uint64_t arena_cap = 0, out_cap = 0, big_words = 0;
+    uint8_t *H[2] = {nullptr, nullptr};
+    uint32_t *q = nullptr, *bm = nullptr, *offs = nullptr, *coffs = nullptr, *ctr = nullptr, *arena = nullptr,
+             *big = nullptr, *resid = nullptr, *out = nullptr;
+    uint64_t *ck = nullptr;
+    Cand *cd = nullptr;
+    u128 *rk = nullptr;
+    SlotState *st = nullptr;
+    uint4 *heavy = nullptr;
+    unsigned long long *prof = nullptr, *arena_used = nullptr, *out_used = nullptr;
+    uint2 *newatt = nullptr, *ovf = nullptr;
+    OutHdr *hdr = nullptr;
+    uint32_t *h_ctr = nullptr;  // pinned
+    uint64_t bytes = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // state of the last device batch (for engine_fetch)
+    uint32_t last_n = 0;
+    std::vector<uint32_t> last_map;  // slot -> query index of the last batch
+    int last_rb[2] = {4, 4};
+    std::vector<std::vector<riki_results *>> dummy;
+    std::vector<void *> allocs;
+
+    template <class T> T *alloc(size_t n) {
+        T *p = nullptr;
+        if (n == 0) n = 1;
+        if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) {
+            cudaGetLastError();
+            RIKI_THROW(RIKI_ENOMEM, "workspace cudaMalloc of " + std::to_string(n * sizeof(T)) + " bytes failed");
+        }
+        allocs.push_back(p);
+        bytes += n * sizeof(T);
+        return p;
+    }
+    void release() {
+        for (void *p : allocs) cudaFree(p);
+        allocs.clear();
+        if (h_ctr) cudaFreeHost(h_ctr);
+        h_ctr = nullptr;
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        ev0 = ev1 = nullptr;
+        bytes = 0;
+    }
+    WsDev dev() const {
+        WsDev d;
+        d.st = st; d.nslots = slots; d.V = V; d.W = W; d.capc = capc; d.kmax = kmax;
+        d.H[0] = H[0]; d.H[1] = H[1]; d.rb[0] = last_rb[0]; d.rb[1] = last_rb[1];
+        d.q = q; d.bm = bm; d.ck = ck; d.cd = cd; d.rk = rk; d.offs = offs; d.coffs = coffs;
+        d.heavy = heavy; d.heavy_cap = heavy_cap; d.ctr = ctr; d.prof = prof;
+        d.arena = arena; d.arena_used = arena_used; d.arena_cap = arena_cap;
+        d.newatt = newatt; d.ovf = ovf; d.ovf_cap = ovf_cap;
+        d.big = big; d.big_words = big_words;
+        d.hdr = hdr; d.resid = resid; d.out = out; d.out_used = out_used; d.out_cap = out_cap;
+        return d;
+    }
+};
+
+namespace {
+
+struct Caps {
+    uint32_t slots, capc, kmax;
+    uint64_t arena, out;
+};
+
+void ensure_workspace(riki_graph *g, const Caps &c) {
+    Workspace *ws = g->ws;
+    if (ws && ws->slots >= c.slots && ws->V == g->V && ws->capc >= c.capc && ws->kmax >= c.kmax &&
+        ws->arena_cap >= c.arena && ws->out_cap >= c.out)
+        return;
+    if (ws) { ws->release(); delete ws; g->ws = nullptr; }
+    ws = new Workspace();
+    g->ws = ws;
+    const uint32_t V = g->V;
+    ws->slots = c.slots; ws->V = V; ws->W = (V + 31) / 32; ws->capc = c.capc; ws->kmax = c.kmax;
+    ws->arena_cap = c.arena; ws->out_cap = c.out;
+    const size_t S = c.slots;
+    ws->H[0] = ws->alloc<uint8_t>(S * V * 8);
+    ws->H[1] = ws->alloc<uint8_t>(S * V * 8);
+    ws->q = ws->alloc<uint32_t>(S * 2 * V);
+    ws->bm = ws->alloc<uint32_t>(S * 2 * ws->W);
+    CUDA_TRY(cudaMemset(ws->bm, 0, S * 2 * ws->W * 4));
+    ws->ck = ws->alloc<uint64_t>(S * c.capc);
+    ws->cd = ws->alloc<Cand>(S * c.capc);
+    ws->rk = ws->alloc<u128>(S * c.capc);
+    ws->st = ws->alloc<SlotState>(S);
+    ws->offs = ws->alloc<uint32_t>(S + 1);
+    ws->coffs = ws->alloc<uint32_t>(S + 1);
+    uint64_t hc = (uint64_t)S * (g->E / CHUNK + g->E / HEAVY + 64);
+    ws->heavy_cap = (uint32_t)std::min<uint64_t>(hc, 1u << 28);
+    ws->heavy = ws->alloc<uint4>(ws->heavy_cap);
+    ws->ctr = ws->alloc<uint32_t>(C_NCTR);
+    ws->prof = ws->alloc<unsigned long long>(P_NPROF);
+    ws->arena = ws->alloc<uint32_t>(c.arena);
+    ws->arena_used = ws->alloc<unsigned long long>(1);
+    ws->newatt = ws->alloc<uint2>(S * c.capc);
+    ws->ovf_cap = (uint32_t)(S * c.capc);
+    ws->ovf = ws->alloc<uint2>(ws->ovf_cap);
+    ws->big_ctas = V <= (4u << 20) ? 8 : 2;
+    uint64_t cu = next_pow2(2 * V + 2);
+    ws->big_words = cu * 3 + (V + 1) + cu / 4 + 16 + std::max<uint64_t>(std::min<uint64_t>(g->E, 1ull << 26), 1u << 20);
+    ws->big = ws->alloc<uint32_t>(ws->big_words * ws->big_ctas);
+    ws->hdr = ws->alloc<OutHdr>(S * c.kmax);
+    ws->resid = ws->alloc<uint32_t>(S * c.kmax);
+    ws->out = ws->alloc<uint32_t>(c.out);
+    ws->out_used = ws->alloc<unsigned long long>(1);
+    CUDA_TRY(cudaMallocHost(&ws->h_ctr, 64 * sizeof(uint32_t)));
+    CUDA_TRY(cudaEventCreate(&ws->ev0));
+    CUDA_TRY(cudaEventCreate(&ws->ev1));
+    static bool attr_done = false;
+    if (!attr_done) {
+        CUDA_TRY(cudaFuncSetAttribute(k_extract_cg<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_EX));
+        CUDA_TRY(cudaFuncSetAttribute(k_extract_cg<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_EX));
+        CUDA_TRY(cudaFuncSetAttribute(k_extract_rpg<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_EX));
+        CUDA_TRY(cudaFuncSetAttribute(k_extract_rpg<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_EX));
+        CUDA_TRY(cudaFuncSetAttribute(k_decide_m, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
+        CUDA_TRY(cudaFuncSetAttribute(k_final_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
+        CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
+        CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
+        attr_done = true;
+    }
+}
+
+unsigned grid_of(uint64_t work, unsigned per_block, unsigned cap = 148 * 16) {
+    uint64_t b = (work + per_block - 1) / per_block;
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(b, cap));
+}
+
+struct Launch {
+    riki_graph *g;
+    cudaStream_t s;
+    uint64_t launches = 0;
+    double expand_ms = 0;
+    uint64_t expand_launches = 0;
+    void check() {
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) RIKI_THROW(RIKI_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+        launches++;
+    }
+};
+
+// Runs one exploration loop over all slots (lock-step).  For run 2 the per-level attach /
+// RPG recovery / decide kernels run before the plan.  Returns when no slot expands.
+template <class RowT, class RowC>
+void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting_mode, uint32_t max_levels,
+               uint64_t total_cands) {
+    cudaStream_t s = L.s;
+    WsDev wd = ws->dev();
+    k_phase_begin<<<(ws->slots + 127) / 128, 128, 0, s>>>(wd, ph, hitting_mode);
+    L.check();
+    k_fill_H<RowT><<<dim3(grid_of(ws->V, 256, 64), ws->slots), 256, 0, s>>>(wd, ph);
+    L.check();
+    k_seed<RowT><<<dim3(16, ws->slots), 256, 0, s>>>(gd, wd, ph);
+    L.check();
+    for (uint32_t l = 0; l <= max_levels; l++) {
+        if (ph == 1) {
+            k_reset_level_ctrs<<<1, 1, 0, s>>>(wd);
+            L.check();
+            if (total_cands) {
+                k_attach<RowT><<<grid_of(total_cands * 32, 256), 256, 0, s>>>(wd);
+                L.check();
+                k_extract_rpg<RowT><<<148 * 2, 256, SMEM_EX, s>>>(gd, wd);
+                L.check();
+                k_extract_rpg_big<RowT><<<ws->big_ctas, 256, 0, s>>>(gd, wd);
+                L.check();
+            }
+            k_decide_m<<<ws->slots, 256, 1024 * 16, s>>>(wd, l);
+            L.check();
+        }
+        k_plan<<<1, MAX_SLOTS, 0, s>>>(wd, ph, l);
+        L.check();
+        CUDA_TRY(cudaMemcpyAsync(ws->h_ctr, ws->ctr, C_NCTR * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (ws->h_ctr[C_ACTIVE] == 0) break;
+        uint32_t total = ws->h_ctr[C_TOTAL];
+        if (L.g->profiling) CUDA_TRY(cudaEventRecord(ws->ev0, s));
+        k_expand<RowT><<<grid_of(total, 256), 256, 0, s>>>(gd, wd, ph, l);
+        L.check();
+        k_expand_heavy<RowT><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
+        L.check();
+        if (L.g->profiling) {
+            CUDA_TRY(cudaEventRecord(ws->ev1, s));
+            CUDA_TRY(cudaEventSynchronize(ws->ev1));
+            float ms = 0;
+            CUDA_TRY(cudaEventElapsedTime(&ms, ws->ev0, ws->ev1));
+            L.expand_ms += ms;
+            L.expand_launches += 2;
+        }
+    }
+    k_clear_bm<<<dim3(8, ws->slots), 256, 0, s>>>(wd, ph);
+    L.check();
+}
+
+template <class RowC, class RowM>
+void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
+    cudaStream_t s = L.s;
+    GraphDev gd = g->dev();
+    WsDev wd = ws->dev();
+    CUDA_TRY(cudaMemsetAsync(ws->arena_used, 0, 8, s));
+    CUDA_TRY(cudaMemsetAsync(ws->out_used, 0, 8, s));
+    CUDA_TRY(cudaMemsetAsync(ws->ctr, 0, C_NCTR * 4, s));
+    // ---- run 1: central keywords
+    run_phase<RowC, RowC>(L, gd, ws, 0, -1, depth + 1, 0);
+    // ---- candidate CGs + recovery
+    k_cand_sort<<<ws->slots, 1024, 4096 * 8, s>>>(wd);
+    L.check();
+    k_scan_cands<<<1, MAX_SLOTS, 0, s>>>(wd);
+    L.check();
+    CUDA_TRY(cudaMemcpyAsync(ws->h_ctr, ws->ctr, C_NCTR * 4, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    uint64_t total_cands = ws->h_ctr[C_NCAND_TOTAL];
+    if (total_cands) {
+        k_extract_cg<RowC><<<grid_of(total_cands, 1, 148 * 2), 256, SMEM_EX, s>>>(gd, wd);
+        L.check();
+        k_extract_cg_big<RowC><<<ws->big_ctas, 256, 0, s>>>(gd, wd);
+        L.check();
+    }
+    // ---- run 2: marginal keywords
+    run_phase<RowM, RowC>(L, gd, ws, 1, -1, depth + 1, total_cands);
+    // ---- top-k and packing
+    k_final_select<<<ws->slots, 256, 1024 * 16, s>>>(wd);
+    L.check();
+    k_final_lists<RowC><<<dim3(ws->kmax, ws->slots), 256, SORT_SMEM * 4, s>>>(wd);
+    L.check();
+}
+
+void run_batch(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
+    int a = ws->last_rb[0], b = ws->last_rb[1];
+    if (a == 4 && b == 4) run_batch_t<uint32_t, uint32_t>(L, g, ws, depth);
+    else if (a == 4) run_batch_t<uint32_t, uint64_t>(L, g, ws, depth);
+    else if (b == 4) run_batch_t<uint64_t, uint32_t>(L, g, ws, depth);
+    else run_batch_t<uint64_t, uint64_t>(L, g, ws, depth);
+}
+
+__global__ void k_slots_from_device(SlotState *st, uint32_t nslots, uint32_t q0, uint32_t nq, const uint64_t *cptr,
+                                    const uint32_t *ct, const uint64_t *mptr, const uint32_t *mt, SlotState tmpl,
+                                    const uint64_t *tptr, uint32_t n_terms) {
+    uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nslots) return;
+    SlotState x = tmpl;
+    uint32_t q = q0 + s;
+    x.active = q < nq;
+    if (x.active) {
+        uint64_t cb = cptr[q], ce = cptr[q + 1], mb = mptr[q], me = mptr[q + 1];
+        x.T[0] = (uint32_t)(ce - cb);
+        x.T[1] = (uint32_t)(me - mb);
+        if (x.T[0] == 0 || x.T[0] > RIKI_MAX_TERMS || x.T[1] > RIKI_MAX_TERMS) x.err |= E_UNRESOLVED;
+        for (uint32_t j = 0; j < x.T[0] && j < RIKI_MAX_TERMS; j++) x.term[0][j] = ct[cb + j];
+        for (uint32_t j = 0; j < x.T[1] && j < RIKI_MAX_TERMS; j++) x.term[1][j] = mt[mb + j];
+        for (int p = 0; p < 2; p++)
+            for (uint32_t j = 0; j < x.T[p] && j < RIKI_MAX_TERMS; j++) {
+                uint32_t t = x.term[p][j];
+                if (t >= n_terms || tptr[t + 1] == tptr[t]) x.err |= E_UNRESOLVED;
+            }
+    } else {
+        x.T[0] = x.T[1] = 0;
+    }
+    st[s] = x;
+}
+
+SlotState make_template(uint32_t k, uint32_t depth, const riki_params &p) {
+    SlotState t;
+    memset(&t, 0, sizeof(t));
+    t.k = k;
+    t.w = p.beam_w ? p.beam_w : k;
+    t.depth = depth;
+    t.beam_mode = p.beam_mode;
+    t.ptc_mode = p.ptc_mode;
+    t.early_term = p.early_term;
+    t.gamma = p.gamma;
+    t.L_end[0] = t.L_end[1] = -1;
+    return t;
+}
+
+uint32_t auto_slots(riki_graph *g, uint32_t nq) {
+    uint32_t want = g->batch_slots ? g->batch_slots : 256;
+    want = std::min<uint32_t>(want, MAX_SLOTS);
+    want = std::min<uint32_t>(want, std::max<uint32_t>(nq, 1));
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    uint64_t per = (uint64_t)g->V * (8 + 8 + 8) + 4096ull * (8 + sizeof(Cand) + 16 + 8) + 64 * 1024;
+    uint64_t budget = fr > (4ull << 30) ? (fr - (4ull << 30)) / 2 : fr / 4;
+    uint32_t fit = (uint32_t)std::max<uint64_t>(1, budget / std::max<uint64_t>(per, 1));
+    return std::max<uint32_t>(1, std::min(want, fit));
+}
+
+void collect_results(riki_graph *g, Workspace *ws, uint32_t n_active, const std::vector<uint32_t> &qidx,
+                     std::vector<riki_results *> *out) {
+    cudaStream_t s = g->stream;
+    std::vector<SlotState> st(ws->slots);
+    std::vector<OutHdr> hdr((size_t)ws->slots * ws->kmax);
+    unsigned long long used = 0;
+    CUDA_TRY(cudaMemcpyAsync(st.data(), ws->st, st.size() * sizeof(SlotState), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(hdr.data(), ws->hdr, hdr.size() * sizeof(OutHdr), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&used, ws->out_used, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    std::vector<uint32_t> lists(used);
+    if (used) CUDA_TRY(cudaMemcpyAsync(lists.data(), ws->out, used * 4, cudaMemcpyDeviceToHost, s));
+    std::vector<uint64_t> cks;
+    if (g->debug) {
+        cks.resize((size_t)ws->slots * ws->capc);
+        CUDA_TRY(cudaMemcpyAsync(cks.data(), ws->ck, cks.size() * 8, cudaMemcpyDeviceToHost, s));
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
+    for (uint32_t sl = 0; sl < n_active; sl++) {
+        const SlotState &x = st[sl];
+        riki_results *r = new riki_results();
+        r->nc = x.T[0];
+        r->nm = x.T[1];
+        r->stats.L_central = x.L_end[0];
+        r->stats.L_marginal = x.T[1] ? x.L_end[1] : -1;
+        r->stats.n_candidates = x.ncand_kept;
+        r->stats.n_attached = x.n_attached;
+        r->stats.n_ptc_fail = x.n_ptc_fail;
+        r->stats.relax_central = x.relax[0];
+        r->stats.relax_marginal = x.T[1] ? x.relax[1] : 0;
+        for (uint32_t i = 0; i < x.nres; i++) {
+            const OutHdr &h = hdr[(size_t)sl * ws->kmax + i];
+            HostRPG p;
+            p.central_node = h.central; p.sc = h.sc; p.sm = h.sm; p.score = h.score; p.ptc = (uint8_t)h.ptc;
+            p.nodes.assign(lists.begin() + h.nodes_off, lists.begin() + h.nodes_off + h.n_nodes);
+            p.vc.assign(lists.begin() + h.vc_off, lists.begin() + h.vc_off + h.n_vc);
+            p.edges.assign(lists.begin() + h.edges_off, lists.begin() + h.edges_off + h.n_edges);
+            memcpy(p.cdist, h.cdist, RIKI_MAX_TERMS);
+            memcpy(p.mdist, h.mdist, RIKI_MAX_TERMS);
+            r->rpgs.push_back(std::move(p));
+        }
+        if (g->debug) {
+            uint32_t n = std::min(x.ncand_kept, ws->capc);
+            r->cand.assign(cks.begin() + (size_t)sl * ws->capc, cks.begin() + (size_t)sl * ws->capc + n);
+        }
+        (*out)[qidx[sl]] = r;
+    }
+}
+
+std::string err_text(uint32_t e) {
+    std::string m;
+    if (e & E_CAND) m += " candidate-capacity";
+    if (e & E_HEAVY) m += " heavy-queue";
+    if (e & E_ARENA) m += " arena";
+    if (e & E_EXTRACT) m += " recovery-scratch";
+    if (e & E_OUT) m += " output";
+    if (e & E_UNRESOLVED) m += " unresolved-term";
+    return m;
+}
+
+// Run [q0, q0+n) of a batch whose slot states are already on the device (any source).
+// Grows capacities and re-runs when a workspace overflow is reported.
+void run_with_retry(riki_graph *g, Launch &L, uint32_t depth, Caps &caps, uint32_t n_active,
+                    const std::function<void()> &upload, std::vector<SlotState> *st_out) {
+    for (int attempt = 0;; attempt++) {
+        ensure_workspace(g, caps);
+        Workspace *ws = g->ws;
+        upload();
+        run_batch(L, g, ws, depth);
+        st_out->resize(ws->slots);
+        CUDA_TRY(cudaMemcpyAsync(st_out->data(), ws->st, ws->slots * sizeof(SlotState), cudaMemcpyDeviceToHost, L.s));
+        CUDA_TRY(cudaStreamSynchronize(L.s));
+        uint32_t err = 0;
+        for (uint32_t i = 0; i < n_active; i++) err |= (*st_out)[i].err;
+        if (err & E_UNRESOLVED) RIKI_THROW(RIKI_EUNRESOLVED, "a query term is unresolved (empty posting) or out of range");
+        if (!err) return;
+        if (attempt >= 6) RIKI_THROW(RIKI_ENOMEM, "workspace overflow:" + err_text(err));
+        if (err & E_CAND) caps.capc = std::min<uint32_t>(caps.capc * 4, next_pow2(g->V + 1));
+        if (err & (E_ARENA | E_EXTRACT)) caps.arena *= 4;
+        if (err & E_OUT) caps.out *= 4;
+        if (err & E_HEAVY) RIKI_THROW(RIKI_ENOMEM, "heavy work queue overflow");
+    }
+}
+
+void add_stats(riki_graph *g, Workspace *ws, Launch &L, uint32_t nq) {
+    unsigned long long prof[P_NPROF];
+    CUDA_TRY(cudaMemcpyAsync(prof, ws->prof, sizeof(prof), cudaMemcpyDeviceToHost, L.s));
+    CUDA_TRY(cudaStreamSynchronize(L.s));
+    uint64_t rb = ws->last_rb[0];  // bytes per H row (approximation when phases differ)
+    g->stats.expand_launches += L.expand_launches;
+    g->stats.expand_ms += L.expand_ms;
+    g->stats.expand_bytes += prof[P_ITEMS] * (12 + rb) + prof[P_EDGES] * (5 + rb) + prof[P_NEWCELLS] + prof[P_ENQ] * 4;
+    g->stats.kernel_launches += L.launches;
+    g->stats.queries += nq;
+}
+
+}  // namespace
+
+static void check_query_host(riki_graph *g, const QueryIn &q) {
+    if (q.nc == 0) RIKI_THROW(RIKI_EEMPTY_CENTRAL, "C must be non-empty (Def. RPQ, P:105)");
+    if (q.nc > RIKI_MAX_TERMS || q.nm > RIKI_MAX_TERMS) RIKI_THROW(RIKI_EINVAL, "at most 8 terms per keyword class");
+    for (uint32_t j = 0; j < q.nc + q.nm; j++) {
+        uint32_t t = j < q.nc ? q.c[j] : q.m[j - q.nc];
+        if (t >= g->n_terms) RIKI_THROW(RIKI_EINVAL, "term id " + std::to_string(t) + " out of range");
+        if (g->h_tptr[t + 1] == g->h_tptr[t])
+            RIKI_THROW(RIKI_EUNRESOLVED, "term " + std::to_string(t) + " (query position " + std::to_string(j) +
+                                             ") has an empty posting list");
+    }
+}
+
+static void check_common(riki_graph *g, uint32_t k, uint32_t depth, const riki_params &p) {
+    if (!g->has_act) RIKI_THROW(RIKI_ENOWEIGHTS, "activation levels not set (call riki_set_*_weights)");
+    if (k == 0) RIKI_THROW(RIKI_EINVAL, "k must be >= 1");
+    if (depth > RIKI_MAX_DEPTH) RIKI_THROW(RIKI_EDEPTH, "depth must be <= 254");
+    if (!(p.gamma >= 0.0 && p.gamma <= 1.0)) RIKI_THROW(RIKI_EINVAL, "gamma must be in [0,1]");
+    if (p.beam_mode < 0 || p.beam_mode > 1) RIKI_THROW(RIKI_EINVAL, "beam_mode must be 0 or 1");
+    if (p.tie_break != 0) RIKI_THROW(RIKI_ENOSYS, "tie_break != 0 not implemented");
+    if (p.ptc_mode < 0 || p.ptc_mode > 1) RIKI_THROW(RIKI_ENOSYS, "ptc_mode must be 0 or 1 in this build");
+    if (p.early_term != 0 && p.early_term != 2) RIKI_THROW(RIKI_ENOSYS, "early_term must be 0 or 2 in this build");
+    if (p.beam_w && p.beam_w < k) RIKI_THROW(RIKI_EINVAL, "beam width must be >= k (P:309)");
+}
+
+static Caps initial_caps(riki_graph *g, uint32_t nq, uint32_t k) {
+    Caps c;
+    c.slots = auto_slots(g, nq);
+    c.capc = std::min<uint32_t>(16384, next_pow2(g->V + 1));
+    c.kmax = std::max<uint32_t>(k, g->ws ? g->ws->kmax : 1);
+    c.arena = std::max<uint64_t>(64ull << 20, g->ws ? g->ws->arena_cap : 0);
+    c.out = std::max<uint64_t>(16ull << 20, g->ws ? g->ws->out_cap : 0);
+    if (g->ws) c.capc = std::max(c.capc, g->ws->capc);
+    return c;
+}
+
+void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, uint32_t depth, const riki_params &p,
+                   cudaStream_t stream, std::vector<riki_results *> *out) {
+    check_common(g, k, depth, p);
+    for (const QueryIn &q : qs) check_query_host(g, q);
+    out->assign(qs.size(), nullptr);
+    if (qs.empty()) return;
+    Caps caps = initial_caps(g, (uint32_t)qs.size(), k);
+    Launch L{g, stream ? stream : g->stream};
+    if (stream) {
+        // run on the library stream, ordered after the caller's stream
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(e, stream));
+        CUDA_TRY(cudaStreamWaitEvent(g->stream, e, 0));
+        cudaEventDestroy(e);
+        L.s = g->stream;
+    }
+    uint32_t maxc = 0, maxm = 0;
+    for (const QueryIn &q : qs) { maxc = std::max(maxc, q.nc); maxm = std::max(maxm, q.nm); }
+    SlotState tmpl = make_template(k, depth, p);
+    std::vector<riki_results *> &res = *out;
+    try {
+        for (size_t q0 = 0; q0 < qs.size();) {
+            ensure_workspace(g, caps);
+            uint32_t slots = g->ws->slots;
+            uint32_t n = (uint32_t)std::min<size_t>(slots, qs.size() - q0);
+            std::vector<uint32_t> qidx(n);
+            for (uint32_t i = 0; i < n; i++) qidx[i] = (uint32_t)(q0 + i);
+            std::vector<SlotState> stv;
+            auto upload = [&]() {
+                Workspace *ws = g->ws;
+                ws->last_rb[0] = maxc <= 4 ? 4 : 8;
+                ws->last_rb[1] = maxm <= 4 ? 4 : 8;
+                std::vector<SlotState> h(ws->slots, tmpl);
+                for (uint32_t i = 0; i < ws->slots; i++) {
+                    SlotState &x = h[i];
+                    if (i < n) {
+                        const QueryIn &q = qs[q0 + i];
+                        x.active = 1;
+                        x.T[0] = q.nc; x.T[1] = q.nm;
+                        for (uint32_t j = 0; j < q.nc; j++) x.term[0][j] = q.c[j];
+                        for (uint32_t j = 0; j < q.nm; j++) x.term[1][j] = q.m[j];
+                    } else {
+                        x.active = 0; x.T[0] = x.T[1] = 0;
+                    }
+                }
+                CUDA_TRY(cudaMemcpyAsync(ws->st, h.data(), h.size() * sizeof(SlotState), cudaMemcpyHostToDevice, L.s));
+                CUDA_TRY(cudaMemsetAsync(ws->prof, 0, P_NPROF * 8, L.s));
+            };
+            run_with_retry(g, L, depth, caps, n, upload, &stv);
+            collect_results(g, g->ws, n, qidx, &res);
+            add_stats(g, g->ws, L, n);
+            q0 += n;
+        }
+    } catch (...) {
+        for (auto *r : res) delete r;
+        res.assign(qs.size(), nullptr);
+        throw;
+    }
+}
+
+void engine_search_device(riki_graph *g, uint32_t nq, const uint64_t *d_cptr, const uint32_t *d_cterms,
+                          const uint64_t *d_mptr, const uint32_t *d_mterms, uint32_t k, uint32_t depth,
+                          const riki_params &p) {
+    check_common(g, k, depth, p);
+    Caps caps = initial_caps(g, nq, k);
+    caps.slots = std::max(caps.slots, std::min<uint32_t>(nq, MAX_SLOTS));
+    ensure_workspace(g, caps);
+    if (nq > g->ws->slots) RIKI_THROW(RIKI_EINVAL, "device batch larger than the workspace slots");
+    Launch L{g, g->stream};
+    SlotState tmpl = make_template(k, depth, p);
+    // row widths need the max term counts: read the (small) pointer arrays' extents on device
+    std::vector<uint64_t> cp(nq + 1), mp(nq + 1);
+    CUDA_TRY(cudaMemcpyAsync(cp.data(), d_cptr, (nq + 1) * 8, cudaMemcpyDeviceToHost, L.s));
+    CUDA_TRY(cudaMemcpyAsync(mp.data(), d_mptr, (nq + 1) * 8, cudaMemcpyDeviceToHost, L.s));
+    CUDA_TRY(cudaStreamSynchronize(L.s));
+    uint32_t maxc = 0, maxm = 0;
+    for (uint32_t q = 0; q < nq; q++) {
+        maxc = std::max<uint32_t>(maxc, (uint32_t)(cp[q + 1] - cp[q]));
+        maxm = std::max<uint32_t>(maxm, (uint32_t)(mp[q + 1] - mp[q]));
+    }
+    if (maxc == 0) RIKI_THROW(RIKI_EEMPTY_CENTRAL, "C must be non-empty (Def. RPQ, P:105)");
+    std::vector<SlotState> stv;
+    auto upload = [&]() {
+        Workspace *ws = g->ws;
+        ws->last_rb[0] = maxc <= 4 ? 4 : 8;
+        ws->last_rb[1] = maxm <= 4 ? 4 : 8;
+        k_slots_from_device<<<(ws->slots + 127) / 128, 128, 0, L.s>>>(ws->st, ws->slots, 0, nq, d_cptr, d_cterms,
+                                                                      d_mptr, d_mterms, tmpl, g->d_tptr, g->n_terms);
+        L.check();
+        CUDA_TRY(cudaMemsetAsync(ws->prof, 0, P_NPROF * 8, L.s));
+    };
+    run_with_retry(g, L, depth, caps, nq, upload, &stv);
+    g->ws->last_n = nq;
+    add_stats(g, g->ws, L, nq);
+}
+
+void engine_fetch(riki_graph *g, uint32_t nq, std::vector<riki_results *> *out) {
+    if (!g->ws || g->ws->last_n != nq) RIKI_THROW(RIKI_EINVAL, "no device batch of that size to fetch");
+    out->assign(nq, nullptr);
+    std::vector<uint32_t> qidx(nq);
+    for (uint32_t i = 0; i < nq; i++) qidx[i] = i;
+    collect_results(g, g->ws, nq, qidx, out);
+}
+
+void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uint32_t depth, int block_mode,
+                           uint8_t *H_out, uint8_t *block_out, uint64_t *relax_out, int32_t *L_out) {
+    if (!g->has_act) RIKI_THROW(RIKI_ENOWEIGHTS, "activation levels not set");
+    if (T == 0 || T > RIKI_MAX_TERMS) RIKI_THROW(RIKI_EINVAL, "1..8 terms");
+    if (depth > RIKI_MAX_DEPTH) RIKI_THROW(RIKI_EDEPTH, "depth must be <= 254");
+    if (block_mode < 0 || block_mode > 2) RIKI_THROW(RIKI_EINVAL, "block_mode must be 0, 1 or 2");
+    if (!H_out || !block_out) RIKI_THROW(RIKI_EINVAL, "null output");
+    QueryIn q{};
+    q.nc = T;
+    for (uint32_t j = 0; j < T; j++) q.c[j] = terms[j];
+    check_query_host(g, q);
+    Caps caps = initial_caps(g, 1, 1);
+    ensure_workspace(g, caps);
+    Workspace *ws = g->ws;
+    ws->last_rb[0] = T <= 4 ? 4 : 8;
+    ws->last_rb[1] = 4;
+    SlotState x = make_template(1, depth, riki_params{0.5, 0, 0, 0, 0, 0});
+    x.w = 0xFFFFFFFFu;
+    std::vector<SlotState> h(ws->slots, x);
+    for (uint32_t i = 0; i < ws->slots; i++) { h[i].active = 0; h[i].T[0] = h[i].T[1] = 0; }
+    h[0].active = 1;
+    h[0].T[0] = T;
+    for (uint32_t j = 0; j < T; j++) h[0].term[0][j] = terms[j];
+    Launch L{g, g->stream};
+    CUDA_TRY(cudaMemcpyAsync(ws->st, h.data(), h.size() * sizeof(SlotState), cudaMemcpyHostToDevice, L.s));
+    CUDA_TRY(cudaMemsetAsync(ws->ctr, 0, C_NCTR * 4, L.s));
+    CUDA_TRY(cudaMemsetAsync(ws->prof, 0, P_NPROF * 8, L.s));
+    GraphDev gd = g->dev();
+    uint8_t *dH = nullptr, *dB = nullptr;
+    CUDA_TRY(cudaMalloc(&dH, (size_t)g->V * T + 1));
+    CUDA_TRY(cudaMalloc(&dB, (size_t)g->V + 1));
+    int blocking = block_mode == 1 || (block_mode == 2 && T >= 2);
+    try {
+        WsDev wd = ws->dev();
+        if (T <= 4) {
+            run_phase<uint32_t, uint32_t>(L, gd, ws, 0, block_mode, depth + 1, 0);
+            k_pack_H<uint32_t><<<grid_of(g->V, 256), 256, 0, L.s>>>(wd, T, dH, dB, blocking);
+        } else {
+            run_phase<uint64_t, uint64_t>(L, gd, ws, 0, block_mode, depth + 1, 0);
+            k_pack_H<uint64_t><<<grid_of(g->V, 256), 256, 0, L.s>>>(wd, T, dH, dB, blocking);
+        }
+        L.check();
+        CUDA_TRY(cudaMemcpyAsync(H_out, dH, (size_t)g->V * T, cudaMemcpyDeviceToHost, L.s));
+        CUDA_TRY(cudaMemcpyAsync(block_out, dB, g->V, cudaMemcpyDeviceToHost, L.s));
+        SlotState s0;
+        CUDA_TRY(cudaMemcpyAsync(&s0, ws->st, sizeof(SlotState), cudaMemcpyDeviceToHost, L.s));
+        CUDA_TRY(cudaStreamSynchronize(L.s));
+        if (s0.err) RIKI_THROW(RIKI_ENOMEM, "workspace overflow:" + err_text(s0.err));
+        if (relax_out) *relax_out = s0.relax[0];
+        if (L_out) *L_out = s0.L_end[0];
+        add_stats(g, ws, L, 0);
+    } catch (...) {
+        cudaFree(dH);
+        cudaFree(dB);
+        throw;
+    }
+    cudaFree(dH);
+    cudaFree(dB);
+}
+
+void engine_free(riki_graph *g) {
+    if (g->ws) {
+        g->ws->release();
+        delete g->ws;
+        g->ws = nullptr;
+    }
+}
+
+uint64_t engine_workspace_bytes(const riki_graph *g) { return g->ws ? g->ws->bytes : 0; }

@@ -1,0 +1,339 @@
+// graph.cu -- graph residency and edge activation levels (a1/a2 of the hot-path table;
+// not timed).  P:339-340 (CSR in GPU memory), P:189-217 (weighting and coarsening).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "internal.cuh"
+
+namespace {
+
+template <class T> T *dmalloc(size_t n, uint64_t *acc = nullptr) {
+    T *p = nullptr;
+    if (n == 0) n = 1;
+    cudaError_t e = cudaMalloc(&p, n * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        RIKI_THROW(RIKI_ENOMEM, "cudaMalloc of " + std::to_string(n * sizeof(T)) + " bytes failed");
+    }
+    if (acc) *acc += n * sizeof(T);
+    return p;
+}
+
+int bits_for(uint64_t x) {
+    int b = 1;
+    while ((1ull << b) <= x) b++;
+    return b;
+}
+
+__global__ void k_histogram(const uint32_t *key, uint64_t n, uint32_t *cnt) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(&cnt[key[i] + 1], 1u);
+}
+
+// Eq. 1-3, half-up rounding (R1), fp64 in the oracle's exact operation order
+// with explicit round-to-nearest intrinsics so no FMA contraction can occur (R5).
+__device__ __forceinline__ uint32_t coarsen_dev(double w, double alpha, double avg) {
+    double x;
+    if (w <= alpha) x = __dsub_rn(avg, __ddiv_rn(__dmul_rn(avg, __dsub_rn(alpha, w)), alpha));
+    else x = __dadd_rn(avg, __ddiv_rn(__dmul_rn(avg, __dsub_rn(w, alpha)), __dsub_rn(1.0, alpha)));
+    return (uint32_t)floor(__dadd_rn(x, 0.5));
+}
+
+__global__ void k_coarsen_edges(const double *w, uint64_t n, double alpha, double avg, uint8_t *a, uint32_t *bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        double x = w[i];
+        if (!(x >= 0.0 && x <= 1.0)) { atomicOr(bad, 1u); a[i] = 0xFF; continue; }
+        a[i] = (uint8_t)coarsen_dev(x, alpha, avg);
+    }
+}
+
+__global__ void k_coarsen_nodes(const double *w, const uint32_t *dst, uint64_t n, double alpha, double avg,
+                                uint8_t *a, uint32_t *bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        double x = w[dst[i]];
+        if (!(x >= 0.0 && x <= 1.0)) { atomicOr(bad, 1u); a[i] = 0xFF; continue; }
+        a[i] = (uint8_t)coarsen_dev(x, alpha, avg);
+    }
+}
+
+__global__ void k_make_keys(const uint32_t *node, const uint32_t *cls, uint64_t n, uint64_t *key, uint32_t *val) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        key[i] = (uint64_t)node[i] << 32 | cls[i];
+        val[i] = (uint32_t)i;
+    }
+}
+
+// run length of sorted key[i] by exponential + binary search around i
+__global__ void k_run_length(const uint64_t *key, const uint32_t *eid, uint64_t n, uint32_t *cnt) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t k = key[i];
+        // lower bound in [0, i]
+        uint64_t step = 1, lo_out = i;  // key[lo_out] == k
+        while (step <= lo_out && key[lo_out - step] == k) { lo_out -= step; step <<= 1; }
+        uint64_t lo = step <= lo_out ? lo_out - step : 0, hi = lo_out;  // first equal in (lo, hi]
+        while (lo < hi) { uint64_t m = (lo + hi) / 2; if (key[m] < k) lo = m + 1; else hi = m; }
+        uint64_t first = lo;
+        step = 1; uint64_t hi_in = i;
+        while (hi_in + step < n && key[hi_in + step] == k) { hi_in += step; step <<= 1; }
+        lo = hi_in; hi = (hi_in + step < n) ? hi_in + step : n;  // last equal in [lo, hi)
+        while (lo + 1 < hi) { uint64_t m = (lo + hi) / 2; if (key[m] == k) lo = m; else hi = m; }
+        cnt[eid[i]] = (uint32_t)(lo - first + 1);
+    }
+}
+
+// P:193 raw weight = ln(count_out + count_in); stored as double
+__global__ void k_raw_weight(const uint32_t *co, const uint32_t *ci, uint64_t n, double *raw) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        raw[i] = log((double)(co[i] + ci[i]));
+}
+
+// P:194 min-max rescale; degenerate max == min -> 0 (R2)
+__global__ void k_rescale(const double *raw, uint64_t n, const double *mnmx, double *w) {
+    double mn = mnmx[0], mx = mnmx[1];
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        w[i] = (mx == mn) ? 0.0 : __ddiv_rn(__dsub_rn(raw[i], mn), __dsub_rn(mx, mn));
+}
+
+__global__ void k_act_keys(const uint32_t *node, const uint8_t *a, uint64_t n, uint64_t *key, uint32_t *val) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        key[i] = (uint64_t)node[i] << 8 | a[i];
+        val[i] = (uint32_t)i;
+    }
+}
+
+__global__ void k_gather_out(const uint64_t *key, const uint32_t *eid, const uint32_t *dst, uint64_t n,
+                             uint32_t *col, uint8_t *act) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        col[i] = dst[eid[i]];
+        act[i] = (uint8_t)(key[i] & 0xFF);
+    }
+}
+
+__global__ void k_gather_in(const uint64_t *key, const uint32_t *eid, const uint32_t *src, uint64_t n,
+                            uint32_t *isrc, uint32_t *ieid, uint8_t *iact) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t e = eid[i];
+        isrc[i] = src[e];
+        ieid[i] = e;
+        iact[i] = (uint8_t)(key[i] & 0xFF);
+    }
+}
+
+__global__ void k_minmax_pair(double *mnmx, const double *mn, const double *mx) {
+    mnmx[0] = *mn;
+    mnmx[1] = *mx;
+}
+
+unsigned grid_for(uint64_t n) { return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 148ull * 16)); }
+
+void sync_check(cudaStream_t s) { CUDA_TRY(cudaStreamSynchronize(s)); }
+
+// Sort (key, eid) pairs by key over [0, end_bit); returns device buffers (caller frees).
+void sort_pairs(cudaStream_t s, uint64_t *&keys, uint32_t *&vals, uint64_t n, int end_bit) {
+    uint64_t *k2 = dmalloc<uint64_t>(n);
+    uint32_t *v2 = dmalloc<uint32_t>(n);
+    size_t tmp = 0;
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp, keys, k2, vals, v2, (int64_t)n, 0, end_bit, s));
+    void *t = dmalloc<uint8_t>(tmp);
+    CUDA_TRY(cub::DeviceRadixSort::SortPairs(t, tmp, keys, k2, vals, v2, (int64_t)n, 0, end_bit, s));
+    sync_check(s);
+    cudaFree(t);
+    cudaFree(keys);
+    cudaFree(vals);
+    keys = k2;
+    vals = v2;
+}
+
+// Builds both CSRs from d_act_e (activation by edge id): rows sorted by (activation, edge id).
+void build_csr(riki_graph *g) {
+    cudaStream_t s = g->stream;
+    uint64_t E = g->E;
+    int eb = bits_for(g->V) + 8;
+    uint64_t *keys = dmalloc<uint64_t>(E);
+    uint32_t *vals = dmalloc<uint32_t>(E);
+    // out-CSR
+    k_act_keys<<<grid_for(E), 256, 0, s>>>(g->d_src, g->d_act_e, E, keys, vals);
+    sort_pairs(s, keys, vals, E, eb);
+    k_gather_out<<<grid_for(E), 256, 0, s>>>(keys, vals, g->d_dst, E, g->d_col, g->d_act);
+    // in-CSR
+    k_act_keys<<<grid_for(E), 256, 0, s>>>(g->d_dst, g->d_act_e, E, keys, vals);
+    sort_pairs(s, keys, vals, E, eb);
+    k_gather_in<<<grid_for(E), 256, 0, s>>>(keys, vals, g->d_src, E, g->d_isrc, g->d_ieid, g->d_iact);
+    sync_check(s);
+    cudaFree(keys);
+    cudaFree(vals);
+    g->has_act = true;
+}
+
+void row_pointers(cudaStream_t s, const uint32_t *key, uint64_t E, uint32_t V, uint32_t *row) {
+    CUDA_TRY(cudaMemsetAsync(row, 0, (V + 1) * sizeof(uint32_t), s));
+    k_histogram<<<grid_for(E), 256, 0, s>>>(key, E, row);
+    size_t tmp = 0;
+    CUDA_TRY(cub::DeviceScan::InclusiveSum(nullptr, tmp, row, row, (int)(V + 1), s));
+    void *t = dmalloc<uint8_t>(tmp);
+    CUDA_TRY(cub::DeviceScan::InclusiveSum(t, tmp, row, row, (int)(V + 1), s));
+    sync_check(s);
+    cudaFree(t);
+}
+
+void check_params(double alpha, double avg) {
+    if (!(alpha > 0.0 && alpha < 1.0)) RIKI_THROW(RIKI_EINVAL, "alpha must be in (0,1) (P:198)");
+    if (!(avg > 0.0) || !(2.0 * avg + 0.5 < 254.0)) RIKI_THROW(RIKI_EINVAL, "avg_hops must be in (0, 126.75)");
+}
+
+}  // namespace
+
+void graph_load(riki_graph *g, uint32_t V, uint64_t E, const uint32_t *src, const uint32_t *dst, const uint32_t *cls,
+                uint32_t n_terms, const uint64_t *tptr, const uint32_t *post) {
+    if (V == 0) RIKI_THROW(RIKI_EINVAL, "n_nodes must be > 0");
+    if (E >= (1ull << 32)) RIKI_THROW(RIKI_EINVAL, "n_edges must be < 2^32");
+    if (E && (!src || !dst)) RIKI_THROW(RIKI_EINVAL, "null edge arrays");
+    if (n_terms && (!tptr)) RIKI_THROW(RIKI_EINVAL, "null term_ptr");
+    for (uint64_t e = 0; e < E; e++)
+        if (src[e] >= V || dst[e] >= V) RIKI_THROW(RIKI_EINVAL, "edge " + std::to_string(e) + " endpoint out of range");
+    uint64_t P = n_terms ? tptr[n_terms] : 0;
+    if (n_terms && tptr[0] != 0) RIKI_THROW(RIKI_EINVAL, "term_ptr[0] must be 0");
+    if (P && !post) RIKI_THROW(RIKI_EINVAL, "null postings");
+    for (uint32_t t = 0; t < n_terms; t++) {
+        if (tptr[t + 1] < tptr[t]) RIKI_THROW(RIKI_EINVAL, "term_ptr not monotone");
+        for (uint64_t i = tptr[t]; i < tptr[t + 1]; i++) {
+            if (post[i] >= V) RIKI_THROW(RIKI_EINVAL, "posting node out of range (term " + std::to_string(t) + ")");
+            if (i > tptr[t] && post[i] <= post[i - 1])
+                RIKI_THROW(RIKI_EINVAL, "postings of term " + std::to_string(t) + " not sorted unique");
+        }
+    }
+    CUDA_TRY(cudaSetDevice(g->device));
+    CUDA_TRY(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+    g->V = V;
+    g->E = E;
+    g->n_terms = n_terms;
+    uint64_t *acc = &g->graph_bytes;
+    g->d_src = dmalloc<uint32_t>(E, acc);
+    g->d_dst = dmalloc<uint32_t>(E, acc);
+    g->d_cls = dmalloc<uint32_t>(E, acc);
+    g->d_act_e = dmalloc<uint8_t>(E, acc);
+    g->d_row = dmalloc<uint32_t>(V + 1, acc);
+    g->d_col = dmalloc<uint32_t>(E, acc);
+    g->d_act = dmalloc<uint8_t>(E, acc);
+    g->d_irow = dmalloc<uint32_t>(V + 1, acc);
+    g->d_isrc = dmalloc<uint32_t>(E, acc);
+    g->d_ieid = dmalloc<uint32_t>(E, acc);
+    g->d_iact = dmalloc<uint8_t>(E, acc);
+    g->d_tptr = dmalloc<uint64_t>(n_terms + 1, acc);
+    g->d_post = dmalloc<uint32_t>(P, acc);
+    cudaStream_t s = g->stream;
+    if (E) {
+        CUDA_TRY(cudaMemcpyAsync(g->d_src, src, E * 4, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(g->d_dst, dst, E * 4, cudaMemcpyHostToDevice, s));
+        if (cls) CUDA_TRY(cudaMemcpyAsync(g->d_cls, cls, E * 4, cudaMemcpyHostToDevice, s));
+        else CUDA_TRY(cudaMemsetAsync(g->d_cls, 0, E * 4, s));
+    }
+    g->h_tptr.assign(n_terms + 1, 0);
+    if (n_terms) {
+        std::copy(tptr, tptr + n_terms + 1, g->h_tptr.begin());
+        CUDA_TRY(cudaMemcpyAsync(g->d_tptr, tptr, (n_terms + 1) * 8, cudaMemcpyHostToDevice, s));
+        if (P) CUDA_TRY(cudaMemcpyAsync(g->d_post, post, P * 4, cudaMemcpyHostToDevice, s));
+    }
+    row_pointers(s, g->d_src, E, V, g->d_row);
+    row_pointers(s, g->d_dst, E, V, g->d_irow);
+    sync_check(s);
+}
+
+void graph_free(riki_graph *g) {
+    void *ps[] = {g->d_src, g->d_dst, g->d_cls, g->d_act_e, g->d_row, g->d_col, g->d_act,
+                  g->d_irow, g->d_isrc, g->d_ieid, g->d_iact, g->d_tptr, g->d_post};
+    for (void *p : ps) if (p) cudaFree(p);
+    if (g->stream) cudaStreamDestroy(g->stream);
+}
+
+static void finish_act(riki_graph *g, uint32_t *d_bad) {
+    uint32_t bad = 0;
+    CUDA_TRY(cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, g->stream));
+    sync_check(g->stream);
+    cudaFree(d_bad);
+    if (bad) RIKI_THROW(RIKI_EINVAL, "weights must lie in [0,1] (P:194)");
+    build_csr(g);
+}
+
+void graph_set_edge_weights(riki_graph *g, const double *w01, double alpha, double avg) {
+    check_params(alpha, avg);
+    if (g->E && !w01) RIKI_THROW(RIKI_EINVAL, "null weights");
+    double *dw = dmalloc<double>(g->E);
+    uint32_t *bad = dmalloc<uint32_t>(1);
+    CUDA_TRY(cudaMemsetAsync(bad, 0, 4, g->stream));
+    if (g->E) CUDA_TRY(cudaMemcpyAsync(dw, w01, g->E * 8, cudaMemcpyHostToDevice, g->stream));
+    k_coarsen_edges<<<grid_for(g->E), 256, 0, g->stream>>>(dw, g->E, alpha, avg, g->d_act_e, bad);
+    sync_check(g->stream);
+    cudaFree(dw);
+    finish_act(g, bad);
+}
+
+void graph_set_node_weights(riki_graph *g, const double *w01, double alpha, double avg) {
+    check_params(alpha, avg);
+    if (!w01) RIKI_THROW(RIKI_EINVAL, "null weights");
+    double *dw = dmalloc<double>(g->V);
+    uint32_t *bad = dmalloc<uint32_t>(1);
+    CUDA_TRY(cudaMemsetAsync(bad, 0, 4, g->stream));
+    CUDA_TRY(cudaMemcpyAsync(dw, w01, (size_t)g->V * 8, cudaMemcpyHostToDevice, g->stream));
+    k_coarsen_nodes<<<grid_for(g->E), 256, 0, g->stream>>>(dw, g->d_dst, g->E, alpha, avg, g->d_act_e, bad);
+    sync_check(g->stream);
+    cudaFree(dw);
+    finish_act(g, bad);
+}
+
+void graph_set_label_weights(riki_graph *g, double alpha, double avg) {
+    check_params(alpha, avg);
+    cudaStream_t s = g->stream;
+    uint64_t E = g->E;
+    int eb = 32 + bits_for(g->V);
+    uint32_t *co = dmalloc<uint32_t>(E), *ci = dmalloc<uint32_t>(E);
+    uint64_t *keys = dmalloc<uint64_t>(E);
+    uint32_t *vals = dmalloc<uint32_t>(E);
+    // |{e_ix : same class}| over out-edges of v_i
+    k_make_keys<<<grid_for(E), 256, 0, s>>>(g->d_src, g->d_cls, E, keys, vals);
+    sort_pairs(s, keys, vals, E, eb);
+    k_run_length<<<grid_for(E), 256, 0, s>>>(keys, vals, E, co);
+    // |{e_xj : same class}| over in-edges of v_j
+    k_make_keys<<<grid_for(E), 256, 0, s>>>(g->d_dst, g->d_cls, E, keys, vals);
+    sort_pairs(s, keys, vals, E, eb);
+    k_run_length<<<grid_for(E), 256, 0, s>>>(keys, vals, E, ci);
+    sync_check(s);
+    cudaFree(keys);
+    cudaFree(vals);
+    double *raw = dmalloc<double>(E), *w = dmalloc<double>(E), *mm = dmalloc<double>(4);
+    k_raw_weight<<<grid_for(E), 256, 0, s>>>(co, ci, E, raw);
+    size_t tmp = 0;
+    CUDA_TRY(cub::DeviceReduce::Min(nullptr, tmp, raw, mm + 2, (int64_t)E, s));
+    size_t tmp2 = 0;
+    CUDA_TRY(cub::DeviceReduce::Max(nullptr, tmp2, raw, mm + 3, (int64_t)E, s));
+    tmp = std::max(tmp, tmp2);
+    void *t = dmalloc<uint8_t>(tmp);
+    CUDA_TRY(cub::DeviceReduce::Min(t, tmp, raw, mm + 2, (int64_t)E, s));
+    CUDA_TRY(cub::DeviceReduce::Max(t, tmp, raw, mm + 3, (int64_t)E, s));
+    k_minmax_pair<<<1, 1, 0, s>>>(mm, mm + 2, mm + 3);
+    k_rescale<<<grid_for(E), 256, 0, s>>>(raw, E, mm, w);
+    uint32_t *bad = dmalloc<uint32_t>(1);
+    CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s));
+    k_coarsen_edges<<<grid_for(E), 256, 0, s>>>(w, E, alpha, avg, g->d_act_e, bad);
+    sync_check(s);
+    cudaFree(t); cudaFree(raw); cudaFree(w); cudaFree(mm); cudaFree(co); cudaFree(ci);
+    finish_act(g, bad);
+}
+
+void graph_set_act(riki_graph *g, const uint8_t *a) {
+    if (g->E && !a) RIKI_THROW(RIKI_EINVAL, "null activation array");
+    for (uint64_t e = 0; e < g->E; e++)
+        if (a[e] == 0xFF) RIKI_THROW(RIKI_EINVAL, "activation 255 is reserved");
+    if (g->E) CUDA_TRY(cudaMemcpyAsync(g->d_act_e, a, g->E, cudaMemcpyHostToDevice, g->stream));
+    sync_check(g->stream);
+    build_csr(g);
+}
+
+void graph_get_act(const riki_graph *g, uint8_t *a) {
+    if (!g->has_act) RIKI_THROW(RIKI_ENOWEIGHTS, "activation levels not set");
+    if (g->E) CUDA_TRY(cudaMemcpyAsync(a, g->d_act_e, g->E, cudaMemcpyDeviceToHost, g->stream));
+    sync_check(g->stream);
+}

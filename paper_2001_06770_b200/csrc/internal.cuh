@@ -1,0 +1,99 @@
+// internal.cuh -- libriki.so internal structures shared by graph.cu, engine.cu, api.cu.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "../../include/riki.h"
+#include "common.cuh"
+
+struct Workspace;  // engine.cu
+
+// Device view of the resident graph (P:339 CSR).  Out-rows are sorted by activation
+// ascending (then by edge id), so the Alg. 1 gate a <= l reads a row prefix.  In-rows
+// (Alg. 2 line 5, N_i) are sorted the same way and carry the forward edge's activation
+// and the caller's edge id.
+struct GraphDev {
+    uint32_t V;
+    uint64_t E;
+    const uint32_t *row, *col;  // out-CSR
+    const uint8_t *act;
+    const uint32_t *irow, *isrc, *ieid;  // in-CSR
+    const uint8_t *iact;
+    const uint32_t *src, *dst;  // caller's edge list by edge id
+    const uint64_t *tptr;       // inverted index
+    const uint32_t *post;
+};
+
+struct riki_graph {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint32_t V = 0;
+    uint64_t E = 0;
+    uint32_t n_terms = 0;
+    uint32_t *d_src = nullptr, *d_dst = nullptr, *d_cls = nullptr;
+    uint8_t *d_act_e = nullptr;  // activation by caller edge id
+    bool has_act = false;
+    uint32_t *d_row = nullptr, *d_col = nullptr;
+    uint8_t *d_act = nullptr;
+    uint32_t *d_irow = nullptr, *d_isrc = nullptr, *d_ieid = nullptr;
+    uint8_t *d_iact = nullptr;
+    uint64_t *d_tptr = nullptr;
+    uint32_t *d_post = nullptr;
+    std::vector<uint64_t> h_tptr;
+    uint64_t graph_bytes = 0;
+    Workspace *ws = nullptr;
+    bool profiling = false, debug = false;
+    uint32_t batch_slots = 0;
+    riki_stats stats{};
+
+    GraphDev dev() const {
+        GraphDev g;
+        g.V = V; g.E = E;
+        g.row = d_row; g.col = d_col; g.act = d_act;
+        g.irow = d_irow; g.isrc = d_isrc; g.ieid = d_ieid; g.iact = d_iact;
+        g.src = d_src; g.dst = d_dst; g.tptr = d_tptr; g.post = d_post;
+        return g;
+    }
+};
+
+// graph.cu
+void graph_load(riki_graph *g, uint32_t n_nodes, uint64_t n_edges, const uint32_t *src, const uint32_t *dst,
+                const uint32_t *cls, uint32_t n_terms, const uint64_t *tptr, const uint32_t *post);
+void graph_free(riki_graph *g);
+void graph_set_edge_weights(riki_graph *g, const double *w01, double alpha, double avg);
+void graph_set_node_weights(riki_graph *g, const double *w01, double alpha, double avg);
+void graph_set_label_weights(riki_graph *g, double alpha, double avg);
+void graph_set_act(riki_graph *g, const uint8_t *a);
+void graph_get_act(const riki_graph *g, uint8_t *a);
+
+// engine.cu
+struct QueryIn {
+    uint32_t nc, nm;
+    uint32_t c[RIKI_MAX_TERMS], m[RIKI_MAX_TERMS];
+};
+struct HostRPG {
+    uint32_t central_node, sc, sm;
+    double score;
+    uint8_t ptc;
+    std::vector<uint32_t> nodes, vc;
+    std::vector<uint64_t> edges;
+    uint8_t cdist[RIKI_MAX_TERMS], mdist[RIKI_MAX_TERMS];
+};
+struct riki_results {
+    uint32_t nc = 0, nm = 0;
+    std::vector<HostRPG> rpgs;
+    riki_query_stats stats{};
+    std::vector<uint64_t> cand;  // (sc << 32 | v), debug only
+};
+void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, uint32_t depth, const riki_params &p,
+                   cudaStream_t stream, std::vector<riki_results *> *out);
+void engine_search_device(riki_graph *g, uint32_t nq, const uint64_t *d_cptr, const uint32_t *d_cterms,
+                          const uint64_t *d_mptr, const uint32_t *d_mterms, uint32_t k, uint32_t depth,
+                          const riki_params &p);
+void engine_fetch(riki_graph *g, uint32_t nq, std::vector<riki_results *> *out);
+void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uint32_t depth, int block_mode,
+                           uint8_t *H_out, uint8_t *block_out, uint64_t *relax_out, int32_t *L_out);
+void engine_free(riki_graph *g);
+uint64_t engine_workspace_bytes(const riki_graph *g);
