@@ -165,6 +165,7 @@ def main():
     ap.add_argument("--ref-queries", type=int, default=4, help="oracle queries per step for --impl reference")
     ap.add_argument("--latency-queries", type=int, default=40)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="timed region only (for ncu launch lists)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -231,6 +232,11 @@ def main():
     relax = sum(r.stats["relax_central"] + r.stats["relax_marginal"] for r in res)
     n_rpg = sum(len(r.rpgs) for r in res)
 
+    if args.quick:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "ms_per_step": tot_ms / args.steps,
+                              "quick": True, "stats": st}), flush=True)
+        return
     # ---------------- e2e through the host C-ABI (H2D of queries, D2H of results inside)
     h2d = cp.nbytes + ct.nbytes + mp.nbytes + mt.nbytes
     e2e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
