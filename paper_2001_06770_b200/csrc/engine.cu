@@ -32,11 +32,9 @@ constexpr uint32_t MAX_SLOTS = 1024;
 constexpr uint32_t HEAVY = 256;  // longer active ranges are split into CHUNK-edge work items
 constexpr uint32_t CHUNK = 256;
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
-// recovery fast path (shared memory) capacities
-constexpr uint32_t CAP_U = 4096, CAP_K = 4096, CAP_Q = 4096, CAP_E = 8192;
 constexpr uint32_t SORT_SMEM = 8192;  // u32 keys sorted in shared memory
 
-enum Ctr { C_NHEAVY = 0, C_NNEWATT, C_NOVF, C_ACTIVE, C_TOTAL, C_NCAND_TOTAL, C_NCTR = 16 };
+enum Ctr { C_NHEAVY = 0, C_NNEWATT, C_NOVF, C_ACTIVE, C_TOTAL, C_NCAND_TOTAL, C_NOVF2, C_NCTR = 16 };
 enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_NPROF = 8 };
 enum Err { E_CAND = 1, E_HEAVY = 2, E_ARENA = 4, E_EXTRACT = 8, E_OUT = 16, E_UNRESOLVED = 32 };
 
@@ -88,10 +86,12 @@ struct WsDev {
     unsigned long long *prof;
     uint32_t *arena;
     unsigned long long *arena_used, arena_cap;
-    uint2 *newatt, *ovf;
+    uint2 *newatt, *ovf, *ovf2;
     uint32_t ovf_cap;
     uint32_t *big;
     unsigned long long big_words;
+    uint32_t *mkeys;
+    unsigned long long *mvals;
     OutHdr *hdr;
     uint32_t *resid;
     uint32_t *out;
@@ -179,7 +179,8 @@ template <class RowT> __global__ void k_seed(GraphDev g, WsDev w, int ph) {
     SlotState &st = w.st[s];
     if (!st.in_phase) return;
     RowT *H = w.Hs<RowT>(ph, s);
-    uint32_t T = st.T[ph];
+    const uint32_t T = st.T[ph];
+    const RowT used = used_mask<RowT>(T);
     for (uint32_t j = 0; j < T; j++) {
         uint32_t t = st.term[ph][j];
         uint64_t b = g.tptr[t], e = g.tptr[t + 1];
@@ -188,9 +189,7 @@ template <class RowT> __global__ void k_seed(GraphDev g, WsDev w, int ph) {
             RowT andm = ~((RowT)0xFF << (8 * j));
             RowT old = Row<RowT>::atomic_and(H + v, andm);
             RowT nw = old & andm;
-            uint32_t bit = 1u << (v & 31);
-            uint32_t ob = atomicOr(w.BM(s, 0) + (v >> 5), bit);
-            if (!(ob & bit)) {
+            if ((Row<RowT>::eq(old, Row<RowT>::splat(0xFF)) & used) == used) {  // first seed of this node
                 uint32_t p = atomicAdd(&st.nq[0], 1u);
                 w.Q(s, 0)[p] = v;
             }
@@ -259,12 +258,15 @@ template <class RowT> struct Relax {
     int cells;   // cells turned from inf to l+1 by this thread
 };
 
-// Relaxation of edge (f -> n) for the byte-columns in `mask` at level l (Alg. 1 lines 12-17).
-template <class RowT> __device__ __forceinline__ Relax<RowT> relax(RowT *H, uint32_t n, RowT mask, uint32_t l) {
+// Relaxation of edge (f -> n) for the byte-columns in `mask` at level l (Alg. 1 lines 12-17),
+// given the (possibly stale) row hn read earlier: one atomicAnd writes l+1 into every selected
+// byte that is still 0xFF; the old row says whether this thread is the first writer of n's row
+// at this level (enqueue) and whether it completed the row (identification at l+1, R10).
+template <class RowT>
+__device__ __forceinline__ Relax<RowT> relax(RowT *H, uint32_t n, RowT hn, RowT mask, uint32_t l) {
     typedef Row<RowT> R;
     Relax<RowT> r{false, false, 0};
     const RowT FF = R::splat(0xFF);
-    RowT hn = R::load(H + n);
     RowT need = mask & R::eq(hn, FF);
     if (!need) return r;
     RowT andm = ~need | (need & R::splat(l + 1));
@@ -277,16 +279,15 @@ template <class RowT> __device__ __forceinline__ Relax<RowT> relax(RowT *H, uint
     return r;
 }
 
-// Enqueue n into the next frontier of slot s: bit-packed frontier dedups (P:347 shared F).
-__device__ __forceinline__ void frontier_push(const WsDev &w, bool want, uint32_t s, uint32_t n, uint32_t nxt) {
-    bool app = false;
-    if (want) {
-        uint32_t bit = 1u << (n & 31);
-        uint32_t ob = atomicOr(w.BM(s, nxt) + (n >> 5), bit);
-        app = !(ob & bit);
-    }
-    uint32_t pos = warp_append(app, s, &w.st[0].nq[nxt], sizeof(SlotState) / 4);
-    if (app) w.Q(s, nxt)[pos] = n;
+// Next frontier Q_{l+1}: a node is appended by the first writer of its row at level l (new
+// entry) or, if it keeps pending edges (Alg. 1 lines 9-11), by its own item (retained entry,
+// tag bit 31).  A retained entry whose row also carries l+1 is a duplicate and is skipped by
+// the consumer, so every node of F is expanded exactly once per level without a
+// separate flag array: the level stored in H is the frontier flag.
+constexpr uint32_t RETAINED = 0x80000000u;
+__device__ __forceinline__ void frontier_push(const WsDev &w, bool want, uint32_t s, uint32_t entry, uint32_t nxt) {
+    uint32_t pos = warp_append(want, s, &w.st[0].nq[nxt], sizeof(SlotState) / 4);
+    if (want) w.Q(s, nxt)[pos] = entry;
 }
 
 __device__ __forceinline__ void cand_push(const WsDev &w, bool want, uint32_t s, uint32_t n, uint32_t level) {
@@ -300,21 +301,22 @@ __device__ __forceinline__ void cand_push(const WsDev &w, bool want, uint32_t s,
 __device__ __forceinline__ uint32_t upper_bound_act(const uint8_t *act, uint32_t lo, uint32_t hi, uint32_t l) {
     while (lo < hi) {  // first index with act > l
         uint32_t m = (lo + hi) >> 1;
-        if (act[m] <= l) lo = m + 1; else hi = m;
+        if (__ldg(act + m) <= l) lo = m + 1; else hi = m;
     }
     return lo;
 }
 __device__ __forceinline__ uint32_t lower_bound_act(const uint8_t *act, uint32_t lo, uint32_t hi, uint32_t l) {
     while (lo < hi) {  // first index with act >= l
         uint32_t m = (lo + hi) >> 1;
-        if (act[m] < l) lo = m + 1; else hi = m;
+        if (__ldg(act + m) < l) lo = m + 1; else hi = m;
     }
     return lo;
 }
 
 // Work item = one frontier node of one slot.  Each warp takes 32 items: lane i does the
 // per-node part (row bounds, CF check, retention, activation range by binary search in the
-// activation-sorted row), then the warp walks the concatenated active ranges edge-parallel.
+// activation-sorted row), then the warp walks the concatenated active ranges edge-parallel,
+// two edges in flight per lane.
 template <class RowT>
 __global__ void __launch_bounds__(256) k_expand(GraphDev g, WsDev w, int ph, uint32_t l) {
     typedef Row<RowT> R;
@@ -338,27 +340,37 @@ __global__ void __launch_bounds__(256) k_expand(GraphDev g, WsDev w, int ph, uin
     for (uint32_t base = gw * 32; base < total; base += nw * 32) {
         uint32_t item = base + lane;
         bool valid = item < total;
-        uint32_t s = 0, f = 0, lo = 0, len = 0, relaxn = 0;
+        uint32_t s = 0, f = 0, lo = 0, len = 0, relaxn = 0, eq0 = 0;
         RowT newc = 0, oldc = 0;
         bool retain = false;
         if (valid) {
             s = find_slot(s_offs, ns, item);
             uint32_t info = s_info[s];
-            f = w.Q(s, cur)[item - s_offs[s]];
+            uint32_t ent = w.Q(s, cur)[item - s_offs[s]];
+            f = ent & ~RETAINED;
             RowT *H = w.Hs<RowT>(ph, s);
             RowT Rf = R::load(H + f);
-            w.BM(s, cur)[f >> 5] = 0;  // every set bit of this word is a node of Q_l (cleared here)
+            RowT used = used_mask<RowT>(info >> 8);
+            bool dup = (ent & RETAINED) && (R::eq(Rf, L) & used);
             bool blocked = (info & 1) && R::le(Rf, L) == (RowT)~(RowT)0;  // CF: row complete, max <= l
-            if (!blocked) {
-                RowT used = used_mask<RowT>(info >> 8);
+            if (!dup && !blocked) {
                 newc = R::eq(Rf, L) & used;   // reached at level l (or seeds at l = 0)
                 oldc = R::lt(Rf, L) & used;   // reached earlier: only edges with a == l are due now
-                uint32_t rb = g.row[f], re = g.row[f + 1];
+                const uint4 d = __ldg(g.desc + f);
+                const uint32_t rb = d.x, re = d.x + d.y;
                 if (re > rb && (newc | oldc)) {
-                    retain = g.act[re - 1] > l;  // Alg. 1 lines 9-11: some a_fn > l keeps f a frontier
-                    uint32_t hi = upper_bound_act(g.act, rb, re, l);
-                    uint32_t eqlo = oldc ? lower_bound_act(g.act, rb, hi, l) : hi;
+                    uint32_t hi, eqlo;
+                    if (d.y <= 8) {  // packed activations (padding 0xFF never passes the gate)
+                        const uint32_t L4 = l * 0x01010101u;
+                        hi = rb + ((__popc(__vcmpleu4(d.z, L4)) + __popc(__vcmpleu4(d.w, L4))) >> 3);
+                        eqlo = rb + ((__popc(__vcmpltu4(d.z, L4)) + __popc(__vcmpltu4(d.w, L4))) >> 3);
+                    } else {
+                        hi = upper_bound_act(g.act, rb, re, l);
+                        eqlo = oldc ? lower_bound_act(g.act, rb, hi, l) : hi;
+                    }
+                    retain = hi < re;  // Alg. 1 lines 9-11: some a_fn > l keeps f a frontier
                     lo = newc ? rb : eqlo;
+                    eq0 = eqlo;
                     len = hi - lo;
                     relaxn = (hi - rb) * R::ones(newc) + (hi - eqlo) * R::ones(oldc);
                     if (len > HEAVY) {
@@ -377,8 +389,7 @@ __global__ void __launch_bounds__(256) k_expand(GraphDev g, WsDev w, int ph, uin
             }
             p_items++;
         }
-        // relaxation count per slot (aggregated)
-        {
+        {   // relaxation count per slot (aggregated)
             uint32_t vm = __ballot_sync(FULLMASK, valid);
             if (valid) {
                 uint32_t peers = __match_any_sync(vm, s);
@@ -386,42 +397,50 @@ __global__ void __launch_bounds__(256) k_expand(GraphDev g, WsDev w, int ph, uin
                 if (lane == __ffs(peers) - 1 && sum) atomicAdd(&w.st[s].relax[ph], (unsigned long long)sum);
             }
         }
-        frontier_push(w, retain, s, f, nxt);
+        frontier_push(w, retain, s, f | RETAINED, nxt);
         p_enq += retain;
-        // edge-parallel walk over the 32 active ranges
+        // edge-parallel walk over the 32 active ranges, two edges per lane in flight
         uint32_t incl = warp_incl_scan(len);
         uint32_t tot = __shfl_sync(FULLMASK, incl, 31);
         uint32_t excl = incl - len;
         p_edges += len;
-        for (uint32_t eb = 0; eb < tot; eb += 32) {
-            uint32_t idx = eb + lane;
-            bool ev = idx < tot;
-            // owner lane: largest i with excl_i <= idx
-            uint32_t own = 0;
+        for (uint32_t eb = 0; eb < tot; eb += 64) {
+            uint32_t n[2], o_s[2];
+            RowT mask[2], hn[2];
+            bool ev[2];
 #pragma unroll
-            for (uint32_t step = 16; step > 0; step >>= 1) {
-                uint32_t cand = own + step;
-                uint32_t ex = __shfl_sync(FULLMASK, excl, cand);
-                if (ex <= idx) own = cand;
-            }
-            uint32_t o_lo = __shfl_sync(FULLMASK, lo, own);
-            uint32_t o_ex = __shfl_sync(FULLMASK, excl, own);
-            uint32_t o_s = __shfl_sync(FULLMASK, s, own);
-            RowT o_new = shfl(newc, own), o_old = shfl(oldc, own);
-            Relax<RowT> r{false, false, 0};
-            uint32_t n = 0;
-            if (ev) {
+            for (int u = 0; u < 2; u++) {
+                uint32_t idx = eb + 32 * u + lane;
+                ev[u] = idx < tot;
+                uint32_t own = 0;  // owner lane: largest i with excl_i <= idx
+#pragma unroll
+                for (uint32_t step = 16; step > 0; step >>= 1) {
+                    uint32_t cand = own + step;
+                    if (__shfl_sync(FULLMASK, excl, cand) <= idx) own = cand;
+                }
+                uint32_t o_lo = __shfl_sync(FULLMASK, lo, own);
+                uint32_t o_ex = __shfl_sync(FULLMASK, excl, own);
+                uint32_t o_eq = __shfl_sync(FULLMASK, eq0, own);
+                o_s[u] = __shfl_sync(FULLMASK, s, own);
+                RowT o_new = shfl(newc, own), o_old = shfl(oldc, own);
                 uint32_t e = o_lo + (idx - o_ex);
-                n = g.col[e];
-                uint32_t a = g.act[e];
-                RowT mask = o_new | (a == l ? o_old : (RowT)0);
-                r = relax<RowT>(w.Hs<RowT>(ph, o_s), n, mask, l);
-                p_cells += r.cells;
-                p_enq += r.enq;
+                n[u] = ev[u] ? __ldg(g.col + e) : 0;
+                mask[u] = o_new | (e >= o_eq ? o_old : (RowT)0);  // [eqlo, hi) are the edges with a == l
             }
-            frontier_push(w, r.enq, o_s, n, nxt);
-            bool id = r.ident && ((s_info[ev ? o_s : 0] >> 1) & 1);
-            cand_push(w, id, o_s, n, l + 1);
+#pragma unroll
+            for (int u = 0; u < 2; u++) hn[u] = ev[u] ? R::load(w.Hs<RowT>(ph, o_s[u]) + n[u]) : (RowT)0;
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                Relax<RowT> r{false, false, 0};
+                if (ev[u]) {
+                    r = relax<RowT>(w.Hs<RowT>(ph, o_s[u]), n[u], hn[u], mask[u], l);
+                    p_cells += r.cells;
+                    p_enq += r.enq;
+                }
+                frontier_push(w, r.enq, o_s[u], n[u], nxt);
+                bool id = r.ident && ((s_info[ev[u] ? o_s[u] : 0] >> 1) & 1);
+                cand_push(w, id, o_s[u], n[u], l + 1);
+            }
         }
     }
     p_items = warp_sum(p_items);
@@ -436,7 +455,7 @@ __global__ void __launch_bounds__(256) k_expand(GraphDev g, WsDev w, int ph, uin
     }
 }
 
-// Heavy ranges (hub rows): one warp per CHUNK-edge piece.
+// Heavy ranges (hub rows): one warp per CHUNK-edge piece, two edges per lane in flight.
 template <class RowT> __global__ void __launch_bounds__(256) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l) {
     typedef Row<RowT> R;
     const uint32_t lane = lane_id();
@@ -455,20 +474,29 @@ template <class RowT> __global__ void __launch_bounds__(256) k_expand_heavy(Grap
         RowT Rf = R::load(H + h.y);  // values <= l are final; concurrent l+1 writes don't change the masks
         RowT newc = R::eq(Rf, L) & used, oldc = R::lt(Rf, L) & used;
         bool collect = st.collect;
-        for (uint32_t e0 = h.z; e0 < h.w; e0 += 32) {
-            uint32_t e = e0 + lane;
-            Relax<RowT> r{false, false, 0};
-            uint32_t n = 0;
-            if (e < h.w) {
-                n = g.col[e];
-                uint32_t a = g.act[e];
-                RowT mask = newc | (a == l ? oldc : (RowT)0);
-                r = relax<RowT>(H, n, mask, l);
-                p_cells += r.cells;
-                p_enq += r.enq;
+        for (uint32_t e0 = h.z; e0 < h.w; e0 += 64) {
+            uint32_t n[2], a[2];
+            RowT hn[2];
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                uint32_t e = e0 + 32 * u + lane;
+                n[u] = e < h.w ? __ldg(g.col + e) : 0;
+                a[u] = e < h.w ? __ldg(g.act + e) : 0xFF;
             }
-            frontier_push(w, r.enq, s, n, nxt);
-            cand_push(w, r.ident && collect, s, n, l + 1);
+#pragma unroll
+            for (int u = 0; u < 2; u++) hn[u] = (e0 + 32 * u + lane < h.w) ? R::load(H + n[u]) : (RowT)0;
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                Relax<RowT> r{false, false, 0};
+                if (e0 + 32 * u + lane < h.w) {
+                    RowT mask = newc | (a[u] == l ? oldc : (RowT)0);
+                    r = relax<RowT>(H, n[u], hn[u], mask, l);
+                    p_cells += r.cells;
+                    p_enq += r.enq;
+                }
+                frontier_push(w, r.enq, s, n[u], nxt);
+                cand_push(w, r.ident && collect, s, n[u], l + 1);
+            }
         }
     }
     p_cells = warp_sum(p_cells);
@@ -477,17 +505,6 @@ template <class RowT> __global__ void __launch_bounds__(256) k_expand_heavy(Grap
         atomicAdd(&w.prof[P_NEWCELLS], p_cells);
         atomicAdd(&w.prof[P_ENQ], p_enq);
     }
-}
-
-// Clear the bits of the last (unexpanded) frontier so the bitmaps are zero for reuse.
-__global__ void k_clear_bm(WsDev w, int ph) {
-    uint32_t s = blockIdx.y;
-    const SlotState &st = w.st[s];
-    if (st.L_end[ph] < 0) return;
-    uint32_t b = (uint32_t)st.L_end[ph] & 1;
-    uint32_t n = st.nq[b];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        w.BM(s, b)[w.Q(s, b)[i] >> 5] = 0;
 }
 
 // ====================================================================== candidates
@@ -551,80 +568,185 @@ __global__ void k_scan_cands(WsDev w) {
         w.coffs[w.nslots] = sc[MAX_SLOTS - 1];
         w.ctr[C_NCAND_TOTAL] = sc[MAX_SLOTS - 1];
         w.ctr[C_NOVF] = 0;
+        w.ctr[C_NOVF2] = 0;
     }
 }
 
 // ====================================================================== recovery (Alg. 2)
+// Hash set of node ids that records its insertions (items = insertion order, slots = where
+// they live), so clearing and enumerating cost O(inserted), not O(capacity).
+struct HSet {
+    uint32_t *keys, *items, *slots;
+    uint32_t cap, items_cap;  // cap: power of two
+    uint32_t *count;          // shared/global counter
+    __device__ __forceinline__ int insert(uint32_t k, uint32_t *ovf) const {
+        uint32_t h = HashSet::hash(k) & (cap - 1);
+        for (uint32_t i = 0; i < cap; i++) {
+            uint32_t sl = (h + i) & (cap - 1);
+            uint32_t prev = atomicCAS(&keys[sl], EMPTY, k);
+            if (prev == EMPTY) {
+                uint32_t idx = atomicAdd(count, 1u);
+                if (idx < items_cap) { items[idx] = k; slots[idx] = sl; } else *ovf = 1;
+                return 1;
+            }
+            if (prev == k) return 0;
+        }
+        *ovf = 1;
+        return -1;
+    }
+    __device__ __forceinline__ int find(uint32_t k) const {
+        uint32_t h = HashSet::hash(k) & (cap - 1);
+        for (uint32_t i = 0; i < cap; i++) {
+            uint32_t sl = (h + i) & (cap - 1);
+            uint32_t v = keys[sl];
+            if (v == k) return (int)sl;
+            if (v == EMPTY) return -1;
+        }
+        return -1;
+    }
+    // CTA-wide; call with all threads, followed by __syncthreads by the caller
+    __device__ __forceinline__ void clear_inserted(bool full) const {
+        uint32_t n = min(*count, items_cap);
+        if (full) for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) keys[i] = EMPTY;
+        else for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) keys[slots[i]] = EMPTY;
+    }
+};
+
 struct ExBuf {
-    uint32_t *hu, *hk, *queue, *edges, *uf;
+    HSet hu, hk;          // union of nodes; per-keyword visited set whose items are the BFS queue
+    uint32_t *edges, *uf;
     uint8_t *flag;
-    uint32_t cap_u, cap_k, cap_q, cap_e;
+    uint32_t cap_e;
 };
 struct ExShared {
-    uint32_t qtail, nedges, nnodes, ovf;
-    uint32_t cnt, off, off2, mnr, mxr, nx, xvc, pass;
+    uint32_t nu, nk, nedges, ovf;
+    uint32_t cnt, off, mnr, mxr, nx, xvc;
+    uint32_t dirty;  // tables may hold unrecorded entries (after an overflow): full clear needed
 };
 
-__device__ __forceinline__ void hs_clear(uint32_t *h, uint32_t cap) {
-    for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) h[i] = EMPTY;
+// ---- memoised recovery DAG.  The Alg. 2 predicate (Lemma recover P:553 + R16) does not
+// depend on the candidate, so the predecessor list of (slot, phase, column j, node q) is
+// computed once and shared by every candidate of the query through a per-slot map with a
+// claim/publish protocol (a claimer never waits, so spinning readers always progress).
+constexpr uint32_t MAPCAP = 8192;
+constexpr unsigned long long NOT_READY = ~0ull;
+
+template <class RowT>
+__device__ void dag_list(const GraphDev &g, const WsDev &w, uint32_t s, int ph, int j, const RowT *H, bool blocking,
+                         uint32_t q, uint32_t hq, uint32_t *off_out, uint32_t *cnt_out) {
+    typedef Row<RowT> R;
+    const uint32_t lane = lane_id();
+    const size_t mi = ((size_t)s * 16 + ph * 8 + j) * MAPCAP;
+    uint32_t *keys = w.mkeys + mi;
+    unsigned long long *vals = w.mvals + mi;
+    int state = 0;  // 0 full (compute, no cache), 1 claimed (compute + publish), 2 found
+    uint32_t slot = 0;
+    if (lane == 0) {
+        uint32_t h = HashSet::hash(q) & (MAPCAP - 1);
+        for (uint32_t i = 0; i < 64; i++) {  // bounded probe: a full neighbourhood just disables caching
+            uint32_t sl = (h + i) & (MAPCAP - 1);
+            uint32_t prev = atomicCAS(&keys[sl], EMPTY, q);
+            if (prev == EMPTY) { state = 1; slot = sl; break; }
+            if (prev == q) { state = 2; slot = sl; break; }
+        }
+    }
+    state = __shfl_sync(FULLMASK, state, 0);
+    slot = __shfl_sync(FULLMASK, slot, 0);
+    if (state == 2) {
+        unsigned long long v = 0;
+        if (lane == 0) {
+            volatile unsigned long long *vv = vals + slot;
+            while ((v = *vv) == NOT_READY) __nanosleep(64);
+            __threadfence();
+        }
+        v = __shfl_sync(FULLMASK, v, 0);
+        *off_out = (uint32_t)(v >> 32);
+        *cnt_out = (uint32_t)v;
+        return;
+    }
+    uint32_t rb = g.irow[q], re = g.irow[q + 1];
+    uint32_t hi = 0;
+    if (lane == 0) hi = upper_bound_act(g.iact, rb, re, hq - 1);  // in-rows are activation-sorted
+    hi = __shfl_sync(FULLMASK, hi, 0);
+    uint32_t off = 0;
+    if (lane == 0) {
+        unsigned long long p = atomicAdd(w.arena_used, 2ull * (hi - rb));
+        if (p + 2ull * (hi - rb) > w.arena_cap) { atomicOr(&w.st[s].err, (uint32_t)E_ARENA); off = EMPTY; }
+        else off = (uint32_t)p;
+    }
+    off = __shfl_sync(FULLMASK, off, 0);
+    uint32_t cnt = 0;
+    if (off != EMPTY) {
+        for (uint32_t k0 = rb; k0 < hi; k0 += 128) {
+            uint32_t n[4], a[4], hn[4];
+            RowT Rn[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                uint32_t k = k0 + u * 32 + lane;
+                n[u] = k < hi ? g.isrc[k] : 0;
+                a[u] = k < hi ? g.iact[k] : 0xFF;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) Rn[u] = (k0 + u * 32 + lane < hi) ? R::load(H + n[u]) : R::splat(0xFF);
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                uint32_t k = k0 + u * 32 + lane;
+                hn[u] = R::byte(Rn[u], j);
+                bool ok = false;
+                if (k < hi && hn[u] != 0xFF) {
+                    uint32_t Lr = max(hn[u], a[u]);
+                    if (Lr + 1 == hq) {
+                        uint32_t blk = 0xFF;
+                        if (blocking && R::eq(Rn[u], R::splat(0xFF)) == 0) blk = R::maxb(Rn[u]);
+                        ok = Lr < blk;
+                    }
+                }
+                uint32_t m = __ballot_sync(FULLMASK, ok);
+                if (ok) {
+                    uint32_t p = off + 2 * (cnt + __popc(m & lanemask_lt()));
+                    w.arena[p] = n[u] | (hn[u] == 0 ? 0x80000000u : 0u);
+                    w.arena[p + 1] = g.ieid[k];
+                }
+                cnt += __popc(m);
+            }
+        }
+    }
+    if (state == 1 && lane == 0) {
+        __threadfence();
+        atomicExch(vals + slot, off == EMPTY ? 0ull : ((unsigned long long)off << 32 | cnt));
+    }
+    *off_out = off == EMPTY ? 0 : off;
+    *cnt_out = off == EMPTY ? 0 : cnt;
 }
 
-// Reverse BFS for keyword column j (Alg. 2 lines 4-10) over the in-CSR.  Edge (n -> q) is
-// recovered iff h_nj finite, h_qj = max(h_nj, a) + 1 (Lemma recover) and
-// max(h_nj, a) < block[n] (n really expanded over it, R16); n is continued from iff
-// h_nj != 0 and not yet visited (R17).  In-rows are activation-sorted, so a row is cut
-// at the first a > h_qj - 1.  queue[0..nsrc) holds the sources (already in hk and hu).
+// Reverse BFS for keyword column j (Alg. 2 lines 4-10): edge (n -> q) is recovered iff it
+// is in q's DAG list; n is continued from iff h_nj != 0 (line 10) and unvisited (R17).
+// hk.items (the queue) holds the sources on entry.
 template <class RowT>
-__device__ void bfs_column(const GraphDev &g, const RowT *H, bool blocking, int j, uint32_t nsrc, const ExBuf &b,
-                           ExShared &sh) {
+__device__ void bfs_column(const GraphDev &g, const WsDev &w, uint32_t s, int ph, int j, const RowT *H,
+                           bool blocking, const ExBuf &b, ExShared &sh) {
     typedef Row<RowT> R;
     const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    HashSet hu{b.hu, b.cap_u}, hk{b.hk, b.cap_k};
-    uint32_t head = 0, tail = nsrc;
+    uint32_t head = 0, tail = min(sh.nk, b.hk.items_cap);
     while (head < tail) {
         for (uint32_t it = head + warp; it < tail; it += nw) {
-            uint32_t q = b.queue[it];
+            uint32_t q = b.hk.items[it];
             uint32_t hq = R::byte(R::load(H + q), j);
             if (hq == 0 || hq == 0xFF) continue;
-            uint32_t rb = g.irow[q], re = g.irow[q + 1];
-            for (uint32_t k0 = rb; k0 < re; k0 += 32) {
-                uint32_t k = k0 + lane;
-                uint32_t a = k < re ? g.iact[k] : 0xFFu;
-                if (__shfl_sync(FULLMASK, a, 0) > hq - 1) break;
-                bool ok = false;
-                uint32_t n = 0, hn = 0xFF;
-                if (a <= hq - 1) {
-                    n = g.isrc[k];
-                    RowT Rn = R::load(H + n);
-                    hn = R::byte(Rn, j);
-                    if (hn != 0xFF) {
-                        uint32_t Lr = max(hn, a);
-                        if (Lr + 1 == hq) {
-                            uint32_t blk = 0xFF;
-                            if (blocking && R::eq(Rn, R::splat(0xFF)) == 0) blk = R::maxb(Rn);
-                            ok = Lr < blk;
-                        }
-                    }
-                }
-                if (ok) {
-                    uint32_t pos = atomicAdd(&sh.nedges, 1u);
-                    if (pos < b.cap_e) b.edges[pos] = g.ieid[k]; else sh.ovf = 1;
-                    int r = hu.insert(n);
-                    if (r < 0) sh.ovf = 1; else if (r == 1) atomicAdd(&sh.nnodes, 1u);
-                    if (hn != 0) {
-                        int r2 = hk.insert(n);
-                        if (r2 < 0) sh.ovf = 1;
-                        else if (r2 == 1) {
-                            uint32_t p = atomicAdd(&sh.qtail, 1u);
-                            if (p < b.cap_q) b.queue[p] = n; else sh.ovf = 1;
-                        }
-                    }
-                }
+            uint32_t off, cnt;
+            dag_list<RowT>(g, w, s, ph, j, H, blocking, q, hq, &off, &cnt);
+            for (uint32_t t = lane; t < cnt; t += 32) {
+                uint32_t nx = w.arena[off + 2 * t], eid = w.arena[off + 2 * t + 1];
+                uint32_t n = nx & 0x7FFFFFFFu;
+                uint32_t pos = atomicAdd(&sh.nedges, 1u);
+                if (pos < b.cap_e) b.edges[pos] = eid; else sh.ovf = 1;
+                b.hu.insert(n, &sh.ovf);
+                if (!(nx >> 31)) b.hk.insert(n, &sh.ovf);
             }
         }
         __syncthreads();
         head = tail;
-        tail = min(sh.qtail, b.cap_q);
+        tail = min(sh.nk, b.hk.items_cap);
         bool stop = sh.ovf;
         __syncthreads();
         if (stop) break;
@@ -640,6 +762,21 @@ __device__ __forceinline__ uint32_t arena_alloc(const WsDev &w, uint32_t words, 
     return (uint32_t)p;
 }
 
+__device__ __forceinline__ void ex_reset(const ExBuf &b, ExShared &sh) {
+    bool full = sh.dirty;
+    b.hu.clear_inserted(full);
+    b.hk.clear_inserted(full);
+    __syncthreads();
+    if (threadIdx.x == 0) { sh.nu = 0; sh.nk = 0; sh.nedges = 0; sh.ovf = 0; sh.dirty = 0; }
+    __syncthreads();
+}
+__device__ __forceinline__ void ex_reset_hk(const ExBuf &b, ExShared &sh) {
+    b.hk.clear_inserted(sh.dirty != 0);
+    __syncthreads();
+    if (threadIdx.x == 0) sh.nk = 0;
+    __syncthreads();
+}
+
 // CG of candidate (s, c): union over central keywords of the recovered SP(c_j, v~).
 // Writes nodes, edge ids and V_C (nodes holding a central keyword) to the arena.
 template <class RowC> __device__ void extract_cg(const GraphDev &g, const WsDev &w, uint32_t s, uint32_t c,
@@ -648,120 +785,138 @@ template <class RowC> __device__ void extract_cg(const GraphDev &g, const WsDev 
     const SlotState &st = w.st[s];
     Cand &cd = w.CD(s)[c];
     const RowC *H = w.Hs<RowC>(0, s);
-    uint32_t T = st.T[0];
-    hs_clear(b.hu, b.cap_u);
-    if (threadIdx.x == 0) { sh.nedges = 0; sh.nnodes = 0; sh.ovf = 0; }
-    __syncthreads();
-    if (threadIdx.x == 0) { HashSet{b.hu, b.cap_u}.insert(cd.v); sh.nnodes = 1; }
+    const uint32_t T = st.T[0];
+    const uint32_t v = cd.v;
+    if (threadIdx.x == 0) b.hu.insert(v, &sh.ovf);
     for (uint32_t j = 0; j < T; j++) {
-        hs_clear(b.hk, b.cap_k);
+        if (threadIdx.x == 0) b.hk.insert(v, &sh.ovf);
         __syncthreads();
-        if (threadIdx.x == 0) { HashSet{b.hk, b.cap_k}.insert(cd.v); b.queue[0] = cd.v; sh.qtail = 1; }
-        __syncthreads();
-        bfs_column<RowC>(g, H, true, j, 1, b, sh);
-        __syncthreads();
+        bfs_column<RowC>(g, w, s, 0, j, H, true, b, sh);
         if (sh.ovf) break;
+        ex_reset_hk(b, sh);
     }
     __syncthreads();
     if (sh.ovf) { *overflow = true; return; }
     *overflow = false;
-    // V_C count
+    const uint32_t nn = min(sh.nu, b.hu.items_cap), ne = min(sh.nedges, b.cap_e);
     RowC used = used_mask<RowC>(T);
     if (threadIdx.x == 0) sh.cnt = 0;
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < b.cap_u; i += blockDim.x) {
-        uint32_t v = b.hu[i];
-        if (v != EMPTY && (R::eq(R::load(H + v), 0) & used)) atomicAdd(&sh.cnt, 1u);
-    }
+    for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x)
+        if (R::eq(R::load(H + b.hu.items[i]), 0) & used) atomicAdd(&sh.cnt, 1u);
     __syncthreads();
-    uint32_t nn = sh.nnodes, ne = min(sh.nedges, b.cap_e), nvc = sh.cnt;
-    if (threadIdx.x == 0) {
-        sh.off = arena_alloc(w, nn + ne + nvc, s);
-        sh.nnodes = 0;
-        sh.cnt = 0;
-    }
+    const uint32_t nvc = sh.cnt;
+    if (threadIdx.x == 0) { sh.off = arena_alloc(w, nn + ne + nvc, s); sh.cnt = 0; }
     __syncthreads();
-    uint32_t off = sh.off;
-    if (off == EMPTY) return;
-    for (uint32_t i = threadIdx.x; i < b.cap_u; i += blockDim.x) {
-        uint32_t v = b.hu[i];
-        if (v == EMPTY) continue;
-        uint32_t p = atomicAdd(&sh.nnodes, 1u);
-        w.arena[off + p] = v;
-        if (R::eq(R::load(H + v), 0) & used) {
-            uint32_t pv = atomicAdd(&sh.cnt, 1u);
-            w.arena[off + nn + ne + pv] = v;
+    const uint32_t off = sh.off;
+    if (off != EMPTY) {
+        for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
+            uint32_t x = b.hu.items[i];
+            w.arena[off + i] = x;
+            if (R::eq(R::load(H + x), 0) & used) w.arena[off + nn + ne + atomicAdd(&sh.cnt, 1u)] = x;
         }
+        for (uint32_t i = threadIdx.x; i < ne; i += blockDim.x) w.arena[off + nn + i] = b.edges[i];
     }
-    for (uint32_t i = threadIdx.x; i < ne; i += blockDim.x) w.arena[off + nn + i] = b.edges[i];
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && off != EMPTY) {
         cd.nodes_off = off; cd.n_nodes = nn;
         cd.edges_off = off + nn; cd.n_edges = ne;
         cd.vc_off = off + nn + ne; cd.n_vc = nvc;
     }
 }
 
-__device__ __forceinline__ ExBuf smem_buf(uint8_t *sm) {
+// shared-memory tiers: 0 = small (64 threads, 15 KB), 1 = medium (256 threads, 58 KB);
+// a candidate that overflows a tier is re-run by the next one, the last tier being global
+// scratch sized by V (big_buf), so recovery is exact for any size.
+template <int TIER> struct Tier;
+template <> struct Tier<0> { static constexpr uint32_t FU = 512, FUI = 256, FK = 512, FKI = 256, FE = 1024, THREADS = 64; };
+template <> struct Tier<1> { static constexpr uint32_t FU = 2048, FUI = 1024, FK = 2048, FKI = 1024, FE = 4096, THREADS = 256; };
+template <int TIER> constexpr size_t smem_ex() {
+    return (size_t)(Tier<TIER>::FU + 2 * Tier<TIER>::FUI + Tier<TIER>::FK + 2 * Tier<TIER>::FKI + Tier<TIER>::FE +
+                    Tier<TIER>::FU) * 4 + Tier<TIER>::FU;
+}
+
+template <int TIER> __device__ __forceinline__ ExBuf smem_buf(uint8_t *sm, ExShared &sh) {
+    typedef Tier<TIER> C;
+    uint32_t *p = (uint32_t *)sm;
     ExBuf b;
-    b.hu = (uint32_t *)sm; b.cap_u = CAP_U;
-    b.hk = b.hu + CAP_U; b.cap_k = CAP_K;
-    b.queue = b.hk + CAP_K; b.cap_q = CAP_Q;
-    b.edges = b.queue + CAP_Q; b.cap_e = CAP_E;
-    b.uf = b.edges + CAP_E;
-    b.flag = (uint8_t *)(b.uf + CAP_U);
+    b.hu = HSet{p, p + C::FU, p + C::FU + C::FUI, C::FU, C::FUI, &sh.nu};
+    p += C::FU + 2 * C::FUI;
+    b.hk = HSet{p, p + C::FK, p + C::FK + C::FKI, C::FK, C::FKI, &sh.nk};
+    p += C::FK + 2 * C::FKI;
+    b.edges = p; b.cap_e = C::FE;
+    p += C::FE;
+    b.uf = p;
+    b.flag = (uint8_t *)(p + C::FU);
     return b;
 }
-constexpr size_t SMEM_EX = (size_t)(CAP_U + CAP_K + CAP_Q + CAP_E + CAP_U) * 4 + CAP_U;
 
-__device__ __forceinline__ ExBuf big_buf(const WsDev &w, uint32_t cta) {
+__device__ __forceinline__ ExBuf big_buf(const WsDev &w, uint32_t cta, ExShared &sh) {
     // global scratch for the overflow path; capacities scale with V
-    uint64_t per = w.big_words;
-    uint32_t *p = w.big + per * cta;
-    uint32_t cu = next_pow2(2 * w.V + 2);
+    uint32_t *p = w.big + w.big_words * cta;
+    const uint32_t cu = next_pow2(2 * w.V + 2), ni = w.V + 1;
     ExBuf b;
-    b.hu = p; b.cap_u = cu;
-    b.hk = b.hu + cu; b.cap_k = cu;
-    b.queue = b.hk + cu; b.cap_q = w.V + 1;
-    b.uf = b.queue + (w.V + 1);
-    b.flag = (uint8_t *)(b.uf + cu);
-    b.edges = (uint32_t *)(b.flag + cu + 16);
-    b.edges = (uint32_t *)(((uintptr_t)b.edges + 15) & ~(uintptr_t)15);
-    unsigned long long rem = per - (unsigned long long)(b.edges - p);
+    b.hu = HSet{p, p + cu, p + cu + ni, cu, ni, &sh.nu};
+    p += cu + 2 * ni;
+    b.hk = HSet{p, p + cu, p + cu + ni, cu, ni, &sh.nk};
+    p += cu + 2 * ni;
+    b.uf = p;
+    p += cu;
+    b.flag = (uint8_t *)p;
+    p += cu / 4 + 4;
+    b.edges = p;
+    unsigned long long rem = w.big_words - (unsigned long long)(p - (w.big + w.big_words * cta));
     b.cap_e = (uint32_t)(rem < 0xFFFFFFFFull ? rem : 0xFFFFFFFFull);
     return b;
 }
 
-template <class RowC> __global__ void __launch_bounds__(256) k_extract_cg(GraphDev g, WsDev w) {
+__device__ __forceinline__ void ex_init(const ExBuf &b, ExShared &sh) {
+    if (threadIdx.x == 0) sh.dirty = 1;
+    __syncthreads();
+    ex_reset(b, sh);
+}
+
+// Tier 0 takes the candidates from the flattened (slot, candidate) range; tier 1 and the
+// global tier take the overflow list of the previous tier.
+template <class RowC, int TIER> __global__ void __launch_bounds__(Tier<TIER>::THREADS) k_extract_cg(GraphDev g, WsDev w) {
     extern __shared__ __align__(16) uint8_t smx[];
     __shared__ ExShared sh;
-    ExBuf b = smem_buf(smx);
-    uint32_t total = w.coffs[w.nslots];
+    uint32_t total = TIER == 0 ? w.coffs[w.nslots] : min(w.ctr[C_NOVF], w.ovf_cap);
+    if (blockIdx.x >= total) return;
+    ExBuf b = smem_buf<TIER>(smx, sh);
+    ex_init(b, sh);
     for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
-        uint32_t s = find_slot(w.coffs, w.nslots, item);
-        uint32_t c = item - w.coffs[s];
+        uint32_t s, c;
+        if (TIER == 0) { s = find_slot(w.coffs, w.nslots, item); c = item - w.coffs[s]; }
+        else { uint2 x = w.ovf[item]; s = x.x; c = x.y; }
         bool ovf = false;
         extract_cg<RowC>(g, w, s, c, b, sh, &ovf);
         if (ovf && threadIdx.x == 0) {
-            uint32_t p = atomicAdd(&w.ctr[C_NOVF], 1u);
-            if (p < w.ovf_cap) w.ovf[p] = make_uint2(s, c); else atomicOr(&w.st[s].err, (uint32_t)E_EXTRACT);
+            sh.dirty = 1;
+            uint32_t *ctr = &w.ctr[TIER == 0 ? C_NOVF : C_NOVF2];
+            uint2 *lst = TIER == 0 ? w.ovf : w.ovf2;
+            uint32_t p = atomicAdd(ctr, 1u);
+            if (p < w.ovf_cap) lst[p] = make_uint2(s, c); else atomicOr(&w.st[s].err, (uint32_t)E_EXTRACT);
         }
         __syncthreads();
+        ex_reset(b, sh);
     }
 }
 
 template <class RowC> __global__ void __launch_bounds__(256) k_extract_cg_big(GraphDev g, WsDev w) {
     __shared__ ExShared sh;
-    ExBuf b = big_buf(w, blockIdx.x);
-    uint32_t n = min(w.ctr[C_NOVF], w.ovf_cap);
+    uint32_t n = min(w.ctr[C_NOVF2], w.ovf_cap);
+    if (blockIdx.x >= n) return;
+    ExBuf b = big_buf(w, blockIdx.x, sh);
+    ex_init(b, sh);
     for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-        uint2 sc = w.ovf[i];
+        uint2 sc = w.ovf2[i];
         bool ovf = false;
         extract_cg<RowC>(g, w, sc.x, sc.y, b, sh, &ovf);
-        if (ovf && threadIdx.x == 0) atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT);
+        if (ovf && threadIdx.x == 0) { sh.dirty = 1; atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT); }
         __syncthreads();
+        ex_reset(b, sh);
     }
-    if (threadIdx.x == 0 && blockIdx.x == 0) {}  // counter reset by the next scan/attach
 }
 
 // ====================================================================== run 2: attach, RPG, PTC
@@ -817,7 +972,7 @@ __device__ __forceinline__ void uf_union(uint32_t *uf, uint32_t a, uint32_t b) {
 }
 
 // RPG of an attached candidate: G^r = CG u (u_i SP(m_i, V_C)) recovered from the V_C nodes
-// at distance D_gi (R18), then PTC (R19/R19').
+// at distance D_gi (R18), then PTC (R19').
 template <class RowM> __device__ void extract_rpg(const GraphDev &g, const WsDev &w, uint32_t s, uint32_t c,
                                                   const ExBuf &b, ExShared &sh, bool *overflow) {
     typedef Row<RowM> R;
@@ -826,61 +981,53 @@ template <class RowM> __device__ void extract_rpg(const GraphDev &g, const WsDev
     const RowM *H = w.Hs<RowM>(1, s);
     const uint32_t T = st.T[1];
     const bool blocking = T >= 2;
-    HashSet hu{b.hu, b.cap_u};
-    hs_clear(b.hu, b.cap_u);
-    if (threadIdx.x == 0) { sh.nedges = 0; sh.nnodes = 0; sh.ovf = 0; }
-    __syncthreads();
-    if (cd.n_nodes > b.cap_u / 2 || cd.n_edges > b.cap_e) { *overflow = true; return; }
-    for (uint32_t i = threadIdx.x; i < cd.n_nodes; i += blockDim.x) {
-        int r = hu.insert(w.arena[cd.nodes_off + i]);
-        if (r == 1) atomicAdd(&sh.nnodes, 1u);
+    if (cd.n_nodes > b.hu.items_cap || cd.n_nodes * 2 > b.hu.cap || cd.n_edges > b.cap_e) {
+        *overflow = true;
+        return;
     }
+    for (uint32_t i = threadIdx.x; i < cd.n_nodes; i += blockDim.x) b.hu.insert(w.arena[cd.nodes_off + i], &sh.ovf);
     for (uint32_t i = threadIdx.x; i < cd.n_edges; i += blockDim.x) b.edges[i] = w.arena[cd.edges_off + i];
     if (threadIdx.x == 0) sh.nedges = cd.n_edges;
     __syncthreads();
-    for (uint32_t j = 0; j < T; j++) {
-        hs_clear(b.hk, b.cap_k);
-        if (threadIdx.x == 0) sh.qtail = 0;
-        __syncthreads();
-        uint32_t dj = cd.mdist[j];
+    for (uint32_t j = 0; j < T && !sh.ovf; j++) {
+        const uint32_t dj = cd.mdist[j];
         for (uint32_t t = threadIdx.x; t < cd.n_vc; t += blockDim.x) {
             uint32_t v = w.arena[cd.vc_off + t];
-            if (R::byte(R::load(H + v), j) == dj) {
-                if (HashSet{b.hk, b.cap_k}.insert(v) < 0) sh.ovf = 1;
-                uint32_t p = atomicAdd(&sh.qtail, 1u);
-                if (p < b.cap_q) b.queue[p] = v; else sh.ovf = 1;
-            }
+            if (R::byte(R::load(H + v), j) == dj) b.hk.insert(v, &sh.ovf);
         }
         __syncthreads();
-        uint32_t nsrc = min(sh.qtail, b.cap_q);
-        if (!sh.ovf) bfs_column<RowM>(g, H, blocking, j, nsrc, b, sh);
+        if (!sh.ovf) bfs_column<RowM>(g, w, s, 1, j, H, blocking, b, sh);
         __syncthreads();
         if (sh.ovf) break;
+        ex_reset_hk(b, sh);
     }
     __syncthreads();
     if (sh.ovf) { *overflow = true; return; }
     *overflow = false;
-    const uint32_t ne = min(sh.nedges, b.cap_e);
+    const uint32_t nn = min(sh.nu, b.hu.items_cap), ne = min(sh.nedges, b.cap_e);
     // ---- PTC: |M| = 1 trivial; else two distinct marginal keyword nodes X whose
     // every simple connection in G^r passes through V_C (endpoint-inclusive, R19').
     uint32_t pass = 1;
     if (T >= 2) {
         RowM used = used_mask<RowM>(T);
-        for (uint32_t i = threadIdx.x; i < b.cap_u; i += blockDim.x) { b.flag[i] = 0; b.uf[i] = i; }
+        for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
+            uint32_t sl = b.hu.slots[i];
+            b.flag[sl] = 0;
+            b.uf[sl] = sl;
+        }
         if (threadIdx.x == 0) { sh.nx = 0; sh.xvc = 0; sh.mnr = EMPTY; sh.mxr = 0; }
         __syncthreads();
         for (uint32_t t = threadIdx.x; t < cd.n_vc; t += blockDim.x) {
-            int sl = hu.find(w.arena[cd.vc_off + t]);
+            int sl = b.hu.find(w.arena[cd.vc_off + t]);
             if (sl >= 0) b.flag[sl] = 1;
         }
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < b.cap_u; i += blockDim.x) {
-            uint32_t v = b.hu[i];
-            if (v == EMPTY) continue;
-            if (R::eq(R::load(H + v), 0) & used) {
-                b.flag[i] |= 2;
+        for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
+            uint32_t sl = b.hu.slots[i];
+            if (R::eq(R::load(H + b.hu.items[i]), 0) & used) {
+                b.flag[sl] |= 2;
                 atomicAdd(&sh.nx, 1u);
-                if (b.flag[i] & 1) sh.xvc = 1;
+                if (b.flag[sl] & 1) sh.xvc = 1;
             }
         }
         __syncthreads();
@@ -889,14 +1036,15 @@ template <class RowM> __device__ void extract_rpg(const GraphDev &g, const WsDev
         else {
             for (uint32_t i = threadIdx.x; i < ne; i += blockDim.x) {
                 uint32_t e = b.edges[i];
-                int sa = hu.find(g.src[e]), sb = hu.find(g.dst[e]);
+                int sa = b.hu.find(g.src[e]), sb = b.hu.find(g.dst[e]);
                 if (sa < 0 || sb < 0 || (b.flag[sa] & 1) || (b.flag[sb] & 1)) continue;
                 uf_union(b.uf, (uint32_t)sa, (uint32_t)sb);
             }
             __syncthreads();
-            for (uint32_t i = threadIdx.x; i < b.cap_u; i += blockDim.x) {
-                if ((b.flag[i] & 3) != 2) continue;  // X outside V_C
-                uint32_t r = uf_find(b.uf, i);
+            for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
+                uint32_t sl = b.hu.slots[i];
+                if ((b.flag[sl] & 3) != 2) continue;  // X outside V_C
+                uint32_t r = uf_find(b.uf, sl);
                 atomicMin(&sh.mnr, r);
                 atomicMax(&sh.mxr, r);
             }
@@ -906,16 +1054,11 @@ template <class RowM> __device__ void extract_rpg(const GraphDev &g, const WsDev
     }
     __syncthreads();
     // ---- write G^r lists
-    uint32_t nn = sh.nnodes;
-    if (threadIdx.x == 0) { sh.off = arena_alloc(w, nn + ne, s); sh.cnt = 0; }
+    if (threadIdx.x == 0) sh.off = arena_alloc(w, nn + ne, s);
     __syncthreads();
-    uint32_t off = sh.off;
+    const uint32_t off = sh.off;
     if (off != EMPTY) {
-        for (uint32_t i = threadIdx.x; i < b.cap_u; i += blockDim.x) {
-            uint32_t v = b.hu[i];
-            if (v == EMPTY) continue;
-            w.arena[off + atomicAdd(&sh.cnt, 1u)] = v;
-        }
+        for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) w.arena[off + i] = b.hu.items[i];
         for (uint32_t i = threadIdx.x; i < ne; i += blockDim.x) w.arena[off + nn + i] = b.edges[i];
     }
     __syncthreads();
@@ -932,39 +1075,49 @@ template <class RowM> __device__ void extract_rpg(const GraphDev &g, const WsDev
     }
 }
 
-template <class RowM> __global__ void __launch_bounds__(256) k_extract_rpg(GraphDev g, WsDev w) {
+template <class RowM, int TIER> __global__ void __launch_bounds__(Tier<TIER>::THREADS) k_extract_rpg(GraphDev g, WsDev w) {
     extern __shared__ __align__(16) uint8_t smx[];
     __shared__ ExShared sh;
-    ExBuf b = smem_buf(smx);
-    uint32_t n = w.ctr[C_NNEWATT];
+    uint32_t n = TIER == 0 ? w.ctr[C_NNEWATT] : min(w.ctr[C_NOVF], w.ovf_cap);
+    if (blockIdx.x >= n) return;
+    ExBuf b = smem_buf<TIER>(smx, sh);
+    ex_init(b, sh);
     for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-        uint2 sc = w.newatt[i];
+        uint2 sc = TIER == 0 ? w.newatt[i] : w.ovf[i];
         bool ovf = false;
         extract_rpg<RowM>(g, w, sc.x, sc.y, b, sh, &ovf);
         if (ovf && threadIdx.x == 0) {
-            uint32_t p = atomicAdd(&w.ctr[C_NOVF], 1u);
-            if (p < w.ovf_cap) w.ovf[p] = sc; else atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT);
+            sh.dirty = 1;
+            uint32_t *ctr = &w.ctr[TIER == 0 ? C_NOVF : C_NOVF2];
+            uint2 *lst = TIER == 0 ? w.ovf : w.ovf2;
+            uint32_t p = atomicAdd(ctr, 1u);
+            if (p < w.ovf_cap) lst[p] = sc; else atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT);
         }
         __syncthreads();
+        ex_reset(b, sh);
     }
 }
 
 template <class RowM> __global__ void __launch_bounds__(256) k_extract_rpg_big(GraphDev g, WsDev w) {
     __shared__ ExShared sh;
-    ExBuf b = big_buf(w, blockIdx.x);
-    uint32_t n = min(w.ctr[C_NOVF], w.ovf_cap);
+    uint32_t n = min(w.ctr[C_NOVF2], w.ovf_cap);
+    if (blockIdx.x >= n) return;
+    ExBuf b = big_buf(w, blockIdx.x, sh);
+    ex_init(b, sh);
     for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-        uint2 sc = w.ovf[i];
+        uint2 sc = w.ovf2[i];
         bool ovf = false;
         extract_rpg<RowM>(g, w, sc.x, sc.y, b, sh, &ovf);
-        if (ovf && threadIdx.x == 0) atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT);
+        if (ovf && threadIdx.x == 0) { sh.dirty = 1; atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT); }
         __syncthreads();
+        ex_reset(b, sh);
     }
 }
 
 __global__ void k_reset_level_ctrs(WsDev w) {
     w.ctr[C_NNEWATT] = 0;
     w.ctr[C_NOVF] = 0;
+    w.ctr[C_NOVF2] = 0;
 }
 
 __device__ void cta_sort_u128(u128 *keys, uint32_t n, u128 *smem, uint32_t smem_cap) {
@@ -1126,14 +1279,15 @@ struct Workspace {
     uint64_t arena_cap = 0, out_cap = 0, big_words = 0;
     uint8_t *H[2] = {nullptr, nullptr};
     uint32_t *q = nullptr, *bm = nullptr, *offs = nullptr, *coffs = nullptr, *ctr = nullptr, *arena = nullptr,
-             *big = nullptr, *resid = nullptr, *out = nullptr;
+             *big = nullptr, *resid = nullptr, *out = nullptr, *mkeys = nullptr;
+    unsigned long long *mvals = nullptr;
     uint64_t *ck = nullptr;
     Cand *cd = nullptr;
     u128 *rk = nullptr;
     SlotState *st = nullptr;
     uint4 *heavy = nullptr;
     unsigned long long *prof = nullptr, *arena_used = nullptr, *out_used = nullptr;
-    uint2 *newatt = nullptr, *ovf = nullptr;
+    uint2 *newatt = nullptr, *ovf = nullptr, *ovf2 = nullptr;
     OutHdr *hdr = nullptr;
     uint32_t *h_ctr = nullptr;  // pinned
     uint64_t bytes = 0;
@@ -1173,8 +1327,8 @@ struct Workspace {
         d.q = q; d.bm = bm; d.ck = ck; d.cd = cd; d.rk = rk; d.offs = offs; d.coffs = coffs;
         d.heavy = heavy; d.heavy_cap = heavy_cap; d.ctr = ctr; d.prof = prof;
         d.arena = arena; d.arena_used = arena_used; d.arena_cap = arena_cap;
-        d.newatt = newatt; d.ovf = ovf; d.ovf_cap = ovf_cap;
-        d.big = big; d.big_words = big_words;
+        d.newatt = newatt; d.ovf = ovf; d.ovf2 = ovf2; d.ovf_cap = ovf_cap;
+        d.big = big; d.big_words = big_words; d.mkeys = mkeys; d.mvals = mvals;
         d.hdr = hdr; d.resid = resid; d.out = out; d.out_used = out_used; d.out_cap = out_cap;
         return d;
     }
@@ -1202,8 +1356,6 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     ws->H[0] = ws->alloc<uint8_t>(S * V * 8);
     ws->H[1] = ws->alloc<uint8_t>(S * V * 8);
     ws->q = ws->alloc<uint32_t>(S * 2 * V);
-    ws->bm = ws->alloc<uint32_t>(S * 2 * ws->W);
-    CUDA_TRY(cudaMemset(ws->bm, 0, S * 2 * ws->W * 4));
     ws->ck = ws->alloc<uint64_t>(S * c.capc);
     ws->cd = ws->alloc<Cand>(S * c.capc);
     ws->rk = ws->alloc<u128>(S * c.capc);
@@ -1220,9 +1372,12 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     ws->newatt = ws->alloc<uint2>(S * c.capc);
     ws->ovf_cap = (uint32_t)(S * c.capc);
     ws->ovf = ws->alloc<uint2>(ws->ovf_cap);
+    ws->ovf2 = ws->alloc<uint2>(ws->ovf_cap);
     ws->big_ctas = V <= (4u << 20) ? 8 : 2;
     uint64_t cu = next_pow2(2 * V + 2);
-    ws->big_words = cu * 3 + (V + 1) + cu / 4 + 16 + std::max<uint64_t>(std::min<uint64_t>(g->E, 1ull << 26), 1u << 20);
+    ws->big_words = cu * 3 + 4ull * (V + 1) + cu / 4 + 16 + std::max<uint64_t>(std::min<uint64_t>(g->E, 1ull << 26), 1u << 20);
+    ws->mkeys = ws->alloc<uint32_t>(S * 16 * MAPCAP);
+    ws->mvals = ws->alloc<unsigned long long>(S * 16 * MAPCAP);
     ws->big = ws->alloc<uint32_t>(ws->big_words * ws->big_ctas);
     ws->hdr = ws->alloc<OutHdr>(S * c.kmax);
     ws->resid = ws->alloc<uint32_t>(S * c.kmax);
@@ -1233,10 +1388,11 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     CUDA_TRY(cudaEventCreate(&ws->ev1));
     static bool attr_done = false;
     if (!attr_done) {
-        CUDA_TRY(cudaFuncSetAttribute(k_extract_cg<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_EX));
-        CUDA_TRY(cudaFuncSetAttribute(k_extract_cg<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_EX));
-        CUDA_TRY(cudaFuncSetAttribute(k_extract_rpg<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_EX));
-        CUDA_TRY(cudaFuncSetAttribute(k_extract_rpg<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_EX));
+#define SET_EX_ATTR(K) CUDA_TRY(cudaFuncSetAttribute(K<uint32_t, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ex<1>())); \
+        CUDA_TRY(cudaFuncSetAttribute(K<uint64_t, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ex<1>()));
+        SET_EX_ATTR(k_extract_cg)
+        SET_EX_ATTR(k_extract_rpg)
+#undef SET_EX_ATTR
         CUDA_TRY(cudaFuncSetAttribute(k_decide_m, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
         CUDA_TRY(cudaFuncSetAttribute(k_final_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
         CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
@@ -1283,7 +1439,9 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             if (total_cands) {
                 k_attach<RowT><<<grid_of(total_cands * 32, 256), 256, 0, s>>>(wd);
                 L.check();
-                k_extract_rpg<RowT><<<148 * 2, 256, SMEM_EX, s>>>(gd, wd);
+                k_extract_rpg<RowT, 0><<<148 * 14, 64, smem_ex<0>(), s>>>(gd, wd);
+                L.check();
+                k_extract_rpg<RowT, 1><<<148 * 3, 256, smem_ex<1>(), s>>>(gd, wd);
                 L.check();
                 k_extract_rpg_big<RowT><<<ws->big_ctas, 256, 0, s>>>(gd, wd);
                 L.check();
@@ -1311,8 +1469,6 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             L.expand_launches += 2;
         }
     }
-    k_clear_bm<<<dim3(8, ws->slots), 256, 0, s>>>(wd, ph);
-    L.check();
 }
 
 template <class RowC, class RowM>
@@ -1323,6 +1479,8 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     CUDA_TRY(cudaMemsetAsync(ws->arena_used, 0, 8, s));
     CUDA_TRY(cudaMemsetAsync(ws->out_used, 0, 8, s));
     CUDA_TRY(cudaMemsetAsync(ws->ctr, 0, C_NCTR * 4, s));
+    CUDA_TRY(cudaMemsetAsync(ws->mkeys, 0xFF, (size_t)ws->slots * 16 * MAPCAP * 4, s));
+    CUDA_TRY(cudaMemsetAsync(ws->mvals, 0xFF, (size_t)ws->slots * 16 * MAPCAP * 8, s));
     // ---- run 1: central keywords
     run_phase<RowC, RowC>(L, gd, ws, 0, -1, depth + 1, 0);
     // ---- candidate CGs + recovery
@@ -1334,7 +1492,9 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     CUDA_TRY(cudaStreamSynchronize(s));
     uint64_t total_cands = ws->h_ctr[C_NCAND_TOTAL];
     if (total_cands) {
-        k_extract_cg<RowC><<<grid_of(total_cands, 1, 148 * 2), 256, SMEM_EX, s>>>(gd, wd);
+        k_extract_cg<RowC, 0><<<grid_of(total_cands, 1, 148 * 14), 64, smem_ex<0>(), s>>>(gd, wd);
+        L.check();
+        k_extract_cg<RowC, 1><<<148 * 3, 256, smem_ex<1>(), s>>>(gd, wd);
         L.check();
         k_extract_cg_big<RowC><<<ws->big_ctas, 256, 0, s>>>(gd, wd);
         L.check();

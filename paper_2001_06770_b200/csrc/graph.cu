@@ -122,6 +122,24 @@ __global__ void k_gather_in(const uint64_t *key, const uint32_t *eid, const uint
     }
 }
 
+// Node descriptor: one 16-byte load gives the row start, the degree and, for rows of at most
+// 8 edges, all their (sorted) activations packed in bytes (padding 0xFF), so the expansion
+// finds the gate ranges a <= l / a == l with byte-SIMD compares instead of a binary search.
+__global__ void k_desc(const uint32_t *row, const uint8_t *act, uint32_t V, uint4 *desc) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+        uint32_t rb = row[v], deg = row[v + 1] - rb;
+        uint32_t lo = 0xFFFFFFFFu, hi = 0xFFFFFFFFu;
+        if (deg <= 8) {
+            for (uint32_t i = 0; i < deg; i++) {
+                uint32_t b = act[rb + i];
+                if (i < 4) lo = (lo & ~(0xFFu << (8 * i))) | (b << (8 * i));
+                else hi = (hi & ~(0xFFu << (8 * (i - 4)))) | (b << (8 * (i - 4)));
+            }
+        }
+        desc[v] = make_uint4(rb, deg, lo, hi);
+    }
+}
+
 __global__ void k_minmax_pair(double *mnmx, const double *mn, const double *mx) {
     mnmx[0] = *mn;
     mnmx[1] = *mx;
@@ -158,6 +176,7 @@ void build_csr(riki_graph *g) {
     k_act_keys<<<grid_for(E), 256, 0, s>>>(g->d_src, g->d_act_e, E, keys, vals);
     sort_pairs(s, keys, vals, E, eb);
     k_gather_out<<<grid_for(E), 256, 0, s>>>(keys, vals, g->d_dst, E, g->d_col, g->d_act);
+    k_desc<<<grid_for(g->V), 256, 0, s>>>(g->d_row, g->d_act, g->V, g->d_desc);
     // in-CSR
     k_act_keys<<<grid_for(E), 256, 0, s>>>(g->d_dst, g->d_act_e, E, keys, vals);
     sort_pairs(s, keys, vals, E, eb);
@@ -218,6 +237,7 @@ void graph_load(riki_graph *g, uint32_t V, uint64_t E, const uint32_t *src, cons
     g->d_row = dmalloc<uint32_t>(V + 1, acc);
     g->d_col = dmalloc<uint32_t>(E, acc);
     g->d_act = dmalloc<uint8_t>(E, acc);
+    g->d_desc = dmalloc<uint4>(V, acc);
     g->d_irow = dmalloc<uint32_t>(V + 1, acc);
     g->d_isrc = dmalloc<uint32_t>(E, acc);
     g->d_ieid = dmalloc<uint32_t>(E, acc);
@@ -243,7 +263,7 @@ void graph_load(riki_graph *g, uint32_t V, uint64_t E, const uint32_t *src, cons
 }
 
 void graph_free(riki_graph *g) {
-    void *ps[] = {g->d_src, g->d_dst, g->d_cls, g->d_act_e, g->d_row, g->d_col, g->d_act,
+    void *ps[] = {g->d_src, g->d_dst, g->d_cls, g->d_act_e, g->d_row, g->d_col, g->d_act, g->d_desc,
                   g->d_irow, g->d_isrc, g->d_ieid, g->d_iact, g->d_tptr, g->d_post};
     for (void *p : ps) if (p) cudaFree(p);
     if (g->stream) cudaStreamDestroy(g->stream);

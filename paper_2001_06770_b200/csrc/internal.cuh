@@ -19,6 +19,7 @@ struct GraphDev {
     uint64_t E;
     const uint32_t *row, *col;  // out-CSR
     const uint8_t *act;
+    const uint4 *desc;          // per node: {row start, degree, packed activations of rows <= 8 edges}
     const uint32_t *irow, *isrc, *ieid;  // in-CSR
     const uint8_t *iact;
     const uint32_t *src, *dst;  // caller's edge list by edge id
@@ -37,6 +38,7 @@ struct riki_graph {
     bool has_act = false;
     uint32_t *d_row = nullptr, *d_col = nullptr;
     uint8_t *d_act = nullptr;
+    uint4 *d_desc = nullptr;
     uint32_t *d_irow = nullptr, *d_isrc = nullptr, *d_ieid = nullptr;
     uint8_t *d_iact = nullptr;
     uint64_t *d_tptr = nullptr;
@@ -51,7 +53,7 @@ struct riki_graph {
     GraphDev dev() const {
         GraphDev g;
         g.V = V; g.E = E;
-        g.row = d_row; g.col = d_col; g.act = d_act;
+        g.row = d_row; g.col = d_col; g.act = d_act; g.desc = d_desc;
         g.irow = d_irow; g.isrc = d_isrc; g.ieid = d_ieid; g.iact = d_iact;
         g.src = d_src; g.dst = d_dst; g.tptr = d_tptr; g.post = d_post;
         return g;
