@@ -57,7 +57,7 @@ struct SlotState {
 struct Cand {
     uint32_t v, sc;
     uint32_t nodes_off, n_nodes, edges_off, n_edges, vc_off, n_vc;
-    uint32_t attached, ptc, sm, flags;
+    uint32_t attached, ptc, sm, ext;  // ext = caller id of v (ordering and output use caller ids)
     double sr;
     uint8_t mdist[RIKI_MAX_TERMS];
 };
@@ -196,7 +196,7 @@ template <class RowT> __global__ void k_seed(GraphDev g, WsDev w, int ph) {
             if (st.collect && Row<RowT>::eq(nw, Row<RowT>::splat(0xFF)) == 0 &&
                 Row<RowT>::byte(old, j) == 0xFF) {
                 uint32_t p = atomicAdd(&st.ncand, 1u);
-                if (p < w.capc) w.CK(s)[p] = (uint64_t)v;  // score 0
+                if (p < w.capc) w.CK(s)[p] = (uint64_t)g.iperm[v];  // score 0
                 else atomicOr(&st.err, (uint32_t)E_CAND);
             }
         }
@@ -290,10 +290,11 @@ __device__ __forceinline__ void frontier_push(const WsDev &w, bool want, uint32_
     if (want) w.Q(s, nxt)[pos] = entry;
 }
 
-__device__ __forceinline__ void cand_push(const WsDev &w, bool want, uint32_t s, uint32_t n, uint32_t level) {
+__device__ __forceinline__ void cand_push(const GraphDev &g, const WsDev &w, bool want, uint32_t s, uint32_t n,
+                                          uint32_t level) {
     uint32_t pos = warp_append(want, s, &w.st[0].ncand, sizeof(SlotState) / 4);
-    if (want) {
-        if (pos < w.capc) w.CK(s)[pos] = (uint64_t)level << 32 | n;
+    if (want) {  // key (S^c, caller id): the (S^c, v) order of R13/R23 uses the caller's ids
+        if (pos < w.capc) w.CK(s)[pos] = (uint64_t)level << 32 | __ldg(g.iperm + n);
         else atomicOr(&w.st[s].err, (uint32_t)E_CAND);
     }
 }
@@ -317,8 +318,14 @@ __device__ __forceinline__ uint32_t lower_bound_act(const uint8_t *act, uint32_t
 // per-node part (row bounds, CF check, retention, activation range by binary search in the
 // activation-sorted row), then the warp walks the concatenated active ranges edge-parallel,
 // two edges in flight per lane.
+#ifndef EXP_UNROLL
+#define EXP_UNROLL 2
+#endif
+#ifndef EXP_MINB
+#define EXP_MINB 8
+#endif
 template <class RowT>
-__global__ void __launch_bounds__(256) k_expand(GraphDev g, WsDev w, int ph, uint32_t l) {
+__global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, int ph, uint32_t l) {
     typedef Row<RowT> R;
     __shared__ uint32_t s_offs[MAX_SLOTS + 1];
     __shared__ uint32_t s_info[MAX_SLOTS];
@@ -335,7 +342,7 @@ __global__ void __launch_bounds__(256) k_expand(GraphDev g, WsDev w, int ph, uin
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const RowT L = R::splat(l);
-    unsigned long long p_items = 0, p_edges = 0, p_cells = 0, p_enq = 0;
+    uint32_t p_items = 0, p_edges = 0, p_cells = 0, p_enq = 0;
 
     for (uint32_t base = gw * 32; base < total; base += nw * 32) {
         uint32_t item = base + lane;
@@ -404,12 +411,12 @@ __global__ void __launch_bounds__(256) k_expand(GraphDev g, WsDev w, int ph, uin
         uint32_t tot = __shfl_sync(FULLMASK, incl, 31);
         uint32_t excl = incl - len;
         p_edges += len;
-        for (uint32_t eb = 0; eb < tot; eb += 64) {
-            uint32_t n[2], o_s[2];
-            RowT mask[2], hn[2];
-            bool ev[2];
+        for (uint32_t eb = 0; eb < tot; eb += 32 * EXP_UNROLL) {
+            uint32_t n[EXP_UNROLL], o_s[EXP_UNROLL];
+            RowT mask[EXP_UNROLL], hn[EXP_UNROLL];
+            bool ev[EXP_UNROLL];
 #pragma unroll
-            for (int u = 0; u < 2; u++) {
+            for (int u = 0; u < EXP_UNROLL; u++) {
                 uint32_t idx = eb + 32 * u + lane;
                 ev[u] = idx < tot;
                 uint32_t own = 0;  // owner lane: largest i with excl_i <= idx
@@ -428,9 +435,9 @@ __global__ void __launch_bounds__(256) k_expand(GraphDev g, WsDev w, int ph, uin
                 mask[u] = o_new | (e >= o_eq ? o_old : (RowT)0);  // [eqlo, hi) are the edges with a == l
             }
 #pragma unroll
-            for (int u = 0; u < 2; u++) hn[u] = ev[u] ? R::load(w.Hs<RowT>(ph, o_s[u]) + n[u]) : (RowT)0;
+            for (int u = 0; u < EXP_UNROLL; u++) hn[u] = ev[u] ? R::load(w.Hs<RowT>(ph, o_s[u]) + n[u]) : (RowT)0;
 #pragma unroll
-            for (int u = 0; u < 2; u++) {
+            for (int u = 0; u < EXP_UNROLL; u++) {
                 Relax<RowT> r{false, false, 0};
                 if (ev[u]) {
                     r = relax<RowT>(w.Hs<RowT>(ph, o_s[u]), n[u], hn[u], mask[u], l);
@@ -439,7 +446,7 @@ __global__ void __launch_bounds__(256) k_expand(GraphDev g, WsDev w, int ph, uin
                 }
                 frontier_push(w, r.enq, o_s[u], n[u], nxt);
                 bool id = r.ident && ((s_info[ev[u] ? o_s[u] : 0] >> 1) & 1);
-                cand_push(w, id, o_s[u], n[u], l + 1);
+                cand_push(g, w, id, o_s[u], n[u], l + 1);
             }
         }
     }
@@ -448,15 +455,15 @@ __global__ void __launch_bounds__(256) k_expand(GraphDev g, WsDev w, int ph, uin
     p_cells = warp_sum(p_cells);
     p_enq = warp_sum(p_enq);
     if (lane == 0 && (p_items | p_edges)) {
-        atomicAdd(&w.prof[P_ITEMS], p_items);
-        atomicAdd(&w.prof[P_EDGES], p_edges);
-        atomicAdd(&w.prof[P_NEWCELLS], p_cells);
-        atomicAdd(&w.prof[P_ENQ], p_enq);
+        atomicAdd(&w.prof[P_ITEMS], (unsigned long long)p_items);
+        atomicAdd(&w.prof[P_EDGES], (unsigned long long)p_edges);
+        atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
+        atomicAdd(&w.prof[P_ENQ], (unsigned long long)p_enq);
     }
 }
 
 // Heavy ranges (hub rows): one warp per CHUNK-edge piece, two edges per lane in flight.
-template <class RowT> __global__ void __launch_bounds__(256) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l) {
+template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l) {
     typedef Row<RowT> R;
     const uint32_t lane = lane_id();
     const uint32_t nxt = (l & 1) ^ 1;
@@ -464,7 +471,7 @@ template <class RowT> __global__ void __launch_bounds__(256) k_expand_heavy(Grap
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     uint32_t nh = min(w.ctr[C_NHEAVY], w.heavy_cap);
     const RowT L = R::splat(l);
-    unsigned long long p_cells = 0, p_enq = 0;
+    uint32_t p_cells = 0, p_enq = 0;
     for (uint32_t it = gw; it < nh; it += nw) {
         uint4 h = w.heavy[it];
         uint32_t s = h.x;
@@ -495,15 +502,15 @@ template <class RowT> __global__ void __launch_bounds__(256) k_expand_heavy(Grap
                     p_enq += r.enq;
                 }
                 frontier_push(w, r.enq, s, n[u], nxt);
-                cand_push(w, r.ident && collect, s, n[u], l + 1);
+                cand_push(g, w, r.ident && collect, s, n[u], l + 1);
             }
         }
     }
     p_cells = warp_sum(p_cells);
     p_enq = warp_sum(p_enq);
     if (lane == 0 && (p_cells | p_enq)) {
-        atomicAdd(&w.prof[P_NEWCELLS], p_cells);
-        atomicAdd(&w.prof[P_ENQ], p_enq);
+        atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
+        atomicAdd(&w.prof[P_ENQ], (unsigned long long)p_enq);
     }
 }
 
@@ -523,7 +530,7 @@ __device__ void cta_sort_u64(uint64_t *keys, uint32_t n, uint64_t *smem, uint32_
 
 // Candidate CGs: all CGs identified by the terminating level, ties kept (R13), ordered
 // by (S^c, v); beam_mode 1 truncates to the first w.
-__global__ void k_cand_sort(WsDev w) {
+__global__ void k_cand_sort(GraphDev g, WsDev w) {
     extern __shared__ uint64_t sm64[];
     uint32_t s = blockIdx.x;
     SlotState &st = w.st[s];
@@ -539,7 +546,8 @@ __global__ void k_cand_sort(WsDev w) {
         uint64_t key = w.CK(s)[i];
         Cand c;
         memset(&c, 0, sizeof(c));
-        c.v = (uint32_t)key;
+        c.ext = (uint32_t)key;
+        c.v = g.perm[c.ext];
         c.sc = (uint32_t)(key >> 32);
         c.sr = (double)c.sc;
         c.ptc = 1;
@@ -1069,7 +1077,7 @@ template <class RowM> __device__ void extract_rpg(const GraphDev &g, const WsDev
         if (!pass) atomicAdd(&st.n_ptc_fail, 1u);
         if (pass || st.ptc_mode == 1) {
             uint32_t p = atomicAdd(&st.nR, 1u);
-            if (p < w.capc) w.RK(s)[p] = rkey(cd.sr, cd.sc, cd.v);
+            if (p < w.capc) w.RK(s)[p] = rkey(cd.sr, cd.sc, cd.ext);
             else atomicOr(&st.err, (uint32_t)E_CAND);
         }
     }
@@ -1153,7 +1161,7 @@ __global__ void k_decide_m(WsDev w, uint32_t l) {
         bool stop = l >= st.depth || st.nq[l & 1] == 0 || first == EMPTY;
         if (!stop && st.early_term == 0 && nR >= st.k) {
             const Cand &fu = w.CD(s)[first];
-            u128 best = rkey(rpg_score(st.gamma, fu.sc, l + 1), fu.sc, fu.v);
+            u128 best = rkey(rpg_score(st.gamma, fu.sc, l + 1), fu.sc, fu.ext);
             stop = w.RK(s)[st.k - 1] < best;
         }
         st.stop_m = stop;
@@ -1190,8 +1198,8 @@ __global__ void k_final_select(WsDev w) {
 }
 
 // sort + unique a u32 list into the output buffer; returns (offset, count) via sh
-__device__ void sort_unique_out(const WsDev &w, uint32_t s, const uint32_t *src, uint32_t n, uint32_t *smem,
-                                uint32_t *scan, uint32_t *res_off, uint32_t *res_n) {
+__device__ void sort_unique_out(const WsDev &w, uint32_t s, const uint32_t *src, uint32_t n, const uint32_t *map,
+                                uint32_t *smem, uint32_t *scan, uint32_t *res_off, uint32_t *res_n) {
     __shared__ uint32_t s_off, s_buf;
     uint32_t *buf = smem;
     bool global = next_pow2(n) > SORT_SMEM;
@@ -1201,7 +1209,7 @@ __device__ void sort_unique_out(const WsDev &w, uint32_t s, const uint32_t *src,
         if (s_buf == EMPTY) { *res_off = 0; *res_n = 0; return; }
         buf = w.arena + s_buf;
     }
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) buf[i] = src[i];
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) buf[i] = map ? map[src[i]] : src[i];
     __syncthreads();
     cta_bitonic_sort(buf, n);
     // unique: per-thread contiguous chunk counts + block scan
@@ -1235,7 +1243,7 @@ __device__ void sort_unique_out(const WsDev &w, uint32_t s, const uint32_t *src,
     *res_n = total;
 }
 
-template <class RowC> __global__ void __launch_bounds__(256) k_final_lists(WsDev w) {
+template <class RowC> __global__ void __launch_bounds__(256) k_final_lists(GraphDev g, WsDev w) {
     extern __shared__ __align__(16) uint32_t sm32[];
     __shared__ uint32_t scan[256];
     uint32_t r = blockIdx.x, s = blockIdx.y;
@@ -1245,14 +1253,14 @@ template <class RowC> __global__ void __launch_bounds__(256) k_final_lists(WsDev
     const Cand &cd = w.CD(s)[c];
     OutHdr h;
     memset(&h, 0, sizeof(h));
-    h.central = cd.v;
+    h.central = cd.ext;
     h.sc = cd.sc;
     h.sm = st.T[1] ? cd.sm : 0;
     h.ptc = cd.ptc;
     h.score = st.T[1] ? cd.sr : (double)cd.sc;
-    sort_unique_out(w, s, w.arena + cd.nodes_off, cd.n_nodes, sm32, scan, &h.nodes_off, &h.n_nodes);
-    sort_unique_out(w, s, w.arena + cd.edges_off, cd.n_edges, sm32, scan, &h.edges_off, &h.n_edges);
-    sort_unique_out(w, s, w.arena + cd.vc_off, cd.n_vc, sm32, scan, &h.vc_off, &h.n_vc);
+    sort_unique_out(w, s, w.arena + cd.nodes_off, cd.n_nodes, g.iperm, sm32, scan, &h.nodes_off, &h.n_nodes);
+    sort_unique_out(w, s, w.arena + cd.edges_off, cd.n_edges, nullptr, sm32, scan, &h.edges_off, &h.n_edges);
+    sort_unique_out(w, s, w.arena + cd.vc_off, cd.n_vc, g.iperm, sm32, scan, &h.vc_off, &h.n_vc);
     RowC hv = Row<RowC>::load(w.Hs<RowC>(0, s) + cd.v);
     for (uint32_t j = 0; j < RIKI_MAX_TERMS; j++) {
         h.cdist[j] = j < st.T[0] ? Row<RowC>::byte(hv, j) : 0;
@@ -1262,10 +1270,11 @@ template <class RowC> __global__ void __launch_bounds__(256) k_final_lists(WsDev
 }
 
 // ====================================================================== debug boundary
-template <class RowT> __global__ void k_pack_H(WsDev w, uint32_t T, uint8_t *Hout, uint8_t *blk, int blocking) {
+template <class RowT>
+__global__ void k_pack_H(GraphDev g, WsDev w, uint32_t T, uint8_t *Hout, uint8_t *blk, int blocking) {
     const RowT *H = w.Hs<RowT>(0, 0);
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < w.V; v += gridDim.x * blockDim.x) {
-        RowT r = Row<RowT>::load(H + v);
+        RowT r = Row<RowT>::load(H + g.perm[v]);  // output indexed by caller id
         for (uint32_t j = 0; j < T; j++) Hout[(size_t)v * T + j] = (uint8_t)Row<RowT>::byte(r, j);
         blk[v] = (blocking && Row<RowT>::eq(r, Row<RowT>::splat(0xFF)) == 0) ? (uint8_t)Row<RowT>::maxb(r) : 0xFF;
     }
@@ -1484,7 +1493,7 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     // ---- run 1: central keywords
     run_phase<RowC, RowC>(L, gd, ws, 0, -1, depth + 1, 0);
     // ---- candidate CGs + recovery
-    k_cand_sort<<<ws->slots, 1024, 4096 * 8, s>>>(wd);
+    k_cand_sort<<<ws->slots, 1024, 4096 * 8, s>>>(gd, wd);
     L.check();
     k_scan_cands<<<1, MAX_SLOTS, 0, s>>>(wd);
     L.check();
@@ -1504,7 +1513,7 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     // ---- top-k and packing
     k_final_select<<<ws->slots, 256, 1024 * 16, s>>>(wd);
     L.check();
-    k_final_lists<RowC><<<dim3(ws->kmax, ws->slots), 256, SORT_SMEM * 4, s>>>(wd);
+    k_final_lists<RowC><<<dim3(ws->kmax, ws->slots), 256, SORT_SMEM * 4, s>>>(gd, wd);
     L.check();
 }
 
@@ -1842,10 +1851,10 @@ void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uin
         WsDev wd = ws->dev();
         if (T <= 4) {
             run_phase<uint32_t, uint32_t>(L, gd, ws, 0, block_mode, depth + 1, 0);
-            k_pack_H<uint32_t><<<grid_of(g->V, 256), 256, 0, L.s>>>(wd, T, dH, dB, blocking);
+            k_pack_H<uint32_t><<<grid_of(g->V, 256), 256, 0, L.s>>>(gd, wd, T, dH, dB, blocking);
         } else {
             run_phase<uint64_t, uint64_t>(L, gd, ws, 0, block_mode, depth + 1, 0);
-            k_pack_H<uint64_t><<<grid_of(g->V, 256), 256, 0, L.s>>>(wd, T, dH, dB, blocking);
+            k_pack_H<uint64_t><<<grid_of(g->V, 256), 256, 0, L.s>>>(gd, wd, T, dH, dB, blocking);
         }
         L.check();
         CUDA_TRY(cudaMemcpyAsync(H_out, dH, (size_t)g->V * T, cudaMemcpyDeviceToHost, L.s));

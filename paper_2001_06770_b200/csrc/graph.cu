@@ -50,10 +50,10 @@ __global__ void k_coarsen_edges(const double *w, uint64_t n, double alpha, doubl
     }
 }
 
-__global__ void k_coarsen_nodes(const double *w, const uint32_t *dst, uint64_t n, double alpha, double avg,
-                                uint8_t *a, uint32_t *bad) {
+__global__ void k_coarsen_nodes(const double *w, const uint32_t *dst, const uint32_t *iperm, uint64_t n,
+                                double alpha, double avg, uint8_t *a, uint32_t *bad) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        double x = w[dst[i]];
+        double x = w[iperm[dst[i]]];  // w is indexed by the caller's node id
         if (!(x >= 0.0 && x <= 1.0)) { atomicOr(bad, 1u); a[i] = 0xFF; continue; }
         a[i] = (uint8_t)coarsen_dev(x, alpha, avg);
     }
@@ -138,6 +138,31 @@ __global__ void k_desc(const uint32_t *row, const uint8_t *act, uint32_t V, uint
         }
         desc[v] = make_uint4(rb, deg, lo, hi);
     }
+}
+
+// Node relabeling for L2 locality: internal id = rank by total degree (descending, then
+// caller id).  In a power-law graph most edge endpoints are hubs, so the H words that the
+// expansion hits most often form a short prefix of every query's H array.
+__global__ void k_degree(const uint32_t *src, const uint32_t *dst, uint64_t n, uint32_t *deg) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        atomicAdd(&deg[src[i]], 1u);
+        atomicAdd(&deg[dst[i]], 1u);
+    }
+}
+__global__ void k_deg_keys(const uint32_t *deg, uint32_t V, uint64_t *key) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
+        key[v] = (uint64_t)(0xFFFFFFFFu - deg[v]) << 32 | v;
+}
+__global__ void k_perm(const uint64_t *sorted, uint32_t V, uint32_t *perm, uint32_t *iperm) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < V; r += gridDim.x * blockDim.x) {
+        uint32_t v = (uint32_t)sorted[r];
+        perm[v] = r;
+        iperm[r] = v;
+    }
+}
+__global__ void k_relabel(uint32_t *x, uint64_t n, const uint32_t *perm) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        x[i] = perm[x[i]];
 }
 
 __global__ void k_minmax_pair(double *mnmx, const double *mn, const double *mx) {
@@ -257,6 +282,28 @@ void graph_load(riki_graph *g, uint32_t V, uint64_t E, const uint32_t *src, cons
         CUDA_TRY(cudaMemcpyAsync(g->d_tptr, tptr, (n_terms + 1) * 8, cudaMemcpyHostToDevice, s));
         if (P) CUDA_TRY(cudaMemcpyAsync(g->d_post, post, P * 4, cudaMemcpyHostToDevice, s));
     }
+    // ---- degree-descending relabeling (internal ids); translated back at the boundary
+    g->d_perm = dmalloc<uint32_t>(V, acc);
+    g->d_iperm = dmalloc<uint32_t>(V, acc);
+    {
+        uint32_t *deg = dmalloc<uint32_t>(V);
+        uint64_t *k1 = dmalloc<uint64_t>(V), *k2 = dmalloc<uint64_t>(V);
+        CUDA_TRY(cudaMemsetAsync(deg, 0, (size_t)V * 4, s));
+        if (E) k_degree<<<grid_for(E), 256, 0, s>>>(g->d_src, g->d_dst, E, deg);
+        k_deg_keys<<<grid_for(V), 256, 0, s>>>(deg, V, k1);
+        size_t tmp = 0;
+        CUDA_TRY(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k1, k2, (int64_t)V, 0, 64, s));
+        void *t = dmalloc<uint8_t>(tmp);
+        CUDA_TRY(cub::DeviceRadixSort::SortKeys(t, tmp, k1, k2, (int64_t)V, 0, 64, s));
+        k_perm<<<grid_for(V), 256, 0, s>>>(k2, V, g->d_perm, g->d_iperm);
+        if (E) {
+            k_relabel<<<grid_for(E), 256, 0, s>>>(g->d_src, E, g->d_perm);
+            k_relabel<<<grid_for(E), 256, 0, s>>>(g->d_dst, E, g->d_perm);
+        }
+        if (P) k_relabel<<<grid_for(P), 256, 0, s>>>(g->d_post, P, g->d_perm);
+        sync_check(s);
+        cudaFree(t); cudaFree(deg); cudaFree(k1); cudaFree(k2);
+    }
     row_pointers(s, g->d_src, E, V, g->d_row);
     row_pointers(s, g->d_dst, E, V, g->d_irow);
     sync_check(s);
@@ -264,7 +311,7 @@ void graph_load(riki_graph *g, uint32_t V, uint64_t E, const uint32_t *src, cons
 
 void graph_free(riki_graph *g) {
     void *ps[] = {g->d_src, g->d_dst, g->d_cls, g->d_act_e, g->d_row, g->d_col, g->d_act, g->d_desc,
-                  g->d_irow, g->d_isrc, g->d_ieid, g->d_iact, g->d_tptr, g->d_post};
+                  g->d_irow, g->d_isrc, g->d_ieid, g->d_iact, g->d_tptr, g->d_post, g->d_perm, g->d_iperm};
     for (void *p : ps) if (p) cudaFree(p);
     if (g->stream) cudaStreamDestroy(g->stream);
 }
@@ -298,7 +345,7 @@ void graph_set_node_weights(riki_graph *g, const double *w01, double alpha, doub
     uint32_t *bad = dmalloc<uint32_t>(1);
     CUDA_TRY(cudaMemsetAsync(bad, 0, 4, g->stream));
     CUDA_TRY(cudaMemcpyAsync(dw, w01, (size_t)g->V * 8, cudaMemcpyHostToDevice, g->stream));
-    k_coarsen_nodes<<<grid_for(g->E), 256, 0, g->stream>>>(dw, g->d_dst, g->E, alpha, avg, g->d_act_e, bad);
+    k_coarsen_nodes<<<grid_for(g->E), 256, 0, g->stream>>>(dw, g->d_dst, g->d_iperm, g->E, alpha, avg, g->d_act_e, bad);
     sync_check(g->stream);
     cudaFree(dw);
     finish_act(g, bad);

@@ -23,8 +23,9 @@ struct GraphDev {
     const uint32_t *irow, *isrc, *ieid;  // in-CSR
     const uint8_t *iact;
     const uint32_t *src, *dst;  // caller's edge list by edge id
-    const uint64_t *tptr;       // inverted index
+    const uint64_t *tptr;       // inverted index (internal ids)
     const uint32_t *post;
+    const uint32_t *perm, *iperm;  // caller id -> internal id (degree-descending), and back
 };
 
 struct riki_graph {
@@ -43,6 +44,7 @@ struct riki_graph {
     uint8_t *d_iact = nullptr;
     uint64_t *d_tptr = nullptr;
     uint32_t *d_post = nullptr;
+    uint32_t *d_perm = nullptr, *d_iperm = nullptr;
     std::vector<uint64_t> h_tptr;
     uint64_t graph_bytes = 0;
     Workspace *ws = nullptr;
@@ -55,7 +57,7 @@ struct riki_graph {
         g.V = V; g.E = E;
         g.row = d_row; g.col = d_col; g.act = d_act; g.desc = d_desc;
         g.irow = d_irow; g.isrc = d_isrc; g.ieid = d_ieid; g.iact = d_iact;
-        g.src = d_src; g.dst = d_dst; g.tptr = d_tptr; g.post = d_post;
+        g.src = d_src; g.dst = d_dst; g.tptr = d_tptr; g.post = d_post; g.perm = d_perm; g.iperm = d_iperm;
         return g;
     }
 };

@@ -12,7 +12,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libriki.so")
+LIB_PATH = os.environ.get("RIKI_LIB", os.path.join(HERE, "libriki.so"))
 HEADER = os.path.join(os.path.dirname(HERE), "include", "riki.h")
 
 STATUS = {0: "RIKI_OK", -1: "RIKI_EINVAL", -2: "RIKI_ENOMEM", -3: "RIKI_ECUDA", -4: "RIKI_EEMPTY_CENTRAL",
