@@ -156,7 +156,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="riki", choices=["riki", "reference"])
     ap.add_argument("--config", type=int, default=2)
@@ -213,7 +213,8 @@ def main():
     torch.cuda.synchronize()
     with Clocks(dev) as clk:
         for i in range(args.steps):
-            flush.fill_(i & 0xFF)
+            flush.fill_(i & 0xFF)      # L2 flush, finished before the step starts (the library
+            torch.cuda.synchronize()   # runs on its own stream and would overlap with it)
             ev[i][0].record()
             step_device()
             ev[i][1].record()
@@ -245,6 +246,7 @@ def main():
     d2h = 0
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
+        torch.cuda.synchronize()
         e2e_ev[i][0].record()
         rr = g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)
         e2e_ev[i][1].record()
@@ -285,6 +287,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": None,
                      "kernel": "k_expand + k_expand_heavy (Alg. 1 expansion), CUDA events on the library stream",
+                     "sections_ms_per_step": [x / args.steps for x in st["section_ms"]], "levels_per_step": st["levels"] / args.steps,
                      "peak_source": peak_src, "expand_share_of_step": st["expand_ms"] / tot_ms if tot_ms else None},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(st["kernel_launches"]),

@@ -194,6 +194,9 @@ typedef struct {
     uint64_t relaxations;          /* (edge, keyword) relaxations                          */
     uint64_t kernel_launches;      /* all library kernel launches                          */
     uint64_t queries;              /* queries completed                                    */
+    double section_ms[4];          /* host wall time: central run, CG recovery, marginal run, finalize
+                                      (exact only with profiling on, which syncs at section ends) */
+    uint64_t levels;               /* lock-step level iterations (one host sync each)       */
 } riki_stats;
 riki_status riki_set_profiling(riki_graph *g, int on);
 riki_status riki_get_stats(const riki_graph *g, riki_stats *out);

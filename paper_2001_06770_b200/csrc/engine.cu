@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <chrono>
 #include <functional>
 #include <string>
 #include <vector>
@@ -321,6 +322,9 @@ __device__ __forceinline__ uint32_t lower_bound_act(const uint8_t *act, uint32_t
 #ifndef EXP_UNROLL
 #define EXP_UNROLL 2
 #endif
+#ifndef EXP_SMALL
+#define EXP_SMALL 0
+#endif
 #ifndef EXP_MINB
 #define EXP_MINB 8
 #endif
@@ -379,6 +383,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
                     lo = newc ? rb : eqlo;
                     eq0 = eqlo;
                     len = hi - lo;
+                    p_edges += len;
                     relaxn = (hi - rb) * R::ones(newc) + (hi - eqlo) * R::ones(oldc);
                     if (len > HEAVY) {
                         uint32_t nch = (len + CHUNK - 1) / CHUNK;
@@ -389,7 +394,6 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
                         } else {
                             atomicOr(&w.st[s].err, (uint32_t)E_HEAVY);
                         }
-                        p_edges += len;
                         len = 0;
                     }
                 }
@@ -406,11 +410,36 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
         }
         frontier_push(w, retain, s, f | RETAINED, nxt);
         p_enq += retain;
-        // edge-parallel walk over the 32 active ranges, two edges per lane in flight
+#if EXP_SMALL > 0
+        {   // short ranges (<= EXP_SMALL edges): the owning lane issues all its loads at once
+            const bool small = len > 0 && len <= EXP_SMALL;
+            const bool collect = valid && ((s_info[s] >> 1) & 1);
+            RowT *H = w.Hs<RowT>(ph, s);
+            uint32_t nA[EXP_SMALL];
+            RowT hA[EXP_SMALL];
+#pragma unroll
+            for (int u = 0; u < EXP_SMALL; u++) nA[u] = (small && u < (int)len) ? __ldg(g.col + lo + u) : 0;
+#pragma unroll
+            for (int u = 0; u < EXP_SMALL; u++) hA[u] = (small && u < (int)len) ? R::load(H + nA[u]) : (RowT)0;
+#pragma unroll
+            for (int u = 0; u < EXP_SMALL; u++) {
+                Relax<RowT> r{false, false, 0};
+                if (small && u < (int)len) {
+                    RowT mask = newc | (lo + u >= eq0 ? oldc : (RowT)0);
+                    r = relax<RowT>(H, nA[u], hA[u], mask, l);
+                    p_cells += r.cells;
+                    p_enq += r.enq;
+                }
+                frontier_push(w, r.enq, s, nA[u], nxt);
+                cand_push(g, w, r.ident && collect, s, nA[u], l + 1);
+            }
+            if (small) len = 0;
+        }
+#endif
+        // edge-parallel walk over the remaining active ranges, EXP_UNROLL edges per lane in flight
         uint32_t incl = warp_incl_scan(len);
         uint32_t tot = __shfl_sync(FULLMASK, incl, 31);
         uint32_t excl = incl - len;
-        p_edges += len;
         for (uint32_t eb = 0; eb < tot; eb += 32 * EXP_UNROLL) {
             uint32_t n[EXP_UNROLL], o_s[EXP_UNROLL];
             RowT mask[EXP_UNROLL], hn[EXP_UNROLL];
@@ -1301,6 +1330,15 @@ struct Workspace {
     uint32_t *h_ctr = nullptr;  // pinned
     uint64_t bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    std::vector<cudaEvent_t> evpool;
+    cudaEvent_t event(uint32_t i) {
+        while (evpool.size() <= i) {
+            cudaEvent_t e;
+            CUDA_TRY(cudaEventCreate(&e));
+            evpool.push_back(e);
+        }
+        return evpool[i];
+    }
     // state of the last device batch (for engine_fetch)
     uint32_t last_n = 0;
     std::vector<uint32_t> last_map;  // slot -> query index of the last batch
@@ -1327,6 +1365,8 @@ struct Workspace {
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         ev0 = ev1 = nullptr;
+        for (cudaEvent_t e : evpool) cudaEventDestroy(e);
+        evpool.clear();
         bytes = 0;
     }
     WsDev dev() const {
@@ -1421,6 +1461,15 @@ struct Launch {
     uint64_t launches = 0;
     double expand_ms = 0;
     uint64_t expand_launches = 0;
+    uint32_t nev = 0;                 // profiling events recorded (pairs around each expansion)
+    double sec_ms[4] = {0, 0, 0, 0};  // central run, recovery, marginal run, finalize (host wall between syncs)
+    uint64_t levels = 0;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    void mark(int sec) {
+        auto t = std::chrono::steady_clock::now();
+        sec_ms[sec] += std::chrono::duration<double, std::milli>(t - t0).count();
+        t0 = t;
+    }
     void check() {
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) RIKI_THROW(RIKI_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
@@ -1463,18 +1512,15 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
         CUDA_TRY(cudaMemcpyAsync(ws->h_ctr, ws->ctr, C_NCTR * 4, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
         if (ws->h_ctr[C_ACTIVE] == 0) break;
+        L.levels++;
         uint32_t total = ws->h_ctr[C_TOTAL];
-        if (L.g->profiling) CUDA_TRY(cudaEventRecord(ws->ev0, s));
+        if (L.g->profiling) CUDA_TRY(cudaEventRecord(ws->event(L.nev++), s));
         k_expand<RowT><<<grid_of(total, 256), 256, 0, s>>>(gd, wd, ph, l);
         L.check();
         k_expand_heavy<RowT><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
         L.check();
-        if (L.g->profiling) {
-            CUDA_TRY(cudaEventRecord(ws->ev1, s));
-            CUDA_TRY(cudaEventSynchronize(ws->ev1));
-            float ms = 0;
-            CUDA_TRY(cudaEventElapsedTime(&ms, ws->ev0, ws->ev1));
-            L.expand_ms += ms;
+        if (L.g->profiling) {  // events are read after the batch: no extra sync per level
+            CUDA_TRY(cudaEventRecord(ws->event(L.nev++), s));
             L.expand_launches += 2;
         }
     }
@@ -1491,7 +1537,9 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     CUDA_TRY(cudaMemsetAsync(ws->mkeys, 0xFF, (size_t)ws->slots * 16 * MAPCAP * 4, s));
     CUDA_TRY(cudaMemsetAsync(ws->mvals, 0xFF, (size_t)ws->slots * 16 * MAPCAP * 8, s));
     // ---- run 1: central keywords
+    L.t0 = std::chrono::steady_clock::now();
     run_phase<RowC, RowC>(L, gd, ws, 0, -1, depth + 1, 0);
+    L.mark(0);
     // ---- candidate CGs + recovery
     k_cand_sort<<<ws->slots, 1024, 4096 * 8, s>>>(gd, wd);
     L.check();
@@ -1508,13 +1556,18 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
         k_extract_cg_big<RowC><<<ws->big_ctas, 256, 0, s>>>(gd, wd);
         L.check();
     }
+    if (L.g->profiling) CUDA_TRY(cudaStreamSynchronize(s));
+    L.mark(1);
     // ---- run 2: marginal keywords
     run_phase<RowM, RowC>(L, gd, ws, 1, -1, depth + 1, total_cands);
+    L.mark(2);
     // ---- top-k and packing
     k_final_select<<<ws->slots, 256, 1024 * 16, s>>>(wd);
     L.check();
     k_final_lists<RowC><<<dim3(ws->kmax, ws->slots), 256, SORT_SMEM * 4, s>>>(gd, wd);
     L.check();
+    if (L.g->profiling) CUDA_TRY(cudaStreamSynchronize(s));
+    L.mark(3);
 }
 
 void run_batch(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
@@ -1665,12 +1718,25 @@ void add_stats(riki_graph *g, Workspace *ws, Launch &L, uint32_t nq) {
     unsigned long long prof[P_NPROF];
     CUDA_TRY(cudaMemcpyAsync(prof, ws->prof, sizeof(prof), cudaMemcpyDeviceToHost, L.s));
     CUDA_TRY(cudaStreamSynchronize(L.s));
+    for (uint32_t i = 0; i + 1 < L.nev; i += 2) {
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, ws->event(i), ws->event(i + 1)));
+        L.expand_ms += ms;
+    }
+    L.nev = 0;
     uint64_t rb = ws->last_rb[0];  // bytes per H row (approximation when phases differ)
     g->stats.expand_launches += L.expand_launches;
     g->stats.expand_ms += L.expand_ms;
     g->stats.expand_bytes += prof[P_ITEMS] * (12 + rb) + prof[P_EDGES] * (5 + rb) + prof[P_NEWCELLS] + prof[P_ENQ] * 4;
     g->stats.kernel_launches += L.launches;
     g->stats.queries += nq;
+    for (int i = 0; i < 4; i++) g->stats.section_ms[i] += L.sec_ms[i];
+    g->stats.levels += L.levels;
+    L.sec_ms[0] = L.sec_ms[1] = L.sec_ms[2] = L.sec_ms[3] = 0;
+    L.levels = 0;
+    L.launches = 0;
+    L.expand_ms = 0;
+    L.expand_launches = 0;
 }
 
 }  // namespace

@@ -48,7 +48,8 @@ class QueryStats(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [("expand_launches", C.c_uint64), ("expand_ms", C.c_double), ("expand_bytes", C.c_uint64),
-                ("relaxations", C.c_uint64), ("kernel_launches", C.c_uint64), ("queries", C.c_uint64)]
+                ("relaxations", C.c_uint64), ("kernel_launches", C.c_uint64), ("queries", C.c_uint64),
+                ("section_ms", C.c_double * 4), ("levels", C.c_uint64)]
 
 
 def declared_symbols():
@@ -277,7 +278,9 @@ class Graph:
     def stats(self) -> dict:
         s = Stats()
         _check(self.lib.riki_get_stats(self.h, C.byref(s)))
-        return {f: getattr(s, f) for f, _ in Stats._fields_}
+        d = {f: getattr(s, f) for f, _ in Stats._fields_}
+        d["section_ms"] = list(d["section_ms"])
+        return d
 
     def reset_stats(self):
         _check(self.lib.riki_reset_stats(self.h))
