@@ -166,6 +166,8 @@ def main():
     ap.add_argument("--latency-queries", type=int, default=40)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--quick", action="store_true", help="timed region only (for ncu launch lists)")
+    ap.add_argument("--slots", type=int, default=0, help="queries in flight per launch (0 = whole batch)")
+    ap.add_argument("--pull", action="store_true", help="enable the direction-optimising (pull) expansion")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -188,7 +190,8 @@ def main():
                                 2000 + args.config + 7919 * rank)
     g = P.Graph(kg.n_nodes, kg.src, kg.dst, kg.label_class, kg.term_ptr, kg.postings, device=dev)
     g.set_label_weights(0.5, kg.avg_hops)
-    g.set_batch_slots(min(nq, 1024))
+    g.set_batch_slots(args.slots or min(nq, 1024))
+    g.set_direction(1 if args.pull else 0)
     cp, ct = P.Graph._csr(qs.central)
     mp, mt = P.Graph._csr(qs.marginal)
     d_cp, d_ct, d_mp, d_mt = [torch.from_numpy(x.view(np.int64) if x.dtype == np.uint64 else x.view(np.int32))

@@ -202,6 +202,10 @@ riki_status riki_set_profiling(riki_graph *g, int on);
 riki_status riki_get_stats(const riki_graph *g, riki_stats *out);
 riki_status riki_reset_stats(riki_graph *g);
 riki_status riki_set_debug(riki_graph *g, int on);
+/* Expansion direction: 0 = push (Alg. 1 order; default), 1 = direction-optimising (bottom-up
+ * pull for frontiers large against the unvisited remainder, Beamer's rule; identical results,
+ * faster only when most gated/unblocked nodes end up reached). */
+riki_status riki_set_direction(riki_graph *g, int mode);
 /* Batch slots (queries in flight per launch); 0 = automatic from free device memory. */
 riki_status riki_set_batch_slots(riki_graph *g, uint32_t slots);
 /* device memory footprint of the resident graph and of the search workspace (bytes) */

@@ -246,6 +246,13 @@ riki_status riki_reset_stats(riki_graph *g) {
 riki_status riki_set_debug(riki_graph *g, int on) {
     return guard([&] { need(g, "null graph"); g->debug = on != 0; });
 }
+riki_status riki_set_direction(riki_graph *g, int mode) {
+    return guard([&] {
+        need(g, "null graph");
+        need(mode == 0 || mode == 1, "direction mode must be 0 or 1");
+        g->pull_on = mode == 1;
+    });
+}
 riki_status riki_set_batch_slots(riki_graph *g, uint32_t slots) {
     return guard([&] {
         need(g, "null graph");

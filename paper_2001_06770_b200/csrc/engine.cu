@@ -35,8 +35,8 @@ constexpr uint32_t CHUNK = 256;
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
 constexpr uint32_t SORT_SMEM = 8192;  // u32 keys sorted in shared memory
 
-enum Ctr { C_NHEAVY = 0, C_NNEWATT, C_NOVF, C_ACTIVE, C_TOTAL, C_NCAND_TOTAL, C_NOVF2, C_NCTR = 16 };
-enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_NPROF = 8 };
+enum Ctr { C_NHEAVY = 0, C_NNEWATT, C_NOVF, C_ACTIVE, C_TOTAL, C_NCAND_TOTAL, C_NOVF2, C_NPULL, C_NCTR = 16 };
+enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_PULLNODES, P_PULLEDGES, P_NPROF = 8 };
 enum Err { E_CAND = 1, E_HEAVY = 2, E_ARENA = 4, E_EXTRACT = 8, E_OUT = 16, E_UNRESOLVED = 32 };
 
 struct SlotState {
@@ -47,7 +47,7 @@ struct SlotState {
     double gamma;
     uint32_t in_phase, level;
     uint32_t nq[2];
-    uint32_t blocking, collect, stop_m;
+    uint32_t blocking, collect, stop_m, pull, reached;  // reached: new-node events this run
     uint32_t ncand, ncand_kept, n_extract;
     int32_t L_end[2];
     unsigned long long relax[2];
@@ -80,7 +80,8 @@ struct WsDev {
     uint64_t *ck;
     Cand *cd;
     u128 *rk;
-    uint32_t *offs, *coffs;
+    uint32_t *offs, *coffs, *pslots;
+    uint32_t track_reached;  // direction-optimising mode: count new nodes per slot
     uint4 *heavy;
     uint32_t heavy_cap;
     uint32_t *ctr;
@@ -91,8 +92,7 @@ struct WsDev {
     uint32_t ovf_cap;
     uint32_t *big;
     unsigned long long big_words;
-    uint32_t *mkeys;
-    unsigned long long *mvals;
+    uint4 *mtab;
     OutHdr *hdr;
     uint32_t *resid;
     uint32_t *out;
@@ -147,6 +147,8 @@ __global__ void k_phase_begin(WsDev w, int ph, int hitting_mode) {
     st.level = 0;
     st.nq[0] = st.nq[1] = 0;
     st.stop_m = 0;
+    st.reached = 0;
+    st.pull = 0;
     st.L_end[ph] = -1;
     if (hitting_mode >= 0) {  // debug boundary: 0 none, 1 central CF, 2 marginal stop rule
         st.blocking = hitting_mode == 1 || (hitting_mode == 2 && T >= 2);
@@ -193,6 +195,7 @@ template <class RowT> __global__ void k_seed(GraphDev g, WsDev w, int ph) {
             if ((Row<RowT>::eq(old, Row<RowT>::splat(0xFF)) & used) == used) {  // first seed of this node
                 uint32_t p = atomicAdd(&st.nq[0], 1u);
                 w.Q(s, 0)[p] = v;
+                atomicAdd(&st.reached, 1u);
             }
             if (st.collect && Row<RowT>::eq(nw, Row<RowT>::splat(0xFF)) == 0 &&
                 Row<RowT>::byte(old, j) == 0xFF) {
@@ -207,11 +210,18 @@ template <class RowT> __global__ void k_seed(GraphDev g, WsDev w, int ph) {
 // ====================================================================== plan / terminate
 // One block: per-slot termination check for level l, then an exclusive scan of the
 // frontier sizes of the slots that expand (flattened work index for k_expand).
-__global__ void k_plan(WsDev w, int ph, uint32_t l) {
+#ifndef PULL_ALPHA
+#define PULL_ALPHA 14
+#endif
+#ifndef PULL_MIN_DIV
+#define PULL_MIN_DIV 64
+#endif
+// pull_min: minimum frontier for bottom-up (0xFFFFFFFF disables it)
+__global__ void k_plan(WsDev w, int ph, uint32_t l, uint32_t pull_min) {
     __shared__ uint32_t sc[MAX_SLOTS];
-    __shared__ uint32_t nact;
+    __shared__ uint32_t nact, npull;
     uint32_t s = threadIdx.x;
-    if (s == 0) nact = 0;
+    if (s == 0) { nact = 0; npull = 0; }
     __syncthreads();
     uint32_t items = 0;
     if (s < w.nslots) {
@@ -227,10 +237,17 @@ __global__ void k_plan(WsDev w, int ph, uint32_t l) {
             if (stop || st.err) {
                 st.in_phase = 0;
                 st.L_end[ph] = (int32_t)l;
+                st.pull = 0;
             } else {
                 items = st.nq[cur];
                 st.nq[cur ^ 1] = 0;
                 atomicAdd(&nact, 1u);
+                // direction-optimising (Beamer): bottom-up once the frontier is large compared
+                // with what is still unvisited (estimate: V*T minus new-node events)
+                uint64_t total = (uint64_t)w.V * st.T[ph];
+                uint64_t unvisited = total > st.reached ? total - st.reached : 0;
+                st.pull = items >= pull_min && (uint64_t)items * PULL_ALPHA > unvisited;
+                if (st.pull) w.pslots[atomicAdd(&npull, 1u)] = s;
             }
         }
     }
@@ -249,6 +266,7 @@ __global__ void k_plan(WsDev w, int ph, uint32_t l) {
         w.ctr[C_ACTIVE] = nact;
         w.ctr[C_TOTAL] = sc[MAX_SLOTS - 1];
         w.ctr[C_NHEAVY] = 0;
+        w.ctr[C_NPULL] = npull;
     }
 }
 
@@ -287,8 +305,21 @@ __device__ __forceinline__ Relax<RowT> relax(RowT *H, uint32_t n, RowT hn, RowT 
 // separate flag array: the level stored in H is the frontier flag.
 constexpr uint32_t RETAINED = 0x80000000u;
 __device__ __forceinline__ void frontier_push(const WsDev &w, bool want, uint32_t s, uint32_t entry, uint32_t nxt) {
-    uint32_t pos = warp_append(want, s, &w.st[0].nq[nxt], sizeof(SlotState) / 4);
-    if (want) w.Q(s, nxt)[pos] = entry;
+    // warp-aggregated append; new (untagged) entries are also counted in st.reached, the
+    // visited estimate of the direction-optimising heuristic
+    uint32_t m = __ballot_sync(FULLMASK, want);
+    if (want) {
+        uint32_t peers = __match_any_sync(m, s);
+        uint32_t leader = __ffs(peers) - 1;
+        uint32_t rank = __popc(peers & lanemask_lt());
+        uint32_t base = 0;
+        if (lane_id() == leader) {
+            base = atomicAdd(&w.st[s].nq[nxt], __popc(peers));
+            if (w.track_reached && !(entry & RETAINED)) atomicAdd(&w.st[s].reached, __popc(peers));
+        }
+        base = __shfl_sync(peers, base, leader);
+        w.Q(s, nxt)[base + rank] = entry;
+    }
 }
 
 __device__ __forceinline__ void cand_push(const GraphDev &g, const WsDev &w, bool want, uint32_t s, uint32_t n,
@@ -337,7 +368,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
     for (uint32_t i = threadIdx.x; i <= ns; i += blockDim.x) s_offs[i] = w.offs[i];
     for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {
         const SlotState &st = w.st[i];
-        s_info[i] = st.blocking | st.collect << 1 | st.T[ph] << 8;
+        s_info[i] = st.blocking | st.collect << 1 | st.pull << 2 | st.T[ph] << 8;
     }
     __syncthreads();
     const uint32_t total = s_offs[ns];
@@ -383,8 +414,9 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
                     lo = newc ? rb : eqlo;
                     eq0 = eqlo;
                     len = hi - lo;
-                    p_edges += len;
                     relaxn = (hi - rb) * R::ones(newc) + (hi - eqlo) * R::ones(oldc);
+                    if (info & 4) len = 0;  // pull slot: relaxed bottom-up by k_pull
+                    p_edges += len;
                     if (len > HEAVY) {
                         uint32_t nch = (len + CHUNK - 1) / CHUNK;
                         uint32_t p = atomicAdd(&w.ctr[C_NHEAVY], nch);
@@ -543,6 +575,123 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
     }
 }
 
+// Bottom-up expansion of a dense level (direction-optimising BFS).  Node n with an infinite
+// column j takes h_nj = l + 1 iff some in-edge (f -> n) has a <= l, h_fj <= l and f is not
+// blocked at l.  This is exactly Alg. 1's push at level l: an unblocked f with
+// max(h_fj, a) < l would have relaxed the edge at an earlier level already.  Only n's own
+// thread writes its row (no atomics); in-rows are activation-sorted so the scan stops at
+// a > l, and as soon as every infinite column found a parent.  Heavy in-rows (internal ids
+// < Vh) are scanned by a warp, the rest by one thread each.
+template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_pull(GraphDev g, WsDev w, int ph, uint32_t l,
+                                                                             uint32_t nbh) {
+    typedef Row<RowT> R;
+    const uint32_t s = w.pslots[blockIdx.y];
+    const SlotState &st = w.st[s];
+    RowT *H = w.Hs<RowT>(ph, s);
+    const RowT used = used_mask<RowT>(st.T[ph]);
+    const RowT FF = R::splat(0xFF), L = R::splat(l);
+    const bool blocking = st.blocking, collect = st.collect;
+    const uint32_t nxt = (l & 1) ^ 1, lane = lane_id();
+    uint32_t p_nodes = 0, p_edges = 0, p_cells = 0, p_enq = 0;
+    if (blockIdx.x < nbh) {  // warp per heavy node
+        const uint32_t nw = nbh * (blockDim.x >> 5);
+        for (uint32_t n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < g.Vh; n += nw) {
+            RowT Rn = R::load(H + n);
+            RowT inf = R::eq(Rn, FF) & used;
+            RowT found = 0;
+            if (inf) {
+                p_nodes++;
+                uint32_t rb = __ldg(g.irow + n), re = __ldg(g.irow + n + 1);
+                for (uint32_t k0 = rb; k0 < re; k0 += 32) {
+                    uint32_t k = k0 + lane;
+                    uint32_t a = k < re ? __ldg(g.iact + k) : 0xFFu;
+                    RowT q = 0;
+                    if (a <= l) {
+                        RowT Rf = R::load(H + __ldg(g.isrc + k));
+                        RowT le = R::le(Rf, L);
+                        if (!(blocking && le == (RowT)~(RowT)0)) q = le & inf;
+                    }
+                    p_edges += (a <= l);
+                    if (sizeof(RowT) == 8) {
+                        found |= (RowT)__reduce_or_sync(FULLMASK, (uint32_t)q) |
+                                 ((RowT)__reduce_or_sync(FULLMASK, (uint32_t)((uint64_t)q >> 32)) << 32);
+                    } else {
+                        found |= (RowT)__reduce_or_sync(FULLMASK, (uint32_t)q);
+                    }
+                    if (found == inf || __shfl_sync(FULLMASK, a, 31) > l) break;
+                }
+            }
+            bool enq = false, id = false;
+            if (found && lane == 0) {
+                RowT nr = (Rn & ~found) | (found & R::splat(l + 1));
+                H[n] = nr;
+                enq = true;
+                id = collect && R::eq(nr, FF) == 0;
+                p_cells += R::ones(found);
+                p_enq++;
+            }
+            frontier_push(w, enq, s, n, nxt);
+            cand_push(g, w, id, s, n, l + 1);
+        }
+    } else {  // thread per light node
+        const uint32_t stride = (gridDim.x - nbh) * blockDim.x;
+        for (uint32_t n0 = g.Vh + (blockIdx.x - nbh) * blockDim.x; n0 < w.V; n0 += stride) {
+            uint32_t n = n0 + threadIdx.x;
+            bool enq = false, id = false;
+            if (n < w.V) {
+                RowT Rn = R::load(H + n);
+                RowT inf = R::eq(Rn, FF) & used;
+                if (inf) {
+                    p_nodes++;
+                    RowT found = 0;
+                    uint32_t rb = __ldg(g.irow + n), re = __ldg(g.irow + n + 1);
+                    for (uint32_t k0 = rb; k0 < re && found != inf; k0 += 4) {
+                        uint32_t f[4];
+                        bool ok[4];
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            uint32_t k = k0 + u;
+                            ok[u] = k < re && __ldg(g.iact + k) <= l;
+                            f[u] = ok[u] ? __ldg(g.isrc + k) : 0;
+                        }
+                        RowT Rf[4];
+#pragma unroll
+                        for (int u = 0; u < 4; u++) Rf[u] = ok[u] ? R::load(H + f[u]) : FF;
+#pragma unroll
+                        for (int u = 0; u < 4; u++) {
+                            if (!ok[u]) continue;
+                            p_edges++;
+                            RowT le = R::le(Rf[u], L);
+                            if (!(blocking && le == (RowT)~(RowT)0)) found |= le & inf;
+                        }
+                        if (!ok[3]) break;  // activation-sorted: past the gate (or the row end)
+                    }
+                    if (found) {
+                        RowT nr = (Rn & ~found) | (found & R::splat(l + 1));
+                        H[n] = nr;
+                        enq = true;
+                        id = collect && R::eq(nr, FF) == 0;
+                        p_cells += R::ones(found);
+                        p_enq++;
+                    }
+                }
+            }
+            frontier_push(w, enq, s, n, nxt);
+            cand_push(g, w, id, s, n, l + 1);
+        }
+    }
+    p_nodes = warp_sum(p_nodes);
+    p_edges = warp_sum(p_edges);
+    p_cells = warp_sum(p_cells);
+    p_enq = warp_sum(p_enq);
+    if (lane == 0 && (p_nodes | p_edges)) {
+        atomicAdd(&w.prof[P_PULLNODES], (unsigned long long)p_nodes);
+        atomicAdd(&w.prof[P_PULLEDGES], (unsigned long long)p_edges);
+        atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
+        atomicAdd(&w.prof[P_ENQ], (unsigned long long)p_enq);
+    }
+}
+
 // ====================================================================== candidates
 __device__ void cta_sort_u64(uint64_t *keys, uint32_t n, uint64_t *smem, uint32_t smem_cap) {
     if (n < 2) return;
@@ -610,12 +759,30 @@ __global__ void k_scan_cands(WsDev w) {
 }
 
 // ====================================================================== recovery (Alg. 2)
+// Recovery code is written for a "group" of threads that cooperates on one candidate: a
+// single warp (fast tier, no block barriers) or a whole CTA (bigger tiers).
+struct GroupWarp {
+    __device__ __forceinline__ uint32_t rank() const { return lane_id(); }
+    __device__ __forceinline__ uint32_t size() const { return 32; }
+    __device__ __forceinline__ uint32_t warp() const { return 0; }
+    __device__ __forceinline__ uint32_t nwarps() const { return 1; }
+    __device__ __forceinline__ void sync() const { __syncwarp(); }
+};
+struct GroupCTA {
+    __device__ __forceinline__ uint32_t rank() const { return threadIdx.x; }
+    __device__ __forceinline__ uint32_t size() const { return blockDim.x; }
+    __device__ __forceinline__ uint32_t warp() const { return threadIdx.x >> 5; }
+    __device__ __forceinline__ uint32_t nwarps() const { return blockDim.x >> 5; }
+    __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
+
 // Hash set of node ids that records its insertions (items = insertion order, slots = where
 // they live), so clearing and enumerating cost O(inserted), not O(capacity).
 struct HSet {
     uint32_t *keys, *items, *slots;
     uint32_t cap, items_cap;  // cap: power of two
     uint32_t *count;          // shared/global counter
+    // returns the insertion index (>= 0), -1 if k was present, -2 on overflow
     __device__ __forceinline__ int insert(uint32_t k, uint32_t *ovf) const {
         uint32_t h = HashSet::hash(k) & (cap - 1);
         for (uint32_t i = 0; i < cap; i++) {
@@ -623,13 +790,14 @@ struct HSet {
             uint32_t prev = atomicCAS(&keys[sl], EMPTY, k);
             if (prev == EMPTY) {
                 uint32_t idx = atomicAdd(count, 1u);
-                if (idx < items_cap) { items[idx] = k; slots[idx] = sl; } else *ovf = 1;
-                return 1;
+                if (idx < items_cap) { items[idx] = k; slots[idx] = sl; return (int)idx; }
+                *ovf = 1;
+                return -2;
             }
-            if (prev == k) return 0;
+            if (prev == k) return -1;
         }
         *ovf = 1;
-        return -1;
+        return -2;
     }
     __device__ __forceinline__ int find(uint32_t k) const {
         uint32_t h = HashSet::hash(k) & (cap - 1);
@@ -641,16 +809,16 @@ struct HSet {
         }
         return -1;
     }
-    // CTA-wide; call with all threads, followed by __syncthreads by the caller
-    __device__ __forceinline__ void clear_inserted(bool full) const {
+    template <class G> __device__ __forceinline__ void clear_inserted(const G &G_, bool full) const {
         uint32_t n = min(*count, items_cap);
-        if (full) for (uint32_t i = threadIdx.x; i < cap; i += blockDim.x) keys[i] = EMPTY;
-        else for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) keys[slots[i]] = EMPTY;
+        if (full) for (uint32_t i = G_.rank(); i < cap; i += G_.size()) keys[i] = EMPTY;
+        else for (uint32_t i = G_.rank(); i < n; i += G_.size()) keys[slots[i]] = EMPTY;
     }
 };
 
 struct ExBuf {
     HSet hu, hk;          // union of nodes; per-keyword visited set whose items are the BFS queue
+    uint8_t *qh;          // hitting level of each queue item (parallel to hk.items)
     uint32_t *edges, *uf;
     uint8_t *flag;
     uint32_t cap_e;
@@ -668,47 +836,50 @@ struct ExShared {
 constexpr uint32_t MAPCAP = 8192;
 constexpr unsigned long long NOT_READY = ~0ull;
 
+// Map entry (16 B): {key, -, (cnt, off) as one 64-bit word}; one 16-byte load finds a
+// published list.  List entries are 3 words: (n, caller edge id, h_n).  Called by a warp.
 template <class RowT>
 __device__ void dag_list(const GraphDev &g, const WsDev &w, uint32_t s, int ph, int j, const RowT *H, bool blocking,
                          uint32_t q, uint32_t hq, uint32_t *off_out, uint32_t *cnt_out) {
     typedef Row<RowT> R;
     const uint32_t lane = lane_id();
-    const size_t mi = ((size_t)s * 16 + ph * 8 + j) * MAPCAP;
-    uint32_t *keys = w.mkeys + mi;
-    unsigned long long *vals = w.mvals + mi;
+    uint4 *tab = w.mtab + ((size_t)s * 16 + ph * 8 + j) * MAPCAP;
     int state = 0;  // 0 full (compute, no cache), 1 claimed (compute + publish), 2 found
     uint32_t slot = 0;
+    unsigned long long v = NOT_READY;
     if (lane == 0) {
         uint32_t h = HashSet::hash(q) & (MAPCAP - 1);
         for (uint32_t i = 0; i < 64; i++) {  // bounded probe: a full neighbourhood just disables caching
             uint32_t sl = (h + i) & (MAPCAP - 1);
-            uint32_t prev = atomicCAS(&keys[sl], EMPTY, q);
-            if (prev == EMPTY) { state = 1; slot = sl; break; }
-            if (prev == q) { state = 2; slot = sl; break; }
+            uint4 e = __ldcg(tab + sl);
+            if (e.x == q) { state = 2; slot = sl; v = (unsigned long long)e.w << 32 | e.z; break; }
+            if (e.x == EMPTY) {
+                uint32_t prev = atomicCAS(&tab[sl].x, EMPTY, q);
+                if (prev == EMPTY) { state = 1; slot = sl; break; }
+                if (prev == q) { state = 2; slot = sl; break; }
+            }
+        }
+        if (state == 2 && v == NOT_READY) {
+            volatile unsigned long long *vv = (volatile unsigned long long *)&tab[slot].z;
+            while ((v = *vv) == NOT_READY) __nanosleep(32);
         }
     }
     state = __shfl_sync(FULLMASK, state, 0);
-    slot = __shfl_sync(FULLMASK, slot, 0);
-    if (state == 2) {
-        unsigned long long v = 0;
-        if (lane == 0) {
-            volatile unsigned long long *vv = vals + slot;
-            while ((v = *vv) == NOT_READY) __nanosleep(64);
-            __threadfence();
-        }
+    if (state == 2) {  // list reads below depend on (off, cnt) and go through L2 (__ldcg)
         v = __shfl_sync(FULLMASK, v, 0);
         *off_out = (uint32_t)(v >> 32);
         *cnt_out = (uint32_t)v;
         return;
     }
-    uint32_t rb = g.irow[q], re = g.irow[q + 1];
+    slot = __shfl_sync(FULLMASK, slot, 0);
+    uint32_t rb = __ldg(g.irow + q), re = __ldg(g.irow + q + 1);
     uint32_t hi = 0;
     if (lane == 0) hi = upper_bound_act(g.iact, rb, re, hq - 1);  // in-rows are activation-sorted
     hi = __shfl_sync(FULLMASK, hi, 0);
     uint32_t off = 0;
     if (lane == 0) {
-        unsigned long long p = atomicAdd(w.arena_used, 2ull * (hi - rb));
-        if (p + 2ull * (hi - rb) > w.arena_cap) { atomicOr(&w.st[s].err, (uint32_t)E_ARENA); off = EMPTY; }
+        unsigned long long p = atomicAdd(w.arena_used, 3ull * (hi - rb));
+        if (p + 3ull * (hi - rb) > w.arena_cap) { atomicOr(&w.st[s].err, (uint32_t)E_ARENA); off = EMPTY; }
         else off = (uint32_t)p;
     }
     off = __shfl_sync(FULLMASK, off, 0);
@@ -720,8 +891,8 @@ __device__ void dag_list(const GraphDev &g, const WsDev &w, uint32_t s, int ph, 
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 uint32_t k = k0 + u * 32 + lane;
-                n[u] = k < hi ? g.isrc[k] : 0;
-                a[u] = k < hi ? g.iact[k] : 0xFF;
+                n[u] = k < hi ? __ldg(g.isrc + k) : 0;
+                a[u] = k < hi ? __ldg(g.iact + k) : 0xFF;
             }
 #pragma unroll
             for (int u = 0; u < 4; u++) Rn[u] = (k0 + u * 32 + lane < hi) ? R::load(H + n[u]) : R::splat(0xFF);
@@ -740,9 +911,10 @@ __device__ void dag_list(const GraphDev &g, const WsDev &w, uint32_t s, int ph, 
                 }
                 uint32_t m = __ballot_sync(FULLMASK, ok);
                 if (ok) {
-                    uint32_t p = off + 2 * (cnt + __popc(m & lanemask_lt()));
-                    w.arena[p] = n[u] | (hn[u] == 0 ? 0x80000000u : 0u);
-                    w.arena[p + 1] = g.ieid[k];
+                    uint32_t p = off + 3 * (cnt + __popc(m & lanemask_lt()));
+                    w.arena[p] = n[u];
+                    w.arena[p + 1] = __ldg(g.ieid + k);
+                    w.arena[p + 2] = hn[u];
                 }
                 cnt += __popc(m);
             }
@@ -750,7 +922,7 @@ __device__ void dag_list(const GraphDev &g, const WsDev &w, uint32_t s, int ph, 
     }
     if (state == 1 && lane == 0) {
         __threadfence();
-        atomicExch(vals + slot, off == EMPTY ? 0ull : ((unsigned long long)off << 32 | cnt));
+        atomicExch((unsigned long long *)&tab[slot].z, off == EMPTY ? 0ull : ((unsigned long long)off << 32 | cnt));
     }
     *off_out = off == EMPTY ? 0 : off;
     *cnt_out = off == EMPTY ? 0 : cnt;
@@ -758,34 +930,36 @@ __device__ void dag_list(const GraphDev &g, const WsDev &w, uint32_t s, int ph, 
 
 // Reverse BFS for keyword column j (Alg. 2 lines 4-10): edge (n -> q) is recovered iff it
 // is in q's DAG list; n is continued from iff h_nj != 0 (line 10) and unvisited (R17).
-// hk.items (the queue) holds the sources on entry.
-template <class RowT>
-__device__ void bfs_column(const GraphDev &g, const WsDev &w, uint32_t s, int ph, int j, const RowT *H,
+// hk.items (the queue) and qh hold the sources and their levels on entry.
+template <class G, class RowT>
+__device__ void bfs_column(const G &G_, const GraphDev &g, const WsDev &w, uint32_t s, int ph, int j, const RowT *H,
                            bool blocking, const ExBuf &b, ExShared &sh) {
-    typedef Row<RowT> R;
-    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const uint32_t lane = lane_id(), warp = G_.warp(), nw = G_.nwarps();
     uint32_t head = 0, tail = min(sh.nk, b.hk.items_cap);
     while (head < tail) {
         for (uint32_t it = head + warp; it < tail; it += nw) {
             uint32_t q = b.hk.items[it];
-            uint32_t hq = R::byte(R::load(H + q), j);
+            uint32_t hq = b.qh[it];
             if (hq == 0 || hq == 0xFF) continue;
             uint32_t off, cnt;
             dag_list<RowT>(g, w, s, ph, j, H, blocking, q, hq, &off, &cnt);
             for (uint32_t t = lane; t < cnt; t += 32) {
-                uint32_t nx = w.arena[off + 2 * t], eid = w.arena[off + 2 * t + 1];
-                uint32_t n = nx & 0x7FFFFFFFu;
+                uint32_t n = __ldcg(w.arena + off + 3 * t), eid = __ldcg(w.arena + off + 3 * t + 1);
+                uint32_t hn = __ldcg(w.arena + off + 3 * t + 2);
                 uint32_t pos = atomicAdd(&sh.nedges, 1u);
                 if (pos < b.cap_e) b.edges[pos] = eid; else sh.ovf = 1;
                 b.hu.insert(n, &sh.ovf);
-                if (!(nx >> 31)) b.hk.insert(n, &sh.ovf);
+                if (hn != 0) {
+                    int idx = b.hk.insert(n, &sh.ovf);
+                    if (idx >= 0) b.qh[idx] = (uint8_t)hn;
+                }
             }
         }
-        __syncthreads();
+        G_.sync();
         head = tail;
         tail = min(sh.nk, b.hk.items_cap);
         bool stop = sh.ovf;
-        __syncthreads();
+        G_.sync();
         if (stop) break;
     }
 }
@@ -799,79 +973,91 @@ __device__ __forceinline__ uint32_t arena_alloc(const WsDev &w, uint32_t words, 
     return (uint32_t)p;
 }
 
-__device__ __forceinline__ void ex_reset(const ExBuf &b, ExShared &sh) {
+template <class G> __device__ __forceinline__ void ex_reset(const G &G_, const ExBuf &b, ExShared &sh) {
     bool full = sh.dirty;
-    b.hu.clear_inserted(full);
-    b.hk.clear_inserted(full);
-    __syncthreads();
-    if (threadIdx.x == 0) { sh.nu = 0; sh.nk = 0; sh.nedges = 0; sh.ovf = 0; sh.dirty = 0; }
-    __syncthreads();
+    b.hu.clear_inserted(G_, full);
+    b.hk.clear_inserted(G_, full);
+    G_.sync();
+    if (G_.rank() == 0) { sh.nu = 0; sh.nk = 0; sh.nedges = 0; sh.ovf = 0; sh.dirty = 0; }
+    G_.sync();
 }
-__device__ __forceinline__ void ex_reset_hk(const ExBuf &b, ExShared &sh) {
-    b.hk.clear_inserted(sh.dirty != 0);
-    __syncthreads();
-    if (threadIdx.x == 0) sh.nk = 0;
-    __syncthreads();
+template <class G> __device__ __forceinline__ void ex_reset_hk(const G &G_, const ExBuf &b, ExShared &sh) {
+    b.hk.clear_inserted(G_, sh.dirty != 0);
+    G_.sync();
+    if (G_.rank() == 0) sh.nk = 0;
+    G_.sync();
+}
+template <class G> __device__ __forceinline__ void ex_init(const G &G_, const ExBuf &b, ExShared &sh) {
+    if (G_.rank() == 0) sh.dirty = 1;
+    G_.sync();
+    ex_reset(G_, b, sh);
 }
 
 // CG of candidate (s, c): union over central keywords of the recovered SP(c_j, v~).
 // Writes nodes, edge ids and V_C (nodes holding a central keyword) to the arena.
-template <class RowC> __device__ void extract_cg(const GraphDev &g, const WsDev &w, uint32_t s, uint32_t c,
-                                                 const ExBuf &b, ExShared &sh, bool *overflow) {
+template <class G, class RowC> __device__ void extract_cg(const G &G_, const GraphDev &g, const WsDev &w, uint32_t s,
+                                                          uint32_t c, const ExBuf &b, ExShared &sh, bool *overflow) {
     typedef Row<RowC> R;
     const SlotState &st = w.st[s];
     Cand &cd = w.CD(s)[c];
     const RowC *H = w.Hs<RowC>(0, s);
     const uint32_t T = st.T[0];
     const uint32_t v = cd.v;
-    if (threadIdx.x == 0) b.hu.insert(v, &sh.ovf);
+    if (G_.rank() == 0) b.hu.insert(v, &sh.ovf);
+    const RowC Rv = R::load(H + v);
     for (uint32_t j = 0; j < T; j++) {
-        if (threadIdx.x == 0) b.hk.insert(v, &sh.ovf);
-        __syncthreads();
-        bfs_column<RowC>(g, w, s, 0, j, H, true, b, sh);
+        if (G_.rank() == 0) {
+            int idx = b.hk.insert(v, &sh.ovf);
+            if (idx >= 0) b.qh[idx] = (uint8_t)R::byte(Rv, j);
+        }
+        G_.sync();
+        bfs_column(G_, g, w, s, 0, j, H, true, b, sh);
         if (sh.ovf) break;
-        ex_reset_hk(b, sh);
+        ex_reset_hk(G_, b, sh);
     }
-    __syncthreads();
+    G_.sync();
     if (sh.ovf) { *overflow = true; return; }
     *overflow = false;
     const uint32_t nn = min(sh.nu, b.hu.items_cap), ne = min(sh.nedges, b.cap_e);
     RowC used = used_mask<RowC>(T);
-    if (threadIdx.x == 0) sh.cnt = 0;
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x)
+    if (G_.rank() == 0) sh.cnt = 0;
+    G_.sync();
+    for (uint32_t i = G_.rank(); i < nn; i += G_.size())
         if (R::eq(R::load(H + b.hu.items[i]), 0) & used) atomicAdd(&sh.cnt, 1u);
-    __syncthreads();
+    G_.sync();
     const uint32_t nvc = sh.cnt;
-    if (threadIdx.x == 0) { sh.off = arena_alloc(w, nn + ne + nvc, s); sh.cnt = 0; }
-    __syncthreads();
+    G_.sync();
+    if (G_.rank() == 0) { sh.off = arena_alloc(w, nn + ne + nvc, s); sh.cnt = 0; }
+    G_.sync();
     const uint32_t off = sh.off;
     if (off != EMPTY) {
-        for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
+        for (uint32_t i = G_.rank(); i < nn; i += G_.size()) {
             uint32_t x = b.hu.items[i];
             w.arena[off + i] = x;
             if (R::eq(R::load(H + x), 0) & used) w.arena[off + nn + ne + atomicAdd(&sh.cnt, 1u)] = x;
         }
-        for (uint32_t i = threadIdx.x; i < ne; i += blockDim.x) w.arena[off + nn + i] = b.edges[i];
+        for (uint32_t i = G_.rank(); i < ne; i += G_.size()) w.arena[off + nn + i] = b.edges[i];
     }
-    __syncthreads();
-    if (threadIdx.x == 0 && off != EMPTY) {
+    G_.sync();
+    if (G_.rank() == 0 && off != EMPTY) {
         cd.nodes_off = off; cd.n_nodes = nn;
         cd.edges_off = off + nn; cd.n_edges = ne;
         cd.vc_off = off + nn + ne; cd.n_vc = nvc;
     }
 }
 
-// shared-memory tiers: 0 = small (64 threads, 15 KB), 1 = medium (256 threads, 58 KB);
-// a candidate that overflows a tier is re-run by the next one, the last tier being global
-// scratch sized by V (big_buf), so recovery is exact for any size.
+// Tiers: 0 = one warp per candidate with 7 KB of shared memory (4 warps per CTA);
+// 1 = one CTA (256 threads) per candidate with 58 KB; 2 = global scratch sized by V.  A
+// candidate that overflows a tier is re-run by the next one, so recovery is exact at any size.
 template <int TIER> struct Tier;
-template <> struct Tier<0> { static constexpr uint32_t FU = 512, FUI = 256, FK = 512, FKI = 256, FE = 1024, THREADS = 64; };
-template <> struct Tier<1> { static constexpr uint32_t FU = 2048, FUI = 1024, FK = 2048, FKI = 1024, FE = 4096, THREADS = 256; };
-template <int TIER> constexpr size_t smem_ex() {
-    return (size_t)(Tier<TIER>::FU + 2 * Tier<TIER>::FUI + Tier<TIER>::FK + 2 * Tier<TIER>::FKI + Tier<TIER>::FE +
-                    Tier<TIER>::FU) * 4 + Tier<TIER>::FU;
+template <> struct Tier<0> { static constexpr uint32_t FU = 256, FUI = 128, FK = 256, FKI = 128, FE = 512, GROUPS = 4; };
+template <> struct Tier<1> { static constexpr uint32_t FU = 2048, FUI = 1024, FK = 2048, FKI = 1024, FE = 4096, GROUPS = 1; };
+template <int TIER> constexpr size_t smem_group() {
+    return ((size_t)(Tier<TIER>::FU + 2 * Tier<TIER>::FUI + Tier<TIER>::FK + 2 * Tier<TIER>::FKI + Tier<TIER>::FE +
+                     Tier<TIER>::FU) * 4 + Tier<TIER>::FU + Tier<TIER>::FKI + 15) & ~(size_t)15;
 }
+template <int TIER> constexpr size_t smem_ex() { return smem_group<TIER>() * Tier<TIER>::GROUPS; }
+template <int TIER> constexpr uint32_t tier_threads() { return TIER == 0 ? 32 * Tier<0>::GROUPS : 256; }
 
 template <int TIER> __device__ __forceinline__ ExBuf smem_buf(uint8_t *sm, ExShared &sh) {
     typedef Tier<TIER> C;
@@ -885,11 +1071,12 @@ template <int TIER> __device__ __forceinline__ ExBuf smem_buf(uint8_t *sm, ExSha
     p += C::FE;
     b.uf = p;
     b.flag = (uint8_t *)(p + C::FU);
+    b.qh = b.flag + C::FU;
     return b;
 }
 
 __device__ __forceinline__ ExBuf big_buf(const WsDev &w, uint32_t cta, ExShared &sh) {
-    // global scratch for the overflow path; capacities scale with V
+    // global scratch for the last tier; capacities scale with V
     uint32_t *p = w.big + w.big_words * cta;
     const uint32_t cu = next_pow2(2 * w.V + 2), ni = w.V + 1;
     ExBuf b;
@@ -901,58 +1088,73 @@ __device__ __forceinline__ ExBuf big_buf(const WsDev &w, uint32_t cta, ExShared 
     p += cu;
     b.flag = (uint8_t *)p;
     p += cu / 4 + 4;
+    b.qh = (uint8_t *)p;
+    p += ni / 4 + 4;
     b.edges = p;
     unsigned long long rem = w.big_words - (unsigned long long)(p - (w.big + w.big_words * cta));
     b.cap_e = (uint32_t)(rem < 0xFFFFFFFFull ? rem : 0xFFFFFFFFull);
     return b;
 }
 
-__device__ __forceinline__ void ex_init(const ExBuf &b, ExShared &sh) {
-    if (threadIdx.x == 0) sh.dirty = 1;
-    __syncthreads();
-    ex_reset(b, sh);
+// overflow hand-off to the next tier
+__device__ __forceinline__ void push_overflow(const WsDev &w, int tier, uint2 sc) {
+    uint32_t *ctr = &w.ctr[tier == 0 ? C_NOVF : C_NOVF2];
+    uint2 *lst = tier == 0 ? w.ovf : w.ovf2;
+    uint32_t p = atomicAdd(ctr, 1u);
+    if (p < w.ovf_cap) lst[p] = sc; else atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT);
 }
 
-// Tier 0 takes the candidates from the flattened (slot, candidate) range; tier 1 and the
-// global tier take the overflow list of the previous tier.
-template <class RowC, int TIER> __global__ void __launch_bounds__(Tier<TIER>::THREADS) k_extract_cg(GraphDev g, WsDev w) {
+// Tier 0 takes the candidates from the flattened (slot, candidate) range (one warp each);
+// tier 1 and tier 2 take the overflow list of the previous tier.
+template <class RowC, int TIER> __global__ void __launch_bounds__(tier_threads<TIER>()) k_extract_cg(GraphDev g, WsDev w) {
     extern __shared__ __align__(16) uint8_t smx[];
-    __shared__ ExShared sh;
-    uint32_t total = TIER == 0 ? w.coffs[w.nslots] : min(w.ctr[C_NOVF], w.ovf_cap);
-    if (blockIdx.x >= total) return;
-    ExBuf b = smem_buf<TIER>(smx, sh);
-    ex_init(b, sh);
-    for (uint32_t item = blockIdx.x; item < total; item += gridDim.x) {
-        uint32_t s, c;
-        if (TIER == 0) { s = find_slot(w.coffs, w.nslots, item); c = item - w.coffs[s]; }
-        else { uint2 x = w.ovf[item]; s = x.x; c = x.y; }
-        bool ovf = false;
-        extract_cg<RowC>(g, w, s, c, b, sh, &ovf);
-        if (ovf && threadIdx.x == 0) {
-            sh.dirty = 1;
-            uint32_t *ctr = &w.ctr[TIER == 0 ? C_NOVF : C_NOVF2];
-            uint2 *lst = TIER == 0 ? w.ovf : w.ovf2;
-            uint32_t p = atomicAdd(ctr, 1u);
-            if (p < w.ovf_cap) lst[p] = make_uint2(s, c); else atomicOr(&w.st[s].err, (uint32_t)E_EXTRACT);
+    __shared__ ExShared shs[Tier<TIER>::GROUPS];
+    const uint32_t total = TIER == 0 ? w.coffs[w.nslots] : min(w.ctr[C_NOVF], w.ovf_cap);
+    const uint32_t gi = TIER == 0 ? threadIdx.x >> 5 : 0;
+    ExShared &sh = shs[gi];
+    ExBuf b = smem_buf<TIER>(smx + smem_group<TIER>() * gi, sh);
+    const uint32_t first = blockIdx.x * Tier<TIER>::GROUPS + gi, stride = gridDim.x * Tier<TIER>::GROUPS;
+    if (TIER == 0) {
+        GroupWarp G_;
+        if (first >= total) return;
+        ex_init(G_, b, sh);
+        for (uint32_t item = first; item < total; item += stride) {
+            uint32_t s = find_slot(w.coffs, w.nslots, item), c = item - w.coffs[s];
+            bool ovf = false;
+            extract_cg<GroupWarp, RowC>(G_, g, w, s, c, b, sh, &ovf);
+            if (ovf && G_.rank() == 0) { sh.dirty = 1; push_overflow(w, 0, make_uint2(s, c)); }
+            G_.sync();
+            ex_reset(G_, b, sh);
         }
-        __syncthreads();
-        ex_reset(b, sh);
+    } else {
+        GroupCTA G_;
+        if (first >= total) return;
+        ex_init(G_, b, sh);
+        for (uint32_t item = first; item < total; item += stride) {
+            uint2 x = w.ovf[item];
+            bool ovf = false;
+            extract_cg<GroupCTA, RowC>(G_, g, w, x.x, x.y, b, sh, &ovf);
+            if (ovf && G_.rank() == 0) { sh.dirty = 1; push_overflow(w, 1, x); }
+            G_.sync();
+            ex_reset(G_, b, sh);
+        }
     }
 }
 
 template <class RowC> __global__ void __launch_bounds__(256) k_extract_cg_big(GraphDev g, WsDev w) {
     __shared__ ExShared sh;
+    GroupCTA G_;
     uint32_t n = min(w.ctr[C_NOVF2], w.ovf_cap);
     if (blockIdx.x >= n) return;
     ExBuf b = big_buf(w, blockIdx.x, sh);
-    ex_init(b, sh);
+    ex_init(G_, b, sh);
     for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
         uint2 sc = w.ovf2[i];
         bool ovf = false;
-        extract_cg<RowC>(g, w, sc.x, sc.y, b, sh, &ovf);
-        if (ovf && threadIdx.x == 0) { sh.dirty = 1; atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT); }
-        __syncthreads();
-        ex_reset(b, sh);
+        extract_cg<GroupCTA, RowC>(G_, g, w, sc.x, sc.y, b, sh, &ovf);
+        if (ovf && G_.rank() == 0) { sh.dirty = 1; atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT); }
+        G_.sync();
+        ex_reset(G_, b, sh);
     }
 }
 
@@ -1010,8 +1212,8 @@ __device__ __forceinline__ void uf_union(uint32_t *uf, uint32_t a, uint32_t b) {
 
 // RPG of an attached candidate: G^r = CG u (u_i SP(m_i, V_C)) recovered from the V_C nodes
 // at distance D_gi (R18), then PTC (R19').
-template <class RowM> __device__ void extract_rpg(const GraphDev &g, const WsDev &w, uint32_t s, uint32_t c,
-                                                  const ExBuf &b, ExShared &sh, bool *overflow) {
+template <class G, class RowM> __device__ void extract_rpg(const G &G_, const GraphDev &g, const WsDev &w, uint32_t s,
+                                                           uint32_t c, const ExBuf &b, ExShared &sh, bool *overflow) {
     typedef Row<RowM> R;
     SlotState &st = w.st[s];
     Cand &cd = w.CD(s)[c];
@@ -1022,23 +1224,26 @@ template <class RowM> __device__ void extract_rpg(const GraphDev &g, const WsDev
         *overflow = true;
         return;
     }
-    for (uint32_t i = threadIdx.x; i < cd.n_nodes; i += blockDim.x) b.hu.insert(w.arena[cd.nodes_off + i], &sh.ovf);
-    for (uint32_t i = threadIdx.x; i < cd.n_edges; i += blockDim.x) b.edges[i] = w.arena[cd.edges_off + i];
-    if (threadIdx.x == 0) sh.nedges = cd.n_edges;
-    __syncthreads();
+    for (uint32_t i = G_.rank(); i < cd.n_nodes; i += G_.size()) b.hu.insert(w.arena[cd.nodes_off + i], &sh.ovf);
+    for (uint32_t i = G_.rank(); i < cd.n_edges; i += G_.size()) b.edges[i] = w.arena[cd.edges_off + i];
+    if (G_.rank() == 0) sh.nedges = cd.n_edges;
+    G_.sync();
     for (uint32_t j = 0; j < T && !sh.ovf; j++) {
         const uint32_t dj = cd.mdist[j];
-        for (uint32_t t = threadIdx.x; t < cd.n_vc; t += blockDim.x) {
+        for (uint32_t t = G_.rank(); t < cd.n_vc; t += G_.size()) {
             uint32_t v = w.arena[cd.vc_off + t];
-            if (R::byte(R::load(H + v), j) == dj) b.hk.insert(v, &sh.ovf);
+            if (R::byte(R::load(H + v), j) == dj) {
+                int idx = b.hk.insert(v, &sh.ovf);
+                if (idx >= 0) b.qh[idx] = (uint8_t)dj;
+            }
         }
-        __syncthreads();
-        if (!sh.ovf) bfs_column<RowM>(g, w, s, 1, j, H, blocking, b, sh);
-        __syncthreads();
+        G_.sync();
+        if (!sh.ovf) bfs_column(G_, g, w, s, 1, j, H, blocking, b, sh);
+        G_.sync();
         if (sh.ovf) break;
-        ex_reset_hk(b, sh);
+        ex_reset_hk(G_, b, sh);
     }
-    __syncthreads();
+    G_.sync();
     if (sh.ovf) { *overflow = true; return; }
     *overflow = false;
     const uint32_t nn = min(sh.nu, b.hu.items_cap), ne = min(sh.nedges, b.cap_e);
@@ -1047,19 +1252,19 @@ template <class RowM> __device__ void extract_rpg(const GraphDev &g, const WsDev
     uint32_t pass = 1;
     if (T >= 2) {
         RowM used = used_mask<RowM>(T);
-        for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
+        for (uint32_t i = G_.rank(); i < nn; i += G_.size()) {
             uint32_t sl = b.hu.slots[i];
             b.flag[sl] = 0;
             b.uf[sl] = sl;
         }
-        if (threadIdx.x == 0) { sh.nx = 0; sh.xvc = 0; sh.mnr = EMPTY; sh.mxr = 0; }
-        __syncthreads();
-        for (uint32_t t = threadIdx.x; t < cd.n_vc; t += blockDim.x) {
+        if (G_.rank() == 0) { sh.nx = 0; sh.xvc = 0; sh.mnr = EMPTY; sh.mxr = 0; }
+        G_.sync();
+        for (uint32_t t = G_.rank(); t < cd.n_vc; t += G_.size()) {
             int sl = b.hu.find(w.arena[cd.vc_off + t]);
             if (sl >= 0) b.flag[sl] = 1;
         }
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
+        G_.sync();
+        for (uint32_t i = G_.rank(); i < nn; i += G_.size()) {
             uint32_t sl = b.hu.slots[i];
             if (R::eq(R::load(H + b.hu.items[i]), 0) & used) {
                 b.flag[sl] |= 2;
@@ -1067,39 +1272,39 @@ template <class RowM> __device__ void extract_rpg(const GraphDev &g, const WsDev
                 if (b.flag[sl] & 1) sh.xvc = 1;
             }
         }
-        __syncthreads();
+        G_.sync();
         if (sh.nx < 2) pass = 0;
         else if (sh.xvc) pass = 1;
         else {
-            for (uint32_t i = threadIdx.x; i < ne; i += blockDim.x) {
+            for (uint32_t i = G_.rank(); i < ne; i += G_.size()) {
                 uint32_t e = b.edges[i];
                 int sa = b.hu.find(g.src[e]), sb = b.hu.find(g.dst[e]);
                 if (sa < 0 || sb < 0 || (b.flag[sa] & 1) || (b.flag[sb] & 1)) continue;
                 uf_union(b.uf, (uint32_t)sa, (uint32_t)sb);
             }
-            __syncthreads();
-            for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) {
+            G_.sync();
+            for (uint32_t i = G_.rank(); i < nn; i += G_.size()) {
                 uint32_t sl = b.hu.slots[i];
                 if ((b.flag[sl] & 3) != 2) continue;  // X outside V_C
                 uint32_t r = uf_find(b.uf, sl);
                 atomicMin(&sh.mnr, r);
                 atomicMax(&sh.mxr, r);
             }
-            __syncthreads();
+            G_.sync();
             pass = sh.mnr != sh.mxr;
         }
     }
-    __syncthreads();
+    G_.sync();
     // ---- write G^r lists
-    if (threadIdx.x == 0) sh.off = arena_alloc(w, nn + ne, s);
-    __syncthreads();
+    if (G_.rank() == 0) sh.off = arena_alloc(w, nn + ne, s);
+    G_.sync();
     const uint32_t off = sh.off;
     if (off != EMPTY) {
-        for (uint32_t i = threadIdx.x; i < nn; i += blockDim.x) w.arena[off + i] = b.hu.items[i];
-        for (uint32_t i = threadIdx.x; i < ne; i += blockDim.x) w.arena[off + nn + i] = b.edges[i];
+        for (uint32_t i = G_.rank(); i < nn; i += G_.size()) w.arena[off + i] = b.hu.items[i];
+        for (uint32_t i = G_.rank(); i < ne; i += G_.size()) w.arena[off + nn + i] = b.edges[i];
     }
-    __syncthreads();
-    if (threadIdx.x == 0 && off != EMPTY) {
+    G_.sync();
+    if (G_.rank() == 0 && off != EMPTY) {
         cd.nodes_off = off; cd.n_nodes = nn;
         cd.edges_off = off + nn; cd.n_edges = ne;
         cd.ptc = pass;
@@ -1112,42 +1317,55 @@ template <class RowM> __device__ void extract_rpg(const GraphDev &g, const WsDev
     }
 }
 
-template <class RowM, int TIER> __global__ void __launch_bounds__(Tier<TIER>::THREADS) k_extract_rpg(GraphDev g, WsDev w) {
+template <class RowM, int TIER> __global__ void __launch_bounds__(tier_threads<TIER>()) k_extract_rpg(GraphDev g, WsDev w) {
     extern __shared__ __align__(16) uint8_t smx[];
-    __shared__ ExShared sh;
-    uint32_t n = TIER == 0 ? w.ctr[C_NNEWATT] : min(w.ctr[C_NOVF], w.ovf_cap);
-    if (blockIdx.x >= n) return;
-    ExBuf b = smem_buf<TIER>(smx, sh);
-    ex_init(b, sh);
-    for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-        uint2 sc = TIER == 0 ? w.newatt[i] : w.ovf[i];
-        bool ovf = false;
-        extract_rpg<RowM>(g, w, sc.x, sc.y, b, sh, &ovf);
-        if (ovf && threadIdx.x == 0) {
-            sh.dirty = 1;
-            uint32_t *ctr = &w.ctr[TIER == 0 ? C_NOVF : C_NOVF2];
-            uint2 *lst = TIER == 0 ? w.ovf : w.ovf2;
-            uint32_t p = atomicAdd(ctr, 1u);
-            if (p < w.ovf_cap) lst[p] = sc; else atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT);
+    __shared__ ExShared shs[Tier<TIER>::GROUPS];
+    const uint32_t n = TIER == 0 ? w.ctr[C_NNEWATT] : min(w.ctr[C_NOVF], w.ovf_cap);
+    const uint32_t gi = TIER == 0 ? threadIdx.x >> 5 : 0;
+    ExShared &sh = shs[gi];
+    ExBuf b = smem_buf<TIER>(smx + smem_group<TIER>() * gi, sh);
+    const uint32_t first = blockIdx.x * Tier<TIER>::GROUPS + gi, stride = gridDim.x * Tier<TIER>::GROUPS;
+    if (TIER == 0) {
+        GroupWarp G_;
+        if (first >= n) return;
+        ex_init(G_, b, sh);
+        for (uint32_t i = first; i < n; i += stride) {
+            uint2 sc = w.newatt[i];
+            bool ovf = false;
+            extract_rpg<GroupWarp, RowM>(G_, g, w, sc.x, sc.y, b, sh, &ovf);
+            if (ovf && G_.rank() == 0) { sh.dirty = 1; push_overflow(w, 0, sc); }
+            G_.sync();
+            ex_reset(G_, b, sh);
         }
-        __syncthreads();
-        ex_reset(b, sh);
+    } else {
+        GroupCTA G_;
+        if (first >= n) return;
+        ex_init(G_, b, sh);
+        for (uint32_t i = first; i < n; i += stride) {
+            uint2 sc = w.ovf[i];
+            bool ovf = false;
+            extract_rpg<GroupCTA, RowM>(G_, g, w, sc.x, sc.y, b, sh, &ovf);
+            if (ovf && G_.rank() == 0) { sh.dirty = 1; push_overflow(w, 1, sc); }
+            G_.sync();
+            ex_reset(G_, b, sh);
+        }
     }
 }
 
 template <class RowM> __global__ void __launch_bounds__(256) k_extract_rpg_big(GraphDev g, WsDev w) {
     __shared__ ExShared sh;
+    GroupCTA G_;
     uint32_t n = min(w.ctr[C_NOVF2], w.ovf_cap);
     if (blockIdx.x >= n) return;
     ExBuf b = big_buf(w, blockIdx.x, sh);
-    ex_init(b, sh);
+    ex_init(G_, b, sh);
     for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
         uint2 sc = w.ovf2[i];
         bool ovf = false;
-        extract_rpg<RowM>(g, w, sc.x, sc.y, b, sh, &ovf);
-        if (ovf && threadIdx.x == 0) { sh.dirty = 1; atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT); }
-        __syncthreads();
-        ex_reset(b, sh);
+        extract_rpg<GroupCTA, RowM>(G_, g, w, sc.x, sc.y, b, sh, &ovf);
+        if (ovf && G_.rank() == 0) { sh.dirty = 1; atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT); }
+        G_.sync();
+        ex_reset(G_, b, sh);
     }
 }
 
@@ -1313,12 +1531,13 @@ __global__ void k_pack_H(GraphDev g, WsDev w, uint32_t T, uint8_t *Hout, uint8_t
 
 // ====================================================================== host side
 struct Workspace {
+    uint32_t track_reached = 0;
     uint32_t slots = 0, V = 0, W = 0, capc = 0, kmax = 0, heavy_cap = 0, ovf_cap = 0, big_ctas = 0;
     uint64_t arena_cap = 0, out_cap = 0, big_words = 0;
     uint8_t *H[2] = {nullptr, nullptr};
-    uint32_t *q = nullptr, *bm = nullptr, *offs = nullptr, *coffs = nullptr, *ctr = nullptr, *arena = nullptr,
-             *big = nullptr, *resid = nullptr, *out = nullptr, *mkeys = nullptr;
-    unsigned long long *mvals = nullptr;
+    uint32_t *q = nullptr, *bm = nullptr, *offs = nullptr, *coffs = nullptr, *pslots = nullptr, *ctr = nullptr, *arena = nullptr,
+             *big = nullptr, *resid = nullptr, *out = nullptr;
+    uint4 *mtab = nullptr;
     uint64_t *ck = nullptr;
     Cand *cd = nullptr;
     u128 *rk = nullptr;
@@ -1373,11 +1592,11 @@ struct Workspace {
         WsDev d;
         d.st = st; d.nslots = slots; d.V = V; d.W = W; d.capc = capc; d.kmax = kmax;
         d.H[0] = H[0]; d.H[1] = H[1]; d.rb[0] = last_rb[0]; d.rb[1] = last_rb[1];
-        d.q = q; d.bm = bm; d.ck = ck; d.cd = cd; d.rk = rk; d.offs = offs; d.coffs = coffs;
+        d.q = q; d.bm = bm; d.ck = ck; d.cd = cd; d.rk = rk; d.offs = offs; d.coffs = coffs; d.pslots = pslots; d.track_reached = track_reached;
         d.heavy = heavy; d.heavy_cap = heavy_cap; d.ctr = ctr; d.prof = prof;
         d.arena = arena; d.arena_used = arena_used; d.arena_cap = arena_cap;
         d.newatt = newatt; d.ovf = ovf; d.ovf2 = ovf2; d.ovf_cap = ovf_cap;
-        d.big = big; d.big_words = big_words; d.mkeys = mkeys; d.mvals = mvals;
+        d.big = big; d.big_words = big_words; d.mtab = mtab;
         d.hdr = hdr; d.resid = resid; d.out = out; d.out_used = out_used; d.out_cap = out_cap;
         return d;
     }
@@ -1411,6 +1630,7 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     ws->st = ws->alloc<SlotState>(S);
     ws->offs = ws->alloc<uint32_t>(S + 1);
     ws->coffs = ws->alloc<uint32_t>(S + 1);
+    ws->pslots = ws->alloc<uint32_t>(S + 1);
     uint64_t hc = (uint64_t)S * (g->E / CHUNK + g->E / HEAVY + 64);
     ws->heavy_cap = (uint32_t)std::min<uint64_t>(hc, 1u << 28);
     ws->heavy = ws->alloc<uint4>(ws->heavy_cap);
@@ -1424,9 +1644,8 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     ws->ovf2 = ws->alloc<uint2>(ws->ovf_cap);
     ws->big_ctas = V <= (4u << 20) ? 8 : 2;
     uint64_t cu = next_pow2(2 * V + 2);
-    ws->big_words = cu * 3 + 4ull * (V + 1) + cu / 4 + 16 + std::max<uint64_t>(std::min<uint64_t>(g->E, 1ull << 26), 1u << 20);
-    ws->mkeys = ws->alloc<uint32_t>(S * 16 * MAPCAP);
-    ws->mvals = ws->alloc<unsigned long long>(S * 16 * MAPCAP);
+    ws->big_words = cu * 3 + 4ull * (V + 1) + cu / 4 + (V + 1) / 4 + 32 + std::max<uint64_t>(std::min<uint64_t>(g->E, 1ull << 26), 1u << 20);
+    ws->mtab = ws->alloc<uint4>(S * 16 * MAPCAP);
     ws->big = ws->alloc<uint32_t>(ws->big_words * ws->big_ctas);
     ws->hdr = ws->alloc<OutHdr>(S * c.kmax);
     ws->resid = ws->alloc<uint32_t>(S * c.kmax);
@@ -1483,6 +1702,7 @@ template <class RowT, class RowC>
 void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting_mode, uint32_t max_levels,
                uint64_t total_cands) {
     cudaStream_t s = L.s;
+    ws->track_reached = L.g->pull_on ? 1 : 0;
     WsDev wd = ws->dev();
     k_phase_begin<<<(ws->slots + 127) / 128, 128, 0, s>>>(wd, ph, hitting_mode);
     L.check();
@@ -1497,7 +1717,7 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             if (total_cands) {
                 k_attach<RowT><<<grid_of(total_cands * 32, 256), 256, 0, s>>>(wd);
                 L.check();
-                k_extract_rpg<RowT, 0><<<148 * 14, 64, smem_ex<0>(), s>>>(gd, wd);
+                k_extract_rpg<RowT, 0><<<148 * 7, tier_threads<0>(), smem_ex<0>(), s>>>(gd, wd);
                 L.check();
                 k_extract_rpg<RowT, 1><<<148 * 3, 256, smem_ex<1>(), s>>>(gd, wd);
                 L.check();
@@ -1507,7 +1727,7 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             k_decide_m<<<ws->slots, 256, 1024 * 16, s>>>(wd, l);
             L.check();
         }
-        k_plan<<<1, MAX_SLOTS, 0, s>>>(wd, ph, l);
+        k_plan<<<1, MAX_SLOTS, 0, s>>>(wd, ph, l, !L.g->pull_on ? 0xFFFFFFFFu : std::max<uint32_t>(ws->V / PULL_MIN_DIV, 1));
         L.check();
         CUDA_TRY(cudaMemcpyAsync(ws->h_ctr, ws->ctr, C_NCTR * 4, cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
@@ -1519,9 +1739,15 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
         L.check();
         k_expand_heavy<RowT><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
         L.check();
+        if (uint32_t npull = ws->h_ctr[C_NPULL]) {
+            uint32_t nbh = (gd.Vh + 7) / 8;
+            uint32_t nbl = std::min<uint32_t>((ws->V - gd.Vh + 255) / 256, 148 * 8);
+            k_pull<RowT><<<dim3(nbh + std::max<uint32_t>(nbl, 1), npull), 256, 0, s>>>(gd, wd, ph, l, nbh);
+            L.check();
+        }
         if (L.g->profiling) {  // events are read after the batch: no extra sync per level
             CUDA_TRY(cudaEventRecord(ws->event(L.nev++), s));
-            L.expand_launches += 2;
+            L.expand_launches += 2 + (ws->h_ctr[C_NPULL] ? 1 : 0);
         }
     }
 }
@@ -1534,8 +1760,7 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     CUDA_TRY(cudaMemsetAsync(ws->arena_used, 0, 8, s));
     CUDA_TRY(cudaMemsetAsync(ws->out_used, 0, 8, s));
     CUDA_TRY(cudaMemsetAsync(ws->ctr, 0, C_NCTR * 4, s));
-    CUDA_TRY(cudaMemsetAsync(ws->mkeys, 0xFF, (size_t)ws->slots * 16 * MAPCAP * 4, s));
-    CUDA_TRY(cudaMemsetAsync(ws->mvals, 0xFF, (size_t)ws->slots * 16 * MAPCAP * 8, s));
+    CUDA_TRY(cudaMemsetAsync(ws->mtab, 0xFF, (size_t)ws->slots * 16 * MAPCAP * 16, s));
     // ---- run 1: central keywords
     L.t0 = std::chrono::steady_clock::now();
     run_phase<RowC, RowC>(L, gd, ws, 0, -1, depth + 1, 0);
@@ -1549,7 +1774,7 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     CUDA_TRY(cudaStreamSynchronize(s));
     uint64_t total_cands = ws->h_ctr[C_NCAND_TOTAL];
     if (total_cands) {
-        k_extract_cg<RowC, 0><<<grid_of(total_cands, 1, 148 * 14), 64, smem_ex<0>(), s>>>(gd, wd);
+        k_extract_cg<RowC, 0><<<grid_of(total_cands, Tier<0>::GROUPS, 148 * 7), tier_threads<0>(), smem_ex<0>(), s>>>(gd, wd);
         L.check();
         k_extract_cg<RowC, 1><<<148 * 3, 256, smem_ex<1>(), s>>>(gd, wd);
         L.check();
@@ -1727,7 +1952,8 @@ void add_stats(riki_graph *g, Workspace *ws, Launch &L, uint32_t nq) {
     uint64_t rb = ws->last_rb[0];  // bytes per H row (approximation when phases differ)
     g->stats.expand_launches += L.expand_launches;
     g->stats.expand_ms += L.expand_ms;
-    g->stats.expand_bytes += prof[P_ITEMS] * (12 + rb) + prof[P_EDGES] * (5 + rb) + prof[P_NEWCELLS] + prof[P_ENQ] * 4;
+    g->stats.expand_bytes += prof[P_ITEMS] * (12 + rb) + prof[P_EDGES] * (5 + rb) + prof[P_NEWCELLS] + prof[P_ENQ] * 4 +
+                             prof[P_PULLNODES] * (8 + rb) + prof[P_PULLEDGES] * (5 + rb);
     g->stats.kernel_launches += L.launches;
     g->stats.queries += nq;
     for (int i = 0; i < 4; i++) g->stats.section_ms[i] += L.sec_ms[i];
@@ -1800,7 +2026,7 @@ void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, ui
     try {
         for (size_t q0 = 0; q0 < qs.size();) {
             ensure_workspace(g, caps);
-            uint32_t slots = g->ws->slots;
+            uint32_t slots = std::min(g->ws->slots, caps.slots);
             uint32_t n = (uint32_t)std::min<size_t>(slots, qs.size() - q0);
             std::vector<uint32_t> qidx(n);
             for (uint32_t i = 0; i < n; i++) qidx[i] = (uint32_t)(q0 + i);

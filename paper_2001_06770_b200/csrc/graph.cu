@@ -160,6 +160,10 @@ __global__ void k_perm(const uint64_t *sorted, uint32_t V, uint32_t *perm, uint3
         iperm[r] = v;
     }
 }
+__global__ void k_count_heavy(const uint32_t *deg, uint32_t V, uint32_t thr, uint32_t *cnt) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
+        if (deg[v] > thr) atomicAdd(cnt, 1u);
+}
 __global__ void k_relabel(uint32_t *x, uint64_t n, const uint32_t *perm) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
         x[i] = perm[x[i]];
@@ -296,6 +300,13 @@ void graph_load(riki_graph *g, uint32_t V, uint64_t E, const uint32_t *src, cons
         void *t = dmalloc<uint8_t>(tmp);
         CUDA_TRY(cub::DeviceRadixSort::SortKeys(t, tmp, k1, k2, (int64_t)V, 0, 64, s));
         k_perm<<<grid_for(V), 256, 0, s>>>(k2, V, g->d_perm, g->d_iperm);
+        uint32_t *cnt = dmalloc<uint32_t>(1);
+        CUDA_TRY(cudaMemsetAsync(cnt, 0, 4, s));
+        // total degree = 2 x in-degree in the bidirected graph; heavy = in-degree > 32
+        k_count_heavy<<<grid_for(V), 256, 0, s>>>(deg, V, 64, cnt);
+        CUDA_TRY(cudaMemcpyAsync(&g->Vh, cnt, 4, cudaMemcpyDeviceToHost, s));
+        sync_check(s);
+        cudaFree(cnt);
         if (E) {
             k_relabel<<<grid_for(E), 256, 0, s>>>(g->d_src, E, g->d_perm);
             k_relabel<<<grid_for(E), 256, 0, s>>>(g->d_dst, E, g->d_perm);

@@ -26,6 +26,7 @@ struct GraphDev {
     const uint64_t *tptr;       // inverted index (internal ids)
     const uint32_t *post;
     const uint32_t *perm, *iperm;  // caller id -> internal id (degree-descending), and back
+    uint32_t Vh;                   // internal ids [0, Vh) have in-degree > 32 (pull: warp per node)
 };
 
 struct riki_graph {
@@ -45,10 +46,11 @@ struct riki_graph {
     uint64_t *d_tptr = nullptr;
     uint32_t *d_post = nullptr;
     uint32_t *d_perm = nullptr, *d_iperm = nullptr;
+    uint32_t Vh = 0;
     std::vector<uint64_t> h_tptr;
     uint64_t graph_bytes = 0;
     Workspace *ws = nullptr;
-    bool profiling = false, debug = false;
+    bool profiling = false, debug = false, pull_on = false;
     uint32_t batch_slots = 0;
     riki_stats stats{};
 
@@ -57,7 +59,7 @@ struct riki_graph {
         g.V = V; g.E = E;
         g.row = d_row; g.col = d_col; g.act = d_act; g.desc = d_desc;
         g.irow = d_irow; g.isrc = d_isrc; g.ieid = d_ieid; g.iact = d_iact;
-        g.src = d_src; g.dst = d_dst; g.tptr = d_tptr; g.post = d_post; g.perm = d_perm; g.iperm = d_iperm;
+        g.src = d_src; g.dst = d_dst; g.tptr = d_tptr; g.post = d_post; g.perm = d_perm; g.iperm = d_iperm; g.Vh = Vh;
         return g;
     }
 };

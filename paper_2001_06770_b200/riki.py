@@ -92,6 +92,7 @@ def load():
         "riki_get_stats": (i32, [P, P]),
         "riki_reset_stats": (i32, [P]),
         "riki_set_debug": (i32, [P, i32]),
+        "riki_set_direction": (i32, [P, i32]),
         "riki_set_batch_slots": (i32, [P, u32]),
         "riki_memory_footprint": (i32, [P, P, P]),
         "riki_last_error": (C.c_char_p, []),
@@ -271,6 +272,10 @@ class Graph:
 
     def set_debug(self, on=True):
         _check(self.lib.riki_set_debug(self.h, int(on)))
+
+    def set_direction(self, mode):
+        """0 = push (default), 1 = direction-optimising (pull for dense frontiers)."""
+        _check(self.lib.riki_set_direction(self.h, mode))
 
     def set_batch_slots(self, n):
         _check(self.lib.riki_set_batch_slots(self.h, n))

@@ -264,3 +264,35 @@ def test_device_batch_api(P):
     ref = g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)
     for a, b in zip(got, ref):
         _cmp_results(a, b)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_direction_optimising_matches_push_and_oracle(P, seed):
+    # hub-heavy graph: in-degree > 32 hubs exercise the warp-per-node pull path, dense
+    # frontiers the thread-per-node path; push-only must agree bit for bit
+    rng = np.random.default_rng(8100 + seed)
+    V = 3000
+    m = 9000
+    hubs = rng.integers(0, V, 12)
+    u = rng.integers(0, V, m)
+    v = np.where(rng.random(m) < 0.4, hubs[rng.integers(0, 12, m)], rng.integers(0, V, m))
+    v = np.where(u == v, (v + 1) % V, v)
+    src = np.empty(2 * m, np.uint32); dst = np.empty(2 * m, np.uint32)
+    src[0::2], dst[0::2] = u, v
+    src[1::2], dst[1::2] = v, u
+    act = rng.integers(0, 5, 2 * m).astype(np.uint8)
+    post = [np.unique(rng.integers(0, V, int(rng.integers(1, 30)))).astype(np.uint32) for _ in range(8)]
+    g = _dev_graph(P, V, src, dst, act, post)
+    og = O.Graph(V, src, dst, act)
+    for mode in (0, 1, 2):
+        terms = np.arange(4, dtype=np.uint32)
+        ref = O.phase(og, [post[t] for t in terms], 20, mode)
+        for direction in (1, 0):
+            g.set_direction(direction)
+            H, blk, rel, L = g.hitting_levels(terms, 20, mode)
+            assert (H == ref[0]).all() and (blk == ref[1]).all() and L == ref[2] and rel == ref[3]
+    C, M = [0, 1], [2, 3]
+    ro = _oracle_run(og, lambda t: post[t], C, M, 5, 20)
+    for direction in (0, 1):
+        g.set_direction(direction)
+        _cmp_results(g.search(C, M, 5, 20), ro)
