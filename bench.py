@@ -177,6 +177,7 @@ def main():
 
     import paper_2001_06770_b200 as P
     import synth
+    from paper_2001_06770_b200.dist import max_over_ranks
 
     rank, world, dist = _dist()
     dev = torch.cuda.current_device()
@@ -227,10 +228,7 @@ def main():
     st = g.stats()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = sum(step_ms)
-    if dist:
-        t = torch.tensor([tot_ms], device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms = float(t.item())
+    tot_ms = max_over_ranks(tot_ms, device=f"cuda:{dev}")  # time = slowest rank (weak scaling)
     value = nq * world * args.steps / (tot_ms / 1000.0)
     res = g.fetch(nq, [len(c) for c in qs.central], [len(m) for m in qs.marginal])
     relax = sum(r.stats["relax_central"] + r.stats["relax_marginal"] for r in res)
@@ -257,10 +255,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
-    if dist:
-        t = torch.tensor([e2e_ms], device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(e2e_ms, device=f"cuda:{dev}")
     e2e_value = nq * world * args.steps / (e2e_ms / 1000.0)
 
     # ---------------- single-query latency (one query in flight, host API incl. D2H)

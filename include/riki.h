@@ -171,6 +171,23 @@ uint32_t riki_results_ncand(const riki_results *r);
 riki_status riki_results_cand(const riki_results *r, uint32_t i, uint32_t *v, uint32_t *sc);
 void riki_results_free(riki_results *r);
 
+/* Bulk export of n result sets (e.g. a batch) into flat caller buffers, avoiding one call
+ * per RPG.  riki_results_export_sizes gives the totals; riki_results_export then fills
+ *   rpg_count[n]        RPGs per result set
+ *   hdr[8 * n_rpg]      per RPG: central_node, sc, sm, ptc, n_nodes, n_edges, n_vc, 0
+ *   score[n_rpg]        S^r
+ *   nodes[n_nodes], edges[n_edges], vc[n_vc]   concatenated sorted lists, in RPG order
+ *   cdist[8 * n_rpg], mdist[8 * n_rpg]         distances (RIKI_MAX_TERMS slots per RPG)
+ *   stats[n]            per-query statistics (may be NULL)
+ * All buffers are host memory owned by the caller. */
+typedef struct {
+    uint64_t n_rpg, n_nodes, n_edges, n_vc;
+} riki_export_sizes;
+riki_status riki_results_export_sizes(riki_results *const *rs, uint32_t n, riki_export_sizes *out);
+riki_status riki_results_export(riki_results *const *rs, uint32_t n, uint32_t *rpg_count, uint32_t *hdr, double *score,
+                                uint32_t *nodes, uint64_t *edges, uint32_t *vc, uint8_t *cdist, uint8_t *mdist,
+                                riki_query_stats *stats);
+
 /* ---------------------------------------------------------------------------------------
  * Debug / parity boundary (minimum slice): one exploration run with no termination other
  * than depth or an empty frontier.  terms[n_terms] term ids (1..8); block_mode 0 = none,

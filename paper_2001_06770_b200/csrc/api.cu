@@ -225,6 +225,50 @@ riki_status riki_results_cand(const riki_results *r, uint32_t i, uint32_t *v, ui
 }
 void riki_results_free(riki_results *r) { delete r; }
 
+riki_status riki_results_export_sizes(riki_results *const *rs, uint32_t n, riki_export_sizes *out) {
+    return guard([&] {
+        need(out && (n == 0 || rs), "null argument");
+        riki_export_sizes z{0, 0, 0, 0};
+        for (uint32_t i = 0; i < n; i++) {
+            need(rs[i] != nullptr, "null result handle");
+            for (const HostRPG &p : rs[i]->rpgs) {
+                z.n_rpg++;
+                z.n_nodes += p.nodes.size();
+                z.n_edges += p.edges.size();
+                z.n_vc += p.vc.size();
+            }
+        }
+        *out = z;
+    });
+}
+
+riki_status riki_results_export(riki_results *const *rs, uint32_t n, uint32_t *rpg_count, uint32_t *hdr, double *score,
+                                uint32_t *nodes, uint64_t *edges, uint32_t *vc, uint8_t *cdist, uint8_t *mdist,
+                                riki_query_stats *stats) {
+    return guard([&] {
+        need(n == 0 || (rs && rpg_count && hdr && score && cdist && mdist), "null argument");
+        uint64_t r = 0, on = 0, oe = 0, ov = 0;
+        for (uint32_t i = 0; i < n; i++) {
+            need(rs[i] != nullptr, "null result handle");
+            rpg_count[i] = (uint32_t)rs[i]->rpgs.size();
+            if (stats) stats[i] = rs[i]->stats;
+            for (const HostRPG &p : rs[i]->rpgs) {
+                uint32_t *h = hdr + 8 * r;
+                h[0] = p.central_node; h[1] = p.sc; h[2] = p.sm; h[3] = p.ptc;
+                h[4] = (uint32_t)p.nodes.size(); h[5] = (uint32_t)p.edges.size(); h[6] = (uint32_t)p.vc.size(); h[7] = 0;
+                score[r] = p.score;
+                memcpy(cdist + 8 * r, p.cdist, RIKI_MAX_TERMS);
+                memcpy(mdist + 8 * r, p.mdist, RIKI_MAX_TERMS);
+                if (nodes && !p.nodes.empty()) memcpy(nodes + on, p.nodes.data(), p.nodes.size() * 4);
+                if (edges && !p.edges.empty()) memcpy(edges + oe, p.edges.data(), p.edges.size() * 8);
+                if (vc && !p.vc.empty()) memcpy(vc + ov, p.vc.data(), p.vc.size() * 4);
+                on += p.nodes.size(); oe += p.edges.size(); ov += p.vc.size();
+                r++;
+            }
+        }
+    });
+}
+
 riki_status riki_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t n_terms, uint32_t depth, int block_mode,
                                 uint8_t *H_out, uint8_t *block_out, uint64_t *relax_out, int32_t *L_end_out) {
     return guard([&] {

@@ -1,0 +1,48 @@
+"""Multi-GPU plumbing for the RIKI hot path.
+
+RPQ queries are independent units, so the path shards by query: the graph is replicated on
+every GPU (one process per GPU, torch.distributed), each rank runs its contiguous shard of
+the batch through libriki.so, and the only collective is the gather of the (small) result
+sets, plus the max-over-ranks timing reduction of the benchmark.  No collective touches the
+data path.  Everything here is host logic, covered by world_size-2 gloo tests on CPU."""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Balanced contiguous shard [lo, hi) of n queries for `rank` of `world`."""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def search_sharded(search_fn, centrals, marginals, k, depth, group=None, **kw):
+    """Run search_fn(centrals_shard, marginals_shard, k, depth, **kw) on this rank's shard and
+    all-gather the per-query results (pickled, via the process group); every rank returns the
+    full list in the original query order."""
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    lo, hi = shard(len(centrals), rank, world)
+    local = search_fn(centrals[lo:hi], marginals[lo:hi], k, depth, **kw) if hi > lo else []
+    parts = [None] * world
+    dist.all_gather_object(parts, local, group=group)
+    return [r for p in parts for r in p]
+
+
+def max_over_ranks(x: float, group=None, device=None) -> float:
+    """Max of a host float over the ranks (NCCL needs a CUDA tensor, gloo a CPU one)."""
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, group=None, device=None) -> float:
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return float(t.item())

@@ -46,6 +46,10 @@ class QueryStats(C.Structure):
                 ("relax_marginal", C.c_uint64)]
 
 
+class ExportSizes(C.Structure):
+    _fields_ = [("n_rpg", C.c_uint64), ("n_nodes", C.c_uint64), ("n_edges", C.c_uint64), ("n_vc", C.c_uint64)]
+
+
 class Stats(C.Structure):
     _fields_ = [("expand_launches", C.c_uint64), ("expand_ms", C.c_double), ("expand_bytes", C.c_uint64),
                 ("relaxations", C.c_uint64), ("kernel_launches", C.c_uint64), ("queries", C.c_uint64),
@@ -87,6 +91,8 @@ def load():
         "riki_results_ncand": (u32, [P]),
         "riki_results_cand": (i32, [P, u32, P, P]),
         "riki_results_free": (None, [P]),
+        "riki_results_export_sizes": (i32, [P, u32, P]),
+        "riki_results_export": (i32, [P, u32, P, P, P, P, P, P, P, P, P]),
         "riki_hitting_levels": (i32, [P, P, u32, u32, i32, P, P, P, P]),
         "riki_set_profiling": (i32, [P, i32]),
         "riki_get_stats": (i32, [P, P]),
@@ -165,6 +171,41 @@ def _take_results(lib, h, nc, nm) -> Result:
         lib.riki_results_free(h)
 
 
+def _take_batch(lib, hs, n, ncs, nms) -> list:
+    """Bulk export of n result handles (one C call), then free them."""
+    try:
+        z = ExportSizes()
+        _check(lib.riki_results_export_sizes(C.cast(hs, C.c_void_p), n, C.byref(z)))
+        cnt = np.zeros(n, np.uint32)
+        hdr = np.zeros((max(z.n_rpg, 1), 8), np.uint32)
+        score = np.zeros(max(z.n_rpg, 1), np.float64)
+        nodes = np.zeros(max(z.n_nodes, 1), np.uint32)
+        edges = np.zeros(max(z.n_edges, 1), np.uint64)
+        vc = np.zeros(max(z.n_vc, 1), np.uint32)
+        cd = np.zeros((max(z.n_rpg, 1), 8), np.uint8)
+        md = np.zeros((max(z.n_rpg, 1), 8), np.uint8)
+        stats = (QueryStats * max(n, 1))()
+        _check(lib.riki_results_export(C.cast(hs, C.c_void_p), n, _p(cnt), _p(hdr), _p(score), _p(nodes), _p(edges),
+                                       _p(vc), _p(cd), _p(md), C.cast(stats, C.c_void_p)))
+        out = []
+        r = on = oe = ov = 0
+        names = [f for f, _ in QueryStats._fields_]
+        for i in range(n):
+            rp = []
+            for _ in range(int(cnt[i])):
+                h = hdr[r]
+                a, b, c = int(h[4]), int(h[5]), int(h[6])
+                rp.append(RPG(int(h[0]), int(h[1]), int(h[2]), float(score[r]), int(h[3]), nodes[on:on + a],
+                              edges[oe:oe + b], vc[ov:ov + c], cd[r, :ncs[i]], md[r, :nms[i]]))
+                on += a; oe += b; ov += c; r += 1
+            st = stats[i]
+            out.append(Result(rp, {f: getattr(st, f) for f in names}))
+        return out
+    finally:
+        for i in range(n):
+            lib.riki_results_free(C.c_void_p(hs[i]))
+
+
 class Graph:
     """Device-resident knowledge graph (riki_load_graph).  Arrays are host numpy arrays."""
 
@@ -180,6 +221,7 @@ class Graph:
         _check(self.lib.riki_load_graph(device, int(n_nodes), len(src), _p(src), _p(dst), _p(cls),
                                         len(tp) - 1, _p(tp), _p(po), C.byref(h)))
         self.h = h
+        self._debug = False
         self.V = int(n_nodes)
         self.E = len(src)
 
@@ -252,7 +294,10 @@ class Graph:
         prm = params(**kw)
         _check(self.lib.riki_rpq_search_batch(self.h, n, _p(cp), _p(ct), _p(mp), _p(mt), k, depth, C.byref(prm),
                                               C.cast(hs, C.c_void_p)))
-        return [_take_results(self.lib, C.c_void_p(hs[i]), len(centrals[i]), len(marginals[i])) for i in range(n)]
+        if self._debug:  # candidate lists are only exposed per handle
+            return [_take_results(self.lib, C.c_void_p(hs[i]), len(centrals[i]), len(marginals[i]))
+                    for i in range(n)]
+        return _take_batch(self.lib, hs, n, [len(c) for c in centrals], [len(m) for m in marginals])
 
     def search_batch_device(self, n, d_cptr, d_cterms, d_mptr, d_mterms, k, depth, **kw):
         """Device pointers (ints, e.g. torch tensor .data_ptr()); results stay on the device."""
@@ -264,7 +309,7 @@ class Graph:
     def fetch(self, n, ncs, nms) -> list:
         hs = (C.c_void_p * max(n, 1))()
         _check(self.lib.riki_batch_fetch(self.h, n, C.cast(hs, C.c_void_p)))
-        return [_take_results(self.lib, C.c_void_p(hs[i]), ncs[i], nms[i]) for i in range(n)]
+        return _take_batch(self.lib, hs, n, ncs, nms)
 
     # -- instrumentation
     def set_profiling(self, on=True):
@@ -272,6 +317,7 @@ class Graph:
 
     def set_debug(self, on=True):
         _check(self.lib.riki_set_debug(self.h, int(on)))
+        self._debug = bool(on)
 
     def set_direction(self, mode):
         """0 = push (default), 1 = direction-optimising (pull for dense frontiers)."""

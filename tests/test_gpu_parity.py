@@ -296,3 +296,21 @@ def test_direction_optimising_matches_push_and_oracle(P, seed):
     for direction in (0, 1):
         g.set_direction(direction)
         _cmp_results(g.search(C, M, 5, 20), ro)
+
+
+@pytest.mark.slow
+def test_search_c3_dbpedia_shaped_sampled(P):
+    # config 3: 5M nodes / 20M directed edges, 3 central + 3 marginal, k = 20; a 200-query
+    # slice of the 1k-query batch runs as one device batch; 4 queries compared exactly
+    kg = synth.make_kg(3)
+    qs = synth.config_queries(kg, 3, 200)
+    g = P.Graph(kg.n_nodes, kg.src, kg.dst, kg.label_class, kg.term_ptr, kg.postings)
+    g.set_label_weights(0.5, kg.avg_hops)
+    a = O.coarsen_all(O.fine_weights(kg.n_nodes, kg.src, kg.dst, kg.label_class), 0.5, kg.avg_hops)
+    assert (g.activation_levels() == a).all()
+    og = O.Graph(kg.n_nodes, kg.src, kg.dst, a)
+    res = g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)
+    for i in (0, 61, 122, 183):
+        ro = _oracle_run(og, kg.posting, qs.central[i], qs.marginal[i], qs.k, qs.depth, want_matrices=False)
+        _cmp_results(res[i], ro)
+        assert res[i].stats["relax_central"] == ro.relax_c and res[i].stats["relax_marginal"] == ro.relax_m
