@@ -13,6 +13,7 @@ bounded sample of the same workload on the host cores.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -209,6 +210,8 @@ def main():
     for _ in range(args.warmup):
         step_device()
     torch.cuda.synchronize()
+    gc.collect()   # no Python GC pauses inside timed regions
+    gc.disable()
     # ---------------- timed region (device-resident inputs and results)
     g.reset_stats()
     g.set_profiling(True)
@@ -259,6 +262,10 @@ def main():
     e2e_value = nq * world * args.steps / (e2e_ms / 1000.0)
 
     # ---------------- single-query latency (one query in flight, host API incl. D2H)
+    del rr
+    gc.collect()
+    for i in range(3):  # warm the single-slot path
+        g.search(qs.central[i], qs.marginal[i], qs.k, qs.depth)
     lat = []
     for i in range(min(args.latency_queries, nq)):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -268,6 +275,7 @@ def main():
         torch.cuda.synchronize()
         lat.append(a.elapsed_time(b))
     lat.sort()
+    gc.enable()
 
     if rank != 0:
         if dist:
@@ -293,6 +301,7 @@ def main():
                        "p99": lat[min(len(lat) - 1, int(0.99 * len(lat)))] if lat else None, "n": len(lat)},
         "gteps": relax / (tot_ms / args.steps / 1000.0) / 1e9,
         "relaxations_per_step": relax, "rpgs_per_step": n_rpg,
+        "step_ms": [round(x, 3) for x in step_ms],
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu:

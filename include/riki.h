@@ -214,6 +214,8 @@ typedef struct {
     double section_ms[4];          /* host wall time: central run, CG recovery, marginal run, finalize
                                       (exact only with profiling on, which syncs at section ends) */
     uint64_t levels;               /* lock-step level iterations (one host sync each)       */
+    uint64_t retries;              /* batches re-run after a workspace capacity overflow    */
+    uint64_t reallocs;             /* workspace (re)allocations                             */
 } riki_stats;
 riki_status riki_set_profiling(riki_graph *g, int on);
 riki_status riki_get_stats(const riki_graph *g, riki_stats *out);

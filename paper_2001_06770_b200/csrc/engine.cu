@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <chrono>
 #include <functional>
@@ -1532,6 +1533,7 @@ __global__ void k_pack_H(GraphDev g, WsDev w, uint32_t T, uint8_t *Hout, uint8_t
 // ====================================================================== host side
 struct Workspace {
     uint32_t track_reached = 0;
+    uint32_t cur = 0;  // slots used by the current batch (<= slots)
     uint32_t slots = 0, V = 0, W = 0, capc = 0, kmax = 0, heavy_cap = 0, ovf_cap = 0, big_ctas = 0;
     uint64_t arena_cap = 0, out_cap = 0, big_words = 0;
     uint8_t *H[2] = {nullptr, nullptr};
@@ -1590,7 +1592,7 @@ struct Workspace {
     }
     WsDev dev() const {
         WsDev d;
-        d.st = st; d.nslots = slots; d.V = V; d.W = W; d.capc = capc; d.kmax = kmax;
+        d.st = st; d.nslots = cur ? cur : slots; d.V = V; d.W = W; d.capc = capc; d.kmax = kmax;
         d.H[0] = H[0]; d.H[1] = H[1]; d.rb[0] = last_rb[0]; d.rb[1] = last_rb[1];
         d.q = q; d.bm = bm; d.ck = ck; d.cd = cd; d.rk = rk; d.offs = offs; d.coffs = coffs; d.pslots = pslots; d.track_reached = track_reached;
         d.heavy = heavy; d.heavy_cap = heavy_cap; d.ctr = ctr; d.prof = prof;
@@ -1604,6 +1606,25 @@ struct Workspace {
 
 namespace {
 
+struct Tracer {  // RIKI_TRACE=<ms>: print the stage times of calls slower than <ms>
+    double thr = getenv("RIKI_TRACE") ? atof(getenv("RIKI_TRACE")) : -1;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now(), t = t0;
+    std::string log;
+    void operator()(const char *what) {
+        if (thr < 0) return;
+        auto n = std::chrono::steady_clock::now();
+        char b[96];
+        snprintf(b, sizeof b, " %s=%.3f", what, std::chrono::duration<double, std::milli>(n - t).count());
+        log += b;
+        t = n;
+    }
+    ~Tracer() {
+        if (thr < 0) return;
+        double tot = std::chrono::duration<double, std::milli>(t - t0).count();
+        if (tot >= thr) fprintf(stderr, "[riki] %.3f ms:%s\n", tot, log.c_str());
+    }
+};
+
 struct Caps {
     uint32_t slots, capc, kmax;
     uint64_t arena, out;
@@ -1615,6 +1636,7 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
         ws->arena_cap >= c.arena && ws->out_cap >= c.out)
         return;
     if (ws) { ws->release(); delete ws; g->ws = nullptr; }
+    g->stats.reallocs++;
     ws = new Workspace();
     g->ws = ws;
     const uint32_t V = g->V;
@@ -1704,11 +1726,11 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
     cudaStream_t s = L.s;
     ws->track_reached = L.g->pull_on ? 1 : 0;
     WsDev wd = ws->dev();
-    k_phase_begin<<<(ws->slots + 127) / 128, 128, 0, s>>>(wd, ph, hitting_mode);
+    k_phase_begin<<<(wd.nslots + 127) / 128, 128, 0, s>>>(wd, ph, hitting_mode);
     L.check();
-    k_fill_H<RowT><<<dim3(grid_of(ws->V, 256, 64), ws->slots), 256, 0, s>>>(wd, ph);
+    k_fill_H<RowT><<<dim3(grid_of(ws->V, 256, 64), wd.nslots), 256, 0, s>>>(wd, ph);
     L.check();
-    k_seed<RowT><<<dim3(16, ws->slots), 256, 0, s>>>(gd, wd, ph);
+    k_seed<RowT><<<dim3(16, wd.nslots), 256, 0, s>>>(gd, wd, ph);
     L.check();
     for (uint32_t l = 0; l <= max_levels; l++) {
         if (ph == 1) {
@@ -1724,7 +1746,7 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
                 k_extract_rpg_big<RowT><<<ws->big_ctas, 256, 0, s>>>(gd, wd);
                 L.check();
             }
-            k_decide_m<<<ws->slots, 256, 1024 * 16, s>>>(wd, l);
+            k_decide_m<<<wd.nslots, 256, 1024 * 16, s>>>(wd, l);
             L.check();
         }
         k_plan<<<1, MAX_SLOTS, 0, s>>>(wd, ph, l, !L.g->pull_on ? 0xFFFFFFFFu : std::max<uint32_t>(ws->V / PULL_MIN_DIV, 1));
@@ -1760,13 +1782,13 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     CUDA_TRY(cudaMemsetAsync(ws->arena_used, 0, 8, s));
     CUDA_TRY(cudaMemsetAsync(ws->out_used, 0, 8, s));
     CUDA_TRY(cudaMemsetAsync(ws->ctr, 0, C_NCTR * 4, s));
-    CUDA_TRY(cudaMemsetAsync(ws->mtab, 0xFF, (size_t)ws->slots * 16 * MAPCAP * 16, s));
+    CUDA_TRY(cudaMemsetAsync(ws->mtab, 0xFF, (size_t)wd.nslots * 16 * MAPCAP * 16, s));
     // ---- run 1: central keywords
     L.t0 = std::chrono::steady_clock::now();
     run_phase<RowC, RowC>(L, gd, ws, 0, -1, depth + 1, 0);
     L.mark(0);
     // ---- candidate CGs + recovery
-    k_cand_sort<<<ws->slots, 1024, 4096 * 8, s>>>(gd, wd);
+    k_cand_sort<<<wd.nslots, 1024, 4096 * 8, s>>>(gd, wd);
     L.check();
     k_scan_cands<<<1, MAX_SLOTS, 0, s>>>(wd);
     L.check();
@@ -1787,9 +1809,9 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     run_phase<RowM, RowC>(L, gd, ws, 1, -1, depth + 1, total_cands);
     L.mark(2);
     // ---- top-k and packing
-    k_final_select<<<ws->slots, 256, 1024 * 16, s>>>(wd);
+    k_final_select<<<wd.nslots, 256, 1024 * 16, s>>>(wd);
     L.check();
-    k_final_lists<RowC><<<dim3(ws->kmax, ws->slots), 256, SORT_SMEM * 4, s>>>(gd, wd);
+    k_final_lists<RowC><<<dim3(ws->kmax, wd.nslots), 256, SORT_SMEM * 4, s>>>(gd, wd);
     L.check();
     if (L.g->profiling) CUDA_TRY(cudaStreamSynchronize(s));
     L.mark(3);
@@ -1858,8 +1880,9 @@ uint32_t auto_slots(riki_graph *g, uint32_t nq) {
 void collect_results(riki_graph *g, Workspace *ws, uint32_t n_active, const std::vector<uint32_t> &qidx,
                      std::vector<riki_results *> *out) {
     cudaStream_t s = g->stream;
-    std::vector<SlotState> st(ws->slots);
-    std::vector<OutHdr> hdr((size_t)ws->slots * ws->kmax);
+    const uint32_t ns = ws->cur ? ws->cur : ws->slots;
+    std::vector<SlotState> st(ns);
+    std::vector<OutHdr> hdr((size_t)ns * ws->kmax);
     unsigned long long used = 0;
     CUDA_TRY(cudaMemcpyAsync(st.data(), ws->st, st.size() * sizeof(SlotState), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(hdr.data(), ws->hdr, hdr.size() * sizeof(OutHdr), cudaMemcpyDeviceToHost, s));
@@ -1869,7 +1892,7 @@ void collect_results(riki_graph *g, Workspace *ws, uint32_t n_active, const std:
     if (used) CUDA_TRY(cudaMemcpyAsync(lists.data(), ws->out, used * 4, cudaMemcpyDeviceToHost, s));
     std::vector<uint64_t> cks;
     if (g->debug) {
-        cks.resize((size_t)ws->slots * ws->capc);
+        cks.resize((size_t)ns * ws->capc);
         CUDA_TRY(cudaMemcpyAsync(cks.data(), ws->ck, cks.size() * 8, cudaMemcpyDeviceToHost, s));
     }
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -1924,13 +1947,16 @@ void run_with_retry(riki_graph *g, Launch &L, uint32_t depth, Caps &caps, uint32
         Workspace *ws = g->ws;
         upload();
         run_batch(L, g, ws, depth);
-        st_out->resize(ws->slots);
-        CUDA_TRY(cudaMemcpyAsync(st_out->data(), ws->st, ws->slots * sizeof(SlotState), cudaMemcpyDeviceToHost, L.s));
+        const uint32_t ns = ws->cur ? ws->cur : ws->slots;
+        st_out->resize(ns);
+        CUDA_TRY(cudaMemcpyAsync(st_out->data(), ws->st, ns * sizeof(SlotState), cudaMemcpyDeviceToHost, L.s));
         CUDA_TRY(cudaStreamSynchronize(L.s));
         uint32_t err = 0;
         for (uint32_t i = 0; i < n_active; i++) err |= (*st_out)[i].err;
         if (err & E_UNRESOLVED) RIKI_THROW(RIKI_EUNRESOLVED, "a query term is unresolved (empty posting) or out of range");
         if (!err) return;
+        g->stats.retries++;
+        if (getenv("RIKI_TRACE")) fprintf(stderr, "[riki] retry after overflow:%s\n", err_text(err).c_str());
         if (attempt >= 6) RIKI_THROW(RIKI_ENOMEM, "workspace overflow:" + err_text(err));
         if (err & E_CAND) caps.capc = std::min<uint32_t>(caps.capc * 4, next_pow2(g->V + 1));
         if (err & (E_ARENA | E_EXTRACT)) caps.arena *= 4;
@@ -2008,7 +2034,9 @@ void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, ui
     for (const QueryIn &q : qs) check_query_host(g, q);
     out->assign(qs.size(), nullptr);
     if (qs.empty()) return;
+    Tracer tr;
     Caps caps = initial_caps(g, (uint32_t)qs.size(), k);
+    tr("initial_caps");
     Launch L{g, stream ? stream : g->stream};
     if (stream) {
         // run on the library stream, ordered after the caller's stream
@@ -2035,8 +2063,9 @@ void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, ui
                 Workspace *ws = g->ws;
                 ws->last_rb[0] = maxc <= 4 ? 4 : 8;
                 ws->last_rb[1] = maxm <= 4 ? 4 : 8;
-                std::vector<SlotState> h(ws->slots, tmpl);
-                for (uint32_t i = 0; i < ws->slots; i++) {
+                ws->cur = n;
+                std::vector<SlotState> h(n, tmpl);
+                for (uint32_t i = 0; i < n; i++) {
                     SlotState &x = h[i];
                     if (i < n) {
                         const QueryIn &q = qs[q0 + i];
@@ -2051,9 +2080,13 @@ void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, ui
                 CUDA_TRY(cudaMemcpyAsync(ws->st, h.data(), h.size() * sizeof(SlotState), cudaMemcpyHostToDevice, L.s));
                 CUDA_TRY(cudaMemsetAsync(ws->prof, 0, P_NPROF * 8, L.s));
             };
+            tr("before run");
             run_with_retry(g, L, depth, caps, n, upload, &stv);
+            tr("run_with_retry");
             collect_results(g, g->ws, n, qidx, &res);
+            tr("collect_results");
             add_stats(g, g->ws, L, n);
+            tr("add_stats");
             q0 += n;
         }
     } catch (...) {
@@ -2089,7 +2122,8 @@ void engine_search_device(riki_graph *g, uint32_t nq, const uint64_t *d_cptr, co
         Workspace *ws = g->ws;
         ws->last_rb[0] = maxc <= 4 ? 4 : 8;
         ws->last_rb[1] = maxm <= 4 ? 4 : 8;
-        k_slots_from_device<<<(ws->slots + 127) / 128, 128, 0, L.s>>>(ws->st, ws->slots, 0, nq, d_cptr, d_cterms,
+        ws->cur = nq;
+        k_slots_from_device<<<(nq + 127) / 128, 128, 0, L.s>>>(ws->st, nq, 0, nq, d_cptr, d_cterms,
                                                                       d_mptr, d_mterms, tmpl, g->d_tptr, g->n_terms);
         L.check();
         CUDA_TRY(cudaMemsetAsync(ws->prof, 0, P_NPROF * 8, L.s));
@@ -2125,8 +2159,8 @@ void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uin
     ws->last_rb[1] = 4;
     SlotState x = make_template(1, depth, riki_params{0.5, 0, 0, 0, 0, 0});
     x.w = 0xFFFFFFFFu;
-    std::vector<SlotState> h(ws->slots, x);
-    for (uint32_t i = 0; i < ws->slots; i++) { h[i].active = 0; h[i].T[0] = h[i].T[1] = 0; }
+    ws->cur = 1;
+    std::vector<SlotState> h(1, x);
     h[0].active = 1;
     h[0].T[0] = T;
     for (uint32_t j = 0; j < T; j++) h[0].term[0][j] = terms[j];
