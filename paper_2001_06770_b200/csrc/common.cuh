@@ -35,6 +35,27 @@ template <> struct Row<uint32_t> {
     __device__ __forceinline__ static uint32_t load(const uint32_t *p) { return __ldcg(p); }
 };
 
+// 16-bit rows (<= 2 keywords): computed as the low half of a 32-bit SIMD word (upper bytes 0);
+// the atomic goes through the containing aligned 32-bit word with the other half kept by 0xFFFF.
+template <> struct Row<uint16_t> {
+    static constexpr int BYTES = 2;
+    __device__ __forceinline__ static uint16_t splat(uint32_t b) { return (uint16_t)(b * 0x0101u); }
+    __device__ __forceinline__ static uint16_t eq(uint32_t x, uint32_t y) { return (uint16_t)__vcmpeq4(x, y); }
+    __device__ __forceinline__ static uint16_t lt(uint32_t x, uint32_t y) { return (uint16_t)__vcmpltu4(x, y); }
+    __device__ __forceinline__ static uint16_t le(uint32_t x, uint32_t y) { return (uint16_t)__vcmpleu4(x, y); }
+    __device__ __forceinline__ static uint32_t maxb(uint32_t x) { return max(x & 0xFFu, (x >> 8) & 0xFFu); }
+    __device__ __forceinline__ static int ones(uint32_t m) { return __popc(m & 0xFFFFu) >> 3; }
+    __device__ __forceinline__ static uint32_t byte(uint32_t x, int j) { return (x >> (8 * j)) & 0xFF; }
+    __device__ __forceinline__ static uint16_t atomic_and(uint16_t *p, uint32_t m) {
+        uintptr_t a = (uintptr_t)p;
+        uint32_t sh = (uint32_t)(a & 2) * 8;
+        uint32_t m32 = ((m & 0xFFFFu) << sh) | (0xFFFFu << (16 - sh));
+        uint32_t old = atomicAnd((uint32_t *)(a & ~(uintptr_t)3), m32);
+        return (uint16_t)(old >> sh);
+    }
+    __device__ __forceinline__ static uint16_t load(const uint16_t *p) { return __ldcg((const unsigned short *)p); }
+};
+
 template <> struct Row<uint64_t> {
     static constexpr int BYTES = 8;
     __device__ __forceinline__ static uint64_t pack(uint32_t lo, uint32_t hi) { return (uint64_t)hi << 32 | lo; }

@@ -114,6 +114,7 @@ template <class RowT> __device__ __forceinline__ RowT used_mask(uint32_t T) {
 }
 template <class RowT> __device__ __forceinline__ RowT vmin(RowT a, RowT b);
 template <> __device__ __forceinline__ uint32_t vmin<uint32_t>(uint32_t a, uint32_t b) { return __vminu4(a, b); }
+template <> __device__ __forceinline__ uint16_t vmin<uint16_t>(uint16_t a, uint16_t b) { return (uint16_t)__vminu4(a, b); }
 template <> __device__ __forceinline__ uint64_t vmin<uint64_t>(uint64_t a, uint64_t b) {
     return (uint64_t)__vminu4((uint32_t)(a >> 32), (uint32_t)(b >> 32)) << 32 |
            __vminu4((uint32_t)a, (uint32_t)b);
@@ -613,7 +614,7 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_pull(Gr
                         if (!(blocking && le == (RowT)~(RowT)0)) q = le & inf;
                     }
                     p_edges += (a <= l);
-                    if (sizeof(RowT) == 8) {
+                    if constexpr (sizeof(RowT) == 8) {
                         found |= (RowT)__reduce_or_sync(FULLMASK, (uint32_t)q) |
                                  ((RowT)__reduce_or_sync(FULLMASK, (uint32_t)((uint64_t)q >> 32)) << 32);
                     } else {
@@ -1679,13 +1680,15 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     static bool attr_done = false;
     if (!attr_done) {
 #define SET_EX_ATTR(K) CUDA_TRY(cudaFuncSetAttribute(K<uint32_t, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ex<1>())); \
-        CUDA_TRY(cudaFuncSetAttribute(K<uint64_t, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ex<1>()));
+        CUDA_TRY(cudaFuncSetAttribute(K<uint64_t, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ex<1>())); \
+        CUDA_TRY(cudaFuncSetAttribute(K<uint16_t, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ex<1>()));
         SET_EX_ATTR(k_extract_cg)
         SET_EX_ATTR(k_extract_rpg)
 #undef SET_EX_ATTR
         CUDA_TRY(cudaFuncSetAttribute(k_decide_m, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
         CUDA_TRY(cudaFuncSetAttribute(k_final_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
         CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
+        CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
         CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
         attr_done = true;
     }
@@ -1817,12 +1820,29 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     L.mark(3);
 }
 
+template <class RowC>
+void run_batch_c(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
+    switch (ws->last_rb[1]) {
+        case 2: run_batch_t<RowC, uint16_t>(L, g, ws, depth); break;
+        case 4: run_batch_t<RowC, uint32_t>(L, g, ws, depth); break;
+        default: run_batch_t<RowC, uint64_t>(L, g, ws, depth); break;
+    }
+}
 void run_batch(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
-    int a = ws->last_rb[0], b = ws->last_rb[1];
-    if (a == 4 && b == 4) run_batch_t<uint32_t, uint32_t>(L, g, ws, depth);
-    else if (a == 4) run_batch_t<uint32_t, uint64_t>(L, g, ws, depth);
-    else if (b == 4) run_batch_t<uint64_t, uint32_t>(L, g, ws, depth);
-    else run_batch_t<uint64_t, uint64_t>(L, g, ws, depth);
+    switch (ws->last_rb[0]) {
+        case 2: run_batch_c<uint16_t>(L, g, ws, depth); break;
+        case 4: run_batch_c<uint32_t>(L, g, ws, depth); break;
+        default: run_batch_c<uint64_t>(L, g, ws, depth); break;
+    }
+}
+
+// bytes per H row for T keywords: 2 (T <= 2), 4 (T <= 4) or 8
+int row_bytes(uint32_t T) {
+#ifdef RIKI_NO_U16
+    return T <= 4 ? 4 : 8;
+#else
+    return T <= 2 ? 2 : (T <= 4 ? 4 : 8);
+#endif
 }
 
 __global__ void k_slots_from_device(SlotState *st, uint32_t nslots, uint32_t q0, uint32_t nq, const uint64_t *cptr,
@@ -2061,8 +2081,8 @@ void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, ui
             std::vector<SlotState> stv;
             auto upload = [&]() {
                 Workspace *ws = g->ws;
-                ws->last_rb[0] = maxc <= 4 ? 4 : 8;
-                ws->last_rb[1] = maxm <= 4 ? 4 : 8;
+                ws->last_rb[0] = row_bytes(maxc);
+                ws->last_rb[1] = row_bytes(maxm);
                 ws->cur = n;
                 std::vector<SlotState> h(n, tmpl);
                 for (uint32_t i = 0; i < n; i++) {
@@ -2120,8 +2140,8 @@ void engine_search_device(riki_graph *g, uint32_t nq, const uint64_t *d_cptr, co
     std::vector<SlotState> stv;
     auto upload = [&]() {
         Workspace *ws = g->ws;
-        ws->last_rb[0] = maxc <= 4 ? 4 : 8;
-        ws->last_rb[1] = maxm <= 4 ? 4 : 8;
+        ws->last_rb[0] = row_bytes(maxc);
+        ws->last_rb[1] = row_bytes(maxm);
         ws->cur = nq;
         k_slots_from_device<<<(nq + 127) / 128, 128, 0, L.s>>>(ws->st, nq, 0, nq, d_cptr, d_cterms,
                                                                       d_mptr, d_mterms, tmpl, g->d_tptr, g->n_terms);
@@ -2155,7 +2175,7 @@ void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uin
     Caps caps = initial_caps(g, 1, 1);
     ensure_workspace(g, caps);
     Workspace *ws = g->ws;
-    ws->last_rb[0] = T <= 4 ? 4 : 8;
+    ws->last_rb[0] = row_bytes(T);
     ws->last_rb[1] = 4;
     SlotState x = make_template(1, depth, riki_params{0.5, 0, 0, 0, 0, 0});
     x.w = 0xFFFFFFFFu;
@@ -2175,7 +2195,10 @@ void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uin
     int blocking = block_mode == 1 || (block_mode == 2 && T >= 2);
     try {
         WsDev wd = ws->dev();
-        if (T <= 4) {
+        if (ws->last_rb[0] == 2) {
+            run_phase<uint16_t, uint16_t>(L, gd, ws, 0, block_mode, depth + 1, 0);
+            k_pack_H<uint16_t><<<grid_of(g->V, 256), 256, 0, L.s>>>(gd, wd, T, dH, dB, blocking);
+        } else if (T <= 4) {
             run_phase<uint32_t, uint32_t>(L, gd, ws, 0, block_mode, depth + 1, 0);
             k_pack_H<uint32_t><<<grid_of(g->V, 256), 256, 0, L.s>>>(gd, wd, T, dH, dB, blocking);
         } else {
