@@ -282,6 +282,16 @@ def main():
             dist.destroy_process_group()
         return
     peak, peak_src = _peaks()
+    traffic, traffic_src = None, None
+    try:  # DRAM bytes of the expansion launches from the committed ncu capture (profiles/)
+        import glob
+        tf = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_expand_traffic.json")))[-1]
+        tj = json.load(open(tf))
+        traffic = tj["dram_bytes_per_launch"]
+        traffic_src = f"{os.path.relpath(tf, ROOT)}: {tj['dram_bytes_step'] / 1e9:.2f} GB DRAM vs " \
+                      f"{(tj['algorithmic_bytes_step'] or 0) / 1e9:.2f} GB algorithmic per step"
+    except Exception:
+        pass
     achieved = (st["expand_bytes"] / 1e9) / (st["expand_ms"] / 1e3) if st["expand_ms"] > 0 else 0.0
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -291,7 +301,8 @@ def main():
                    "l2": "flushed between steps (256 MiB write)", "parallelism": f"query-sharded replicas x{world}",
                    "graph_seed": 1000 + args.config, "query_seed": 2000 + args.config},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "frac": achieved / peak if peak else None, "traffic": traffic, "traffic_source": traffic_src,
+                     "achieved_bytes_per_launch": st["expand_bytes"] / max(1, st["expand_launches"]),
                      "kernel": "k_expand + k_expand_heavy (Alg. 1 expansion), CUDA events on the library stream",
                      "sections_ms_per_step": [x / args.steps for x in st["section_ms"]], "levels_per_step": st["levels"] / args.steps,
                      "peak_source": peak_src, "expand_share_of_step": st["expand_ms"] / tot_ms if tot_ms else None},
