@@ -91,9 +91,11 @@ riki_status riki_get_activation_levels(const riki_graph *g, uint8_t *a);
  *   beam_mode  0 = keep every CG identified by the terminating level (ties, R13) [0];
  *              1 = truncate the candidate CGs to the first w by (S^c, v)
  *   tie_break  0 = (S^r, S^c, v) ascending (R23) [0]; others RIKI_ENOSYS
- *   ptc_mode   0 = filter PTC failures, RPG-wide endpoint-inclusive (R19) [0];
- *              1 = keep failures, flagged ptc = 0
- *   early_term 0 = exact bound (R21) [0]; 2 = none (exhaustive marginal run to depth)
+ *   ptc_mode   0 = filter PTC failures, RPG-wide endpoint-inclusive (R19') [0];
+ *              1 = keep failures, flagged ptc = 0; 2 = filter, PTC evaluated on G^m only;
+ *              3 = filter, SPEC's exclusive form (V_C-resident marginal nodes never qualify)
+ *   early_term 0 = exact bound (R21) [0]; 1 = the paper's literal inequality (Theorem
+ *              earlyTermination P:375-378; unsafe in general, R21); 2 = none (exhaustive)
  * ------------------------------------------------------------------------------------- */
 typedef struct {
     double gamma;

@@ -1251,23 +1251,44 @@ template <class G, class RowM> __device__ void extract_rpg(const G &G_, const Gr
     const uint32_t nn = min(sh.nu, b.hu.items_cap), ne = min(sh.nedges, b.cap_e);
     // ---- PTC: |M| = 1 trivial; else two distinct marginal keyword nodes X whose
     // every simple connection in G^r passes through V_C (endpoint-inclusive, R19').
+    // ptc_mode 2 evaluates it on G^m only (nodes and edges of the marginal recovery);
+    // ptc_mode 3 is SPEC's exclusive form (V_C-resident X never qualifies a pair).
     uint32_t pass = 1;
     if (T >= 2) {
+        const int mode = st.ptc_mode;
+        const uint32_t ncg = cd.n_edges;  // edges [0, ncg) are the CG's, [ncg, ne) G^m's
         RowM used = used_mask<RowM>(T);
         for (uint32_t i = G_.rank(); i < nn; i += G_.size()) {
             uint32_t sl = b.hu.slots[i];
-            b.flag[sl] = 0;
+            b.flag[sl] = mode == 2 ? 0 : 4;  // bit 4: node of the graph PTC is evaluated on
             b.uf[sl] = sl;
         }
         if (G_.rank() == 0) { sh.nx = 0; sh.xvc = 0; sh.mnr = EMPTY; sh.mxr = 0; }
         G_.sync();
         for (uint32_t t = G_.rank(); t < cd.n_vc; t += G_.size()) {
-            int sl = b.hu.find(w.arena[cd.vc_off + t]);
-            if (sl >= 0) b.flag[sl] = 1;
+            uint32_t v = w.arena[cd.vc_off + t];
+            int sl = b.hu.find(v);
+            if (sl < 0) continue;
+            b.flag[sl] |= 1;
+            if (mode == 2) {  // recovery sources: V_C nodes at the marginal distance
+                RowM r = R::load(H + v);
+                for (uint32_t j = 0; j < T; j++)
+                    if (R::byte(r, j) == cd.mdist[j]) b.flag[sl] |= 4;
+            }
+        }
+        G_.sync();  // byte stores above must land before the word atomics below
+        if (mode == 2) {
+            for (uint32_t i = ncg + G_.rank(); i < ne; i += G_.size()) {
+                uint32_t e = b.edges[i];
+                int sa = b.hu.find(g.src[e]), sb = b.hu.find(g.dst[e]);
+                if (sa >= 0) atomicOr((uint32_t *)&b.flag[sa & ~3] , 4u << (8 * (sa & 3)));
+                if (sb >= 0) atomicOr((uint32_t *)&b.flag[sb & ~3], 4u << (8 * (sb & 3)));
+            }
         }
         G_.sync();
         for (uint32_t i = G_.rank(); i < nn; i += G_.size()) {
             uint32_t sl = b.hu.slots[i];
+            if (!(b.flag[sl] & 4)) continue;
             if (R::eq(R::load(H + b.hu.items[i]), 0) & used) {
                 b.flag[sl] |= 2;
                 atomicAdd(&sh.nx, 1u);
@@ -1276,18 +1297,19 @@ template <class G, class RowM> __device__ void extract_rpg(const G &G_, const Gr
         }
         G_.sync();
         if (sh.nx < 2) pass = 0;
-        else if (sh.xvc) pass = 1;
+        else if (mode != 3 && sh.xvc) pass = 1;
         else {
-            for (uint32_t i = G_.rank(); i < ne; i += G_.size()) {
+            for (uint32_t i = (mode == 2 ? ncg : 0) + G_.rank(); i < ne; i += G_.size()) {
                 uint32_t e = b.edges[i];
                 int sa = b.hu.find(g.src[e]), sb = b.hu.find(g.dst[e]);
                 if (sa < 0 || sb < 0 || (b.flag[sa] & 1) || (b.flag[sb] & 1)) continue;
+                if (!(b.flag[sa] & 4) || !(b.flag[sb] & 4)) continue;
                 uf_union(b.uf, (uint32_t)sa, (uint32_t)sb);
             }
             G_.sync();
             for (uint32_t i = G_.rank(); i < nn; i += G_.size()) {
                 uint32_t sl = b.hu.slots[i];
-                if ((b.flag[sl] & 3) != 2) continue;  // X outside V_C
+                if ((b.flag[sl] & 7) != 6) continue;  // X outside V_C, in the PTC graph
                 uint32_t r = uf_find(b.uf, sl);
                 atomicMin(&sh.mnr, r);
                 atomicMax(&sh.mxr, r);
@@ -1408,10 +1430,21 @@ __global__ void k_decide_m(WsDev w, uint32_t l) {
     __syncthreads();
     if (threadIdx.x == 0) {
         bool stop = l >= st.depth || st.nq[l & 1] == 0 || first == EMPTY;
-        if (!stop && st.early_term == 0 && nR >= st.k) {
+        if (!stop && st.early_term != 2 && nR >= st.k) {
             const Cand &fu = w.CD(s)[first];
-            u128 best = rkey(rpg_score(st.gamma, fu.sc, l + 1), fu.sc, fu.ext);
-            stop = w.RK(s)[st.k - 1] < best;
+            const u128 kth = w.RK(s)[st.k - 1];
+            if (st.early_term == 0) {
+                u128 best = rkey(rpg_score(st.gamma, fu.sc, l + 1), fu.sc, fu.ext);
+                stop = kth < best;
+            } else {  // paper-literal inequality (Theorem earlyTermination)
+                uint64_t ck = (uint64_t)kth;  // (S^c << 32 | v) locates the k-th RPG's candidate
+                uint32_t lo = 0, hi = st.n_extract;
+                const uint64_t *K = w.CK(s);
+                while (lo < hi) { uint32_t m = (lo + hi) >> 1; if (K[m] < ck) lo = m + 1; else hi = m; }
+                const Cand &kc = w.CD(s)[lo];
+                double rhs = rpg_score(st.gamma, fu.sc, kc.sm);  // gamma*min S^c + (1-gamma)*S^m(kth)
+                stop = kc.sr <= rhs;
+            }
         }
         st.stop_m = stop;
     }
@@ -2032,8 +2065,8 @@ static void check_common(riki_graph *g, uint32_t k, uint32_t depth, const riki_p
     if (!(p.gamma >= 0.0 && p.gamma <= 1.0)) RIKI_THROW(RIKI_EINVAL, "gamma must be in [0,1]");
     if (p.beam_mode < 0 || p.beam_mode > 1) RIKI_THROW(RIKI_EINVAL, "beam_mode must be 0 or 1");
     if (p.tie_break != 0) RIKI_THROW(RIKI_ENOSYS, "tie_break != 0 not implemented");
-    if (p.ptc_mode < 0 || p.ptc_mode > 1) RIKI_THROW(RIKI_ENOSYS, "ptc_mode must be 0 or 1 in this build");
-    if (p.early_term != 0 && p.early_term != 2) RIKI_THROW(RIKI_ENOSYS, "early_term must be 0 or 2 in this build");
+    if (p.ptc_mode < 0 || p.ptc_mode > 3) RIKI_THROW(RIKI_EINVAL, "ptc_mode must be 0..3");
+    if (p.early_term < 0 || p.early_term > 2) RIKI_THROW(RIKI_EINVAL, "early_term must be 0..2");
     if (p.beam_w && p.beam_w < k) RIKI_THROW(RIKI_EINVAL, "beam width must be >= k (P:309)");
 }
 

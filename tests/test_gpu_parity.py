@@ -140,7 +140,7 @@ def test_search_random_small(P, seed):
         C, M = tt[:nc], tt[nc:]
         k = int(rng.choice([1, 3, 5]))
         D = int(rng.choice([3, 6, 20]))
-        kw = dict(ptc_mode=int(rng.integers(0, 2)), early_term=int(rng.choice([0, 2])),
+        kw = dict(ptc_mode=int(rng.integers(0, 4)), early_term=int(rng.integers(0, 3)),
                   beam_mode=int(rng.integers(0, 2)))
         r = g.search(C, M, k, D, **kw)
         ro = _oracle_run(og, lambda t: post[t], C, M, k, D, **kw)
@@ -296,6 +296,23 @@ def test_direction_optimising_matches_push_and_oracle(P, seed):
     for direction in (0, 1):
         g.set_direction(direction)
         _cmp_results(g.search(C, M, 5, 20), ro)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_search_modes_marginal_heavy(P, seed):
+    # |M| in {2, 3}: every PTC mode and early-termination mode against the oracle
+    rng = np.random.default_rng(9100 + seed)
+    V, src, dst, act, _ = random_instance(rng, 8, 40, deg=2.5, amax=3)
+    post = [np.unique(rng.integers(0, V, int(rng.integers(1, 3)))).astype(np.uint32) for _ in range(8)]
+    g = _dev_graph(P, V, src, dst, act, post)
+    og = O.Graph(V, src, dst, act)
+    nc, nm = int(rng.integers(1, 3)), int(rng.integers(2, 4))
+    tt = rng.choice(8, nc + nm, replace=False)
+    C, M = tt[:nc], tt[nc:]
+    for ptc_mode in range(4):
+        for early_term in range(3):
+            kw = dict(ptc_mode=ptc_mode, early_term=early_term)
+            _cmp_results(g.search(C, M, 3, 20, **kw), _oracle_run(og, lambda t: post[t], C, M, 3, 20, **kw))
 
 
 @pytest.mark.slow
