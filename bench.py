@@ -169,6 +169,7 @@ def main():
     ap.add_argument("--quick", action="store_true", help="timed region only (for ncu launch lists)")
     ap.add_argument("--slots", type=int, default=0, help="queries in flight per launch (0 = whole batch)")
     ap.add_argument("--pull", action="store_true", help="enable the direction-optimising (pull) expansion")
+    ap.add_argument("--joint", type=int, default=0, help="1 = joint multi-query traversal for the batch")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -194,6 +195,7 @@ def main():
     g.set_label_weights(0.5, kg.avg_hops)
     g.set_batch_slots(args.slots or min(nq, 1024))
     g.set_direction(1 if args.pull else 0)
+    g.set_joint(bool(args.joint))
     cp, ct = P.Graph._csr(qs.central)
     mp, mt = P.Graph._csr(qs.marginal)
     d_cp, d_ct, d_mp, d_mt = [torch.from_numpy(x.view(np.int64) if x.dtype == np.uint64 else x.view(np.int32))

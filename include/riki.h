@@ -227,6 +227,11 @@ riki_status riki_set_debug(riki_graph *g, int on);
  * pull for frontiers large against the unvisited remainder, Beamer's rule; identical results,
  * faster only when most gated/unblocked nodes end up reached). */
 riki_status riki_set_direction(riki_graph *g, int mode);
+/* Joint multi-query traversal: for batches of >= 32 queries whose H rows are
+ * <= 4 bytes (<= 4 keywords per run), every frontier node and due edge is visited once per
+ * level for the whole batch, reading all queries' rows of a node with one coalesced access
+ * (node-major H).  Identical results.  on = 1 enables it (default 0). */
+riki_status riki_set_joint(riki_graph *g, int on);
 /* Batch slots (queries in flight per launch); 0 = automatic from free device memory. */
 riki_status riki_set_batch_slots(riki_graph *g, uint32_t slots);
 /* device memory footprint of the resident graph and of the search workspace (bytes) */

@@ -297,6 +297,9 @@ riki_status riki_set_direction(riki_graph *g, int mode) {
         g->pull_on = mode == 1;
     });
 }
+riki_status riki_set_joint(riki_graph *g, int on) {
+    return guard([&] { need(g, "null graph"); g->joint_on = on != 0; });
+}
 riki_status riki_set_batch_slots(riki_graph *g, uint32_t slots) {
     return guard([&] {
         need(g, "null graph");

@@ -36,7 +36,8 @@ constexpr uint32_t CHUNK = 256;
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
 constexpr uint32_t SORT_SMEM = 8192;  // u32 keys sorted in shared memory
 
-enum Ctr { C_NHEAVY = 0, C_NNEWATT, C_NOVF, C_ACTIVE, C_TOTAL, C_NCAND_TOTAL, C_NOVF2, C_NPULL, C_NCTR = 16 };
+enum Ctr { C_NHEAVY = 0, C_NNEWATT, C_NOVF, C_ACTIVE, C_TOTAL, C_NCAND_TOTAL, C_NOVF2, C_NPULL, C_JQN0, C_JQN1,
+           C_JQCUR, C_JHEAVY, C_NCTR = 16 };
 enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_PULLNODES, P_PULLEDGES, P_NPROF = 8 };
 enum Err { E_CAND = 1, E_HEAVY = 2, E_ARENA = 4, E_EXTRACT = 8, E_OUT = 16, E_UNRESOLVED = 32 };
 
@@ -71,6 +72,14 @@ struct OutHdr {
     uint8_t cdist[RIKI_MAX_TERMS], mdist[RIKI_MAX_TERMS];
 };
 
+// View of one query's H array: slot-major (row of node n at base + n) or node-major (all
+// slots' rows of node n contiguous, stride SP rows) for the joint multi-query traversal.
+template <class RowT> struct HV {
+    RowT *base;
+    uint32_t sn;
+    __device__ __forceinline__ RowT *operator+(uint32_t n) const { return base + (size_t)n * sn; }
+};
+
 // Device view of the workspace (passed by value to every kernel).
 struct WsDev {
     SlotState *st;
@@ -78,6 +87,7 @@ struct WsDev {
     uint8_t *H[2];
     uint32_t rb[2];
     uint32_t *q, *bm;
+    uint32_t *jq, *jbm;  // joint traversal: union frontier queues [2][V] and bit-packed flags [2][W]
     uint64_t *ck;
     Cand *cd;
     u128 *rk;
@@ -100,9 +110,12 @@ struct WsDev {
     unsigned long long *out_used, out_cap;
 
     __device__ __forceinline__ uint32_t *Q(uint32_t s, uint32_t b) const { return q + ((size_t)s * 2 + b) * V; }
-    __device__ __forceinline__ uint32_t *BM(uint32_t s, uint32_t b) const { return bm + ((size_t)s * 2 + b) * W; }
-    template <class RowT> __device__ __forceinline__ RowT *Hs(int ph, uint32_t s) const {
-        return (RowT *)(H[ph] + (size_t)s * V * rb[ph]);
+    __device__ __forceinline__ uint32_t *JQ(uint32_t b) const { return jq + (size_t)b * V; }
+    __device__ __forceinline__ uint32_t *JBM(uint32_t b) const { return jbm + (size_t)b * W; }
+    uint32_t hnode, SP;  // H layout: 0 slot-major, 1 node-major with SP (padded) slots per node
+    template <class RowT> __device__ __forceinline__ HV<RowT> Hs(int ph, uint32_t s) const {
+        return hnode ? HV<RowT>{(RowT *)(H[ph] + (size_t)s * rb[ph]), SP}
+                     : HV<RowT>{(RowT *)(H[ph] + (size_t)s * V * rb[ph]), 1u};
     }
     __device__ __forceinline__ uint64_t *CK(uint32_t s) const { return ck + (size_t)s * capc; }
     __device__ __forceinline__ Cand *CD(uint32_t s) const { return cd + (size_t)s * capc; }
@@ -173,8 +186,30 @@ template <class RowT> __global__ void k_fill_H(WsDev w, int ph) {
     uint32_t s = blockIdx.y;
     if (!w.st[s].in_phase) return;
     RowT pat = used_mask<RowT>(w.st[s].T[ph]);
-    RowT *H = w.Hs<RowT>(ph, s);
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < w.V; i += gridDim.x * blockDim.x) H[i] = pat;
+    const HV<RowT> H = w.Hs<RowT>(ph, s);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < w.V; i += gridDim.x * blockDim.x) *(H + i) = pat;
+}
+
+// Node-major H (joint traversal): one 16-byte chunk per thread, slot patterns from shared
+// memory; slots not in this run (or padding) get 0 (= complete and blocked: never touched).
+template <class RowT> __global__ void k_fill_H_nodemajor(WsDev w, int ph) {
+    __shared__ RowT pat[1024];
+    for (uint32_t s = threadIdx.x; s < w.SP; s += blockDim.x) {
+        RowT p = 0;
+        if (s < w.nslots && w.st[s].in_phase) p = used_mask<RowT>(w.st[s].T[ph]);
+        pat[s] = p;
+    }
+    __syncthreads();
+    const uint32_t per = 16 / sizeof(RowT), chunks = w.SP / per;
+    const uint64_t total = (uint64_t)w.V * chunks;
+    uint4 *H = (uint4 *)w.H[ph];
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t c = (uint32_t)(i % chunks);
+        RowT v[16 / sizeof(RowT)];
+#pragma unroll
+        for (uint32_t k = 0; k < per; k++) v[k] = pat[c * per + k];
+        H[i] = *(uint4 *)v;
+    }
 }
 
 // Seeds: h = 0 at keyword nodes, all keyword nodes are frontiers; level-0
@@ -183,7 +218,7 @@ template <class RowT> __global__ void k_seed(GraphDev g, WsDev w, int ph) {
     uint32_t s = blockIdx.y;
     SlotState &st = w.st[s];
     if (!st.in_phase) return;
-    RowT *H = w.Hs<RowT>(ph, s);
+    const HV<RowT> H = w.Hs<RowT>(ph, s);
     const uint32_t T = st.T[ph];
     const RowT used = used_mask<RowT>(T);
     for (uint32_t j = 0; j < T; j++) {
@@ -196,7 +231,12 @@ template <class RowT> __global__ void k_seed(GraphDev g, WsDev w, int ph) {
             RowT nw = old & andm;
             if ((Row<RowT>::eq(old, Row<RowT>::splat(0xFF)) & used) == used) {  // first seed of this node
                 uint32_t p = atomicAdd(&st.nq[0], 1u);
-                w.Q(s, 0)[p] = v;
+                if (w.hnode) {  // joint traversal: union frontier, deduplicated by the bit-packed flags
+                    uint32_t bit = 1u << (v & 31);
+                    if (!(atomicOr(w.JBM(0) + (v >> 5), bit) & bit)) w.JQ(0)[atomicAdd(&w.ctr[C_JQN0], 1u)] = v;
+                } else {
+                    w.Q(s, 0)[p] = v;
+                }
                 atomicAdd(&st.reached, 1u);
             }
             if (st.collect && Row<RowT>::eq(nw, Row<RowT>::splat(0xFF)) == 0 &&
@@ -269,6 +309,10 @@ __global__ void k_plan(WsDev w, int ph, uint32_t l, uint32_t pull_min) {
         w.ctr[C_TOTAL] = sc[MAX_SLOTS - 1];
         w.ctr[C_NHEAVY] = 0;
         w.ctr[C_NPULL] = npull;
+        // joint traversal: size of the union frontier of this level, reset the next one
+        w.ctr[C_JQCUR] = w.ctr[C_JQN0 + (l & 1)];
+        w.ctr[C_JQN0 + ((l & 1) ^ 1)] = 0;
+        w.ctr[C_JHEAVY] = 0;
     }
 }
 
@@ -284,7 +328,7 @@ template <class RowT> struct Relax {
 // byte that is still 0xFF; the old row says whether this thread is the first writer of n's row
 // at this level (enqueue) and whether it completed the row (identification at l+1, R10).
 template <class RowT>
-__device__ __forceinline__ Relax<RowT> relax(RowT *H, uint32_t n, RowT hn, RowT mask, uint32_t l) {
+__device__ __forceinline__ Relax<RowT> relax(const HV<RowT> &H, uint32_t n, RowT hn, RowT mask, uint32_t l) {
     typedef Row<RowT> R;
     Relax<RowT> r{false, false, 0};
     const RowT FF = R::splat(0xFF);
@@ -392,7 +436,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
             uint32_t info = s_info[s];
             uint32_t ent = w.Q(s, cur)[item - s_offs[s]];
             f = ent & ~RETAINED;
-            RowT *H = w.Hs<RowT>(ph, s);
+            const HV<RowT> H = w.Hs<RowT>(ph, s);
             RowT Rf = R::load(H + f);
             RowT used = used_mask<RowT>(info >> 8);
             bool dup = (ent & RETAINED) && (R::eq(Rf, L) & used);
@@ -448,7 +492,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
         {   // short ranges (<= EXP_SMALL edges): the owning lane issues all its loads at once
             const bool small = len > 0 && len <= EXP_SMALL;
             const bool collect = valid && ((s_info[s] >> 1) & 1);
-            RowT *H = w.Hs<RowT>(ph, s);
+            const HV<RowT> H = w.Hs<RowT>(ph, s);
             uint32_t nA[EXP_SMALL];
             RowT hA[EXP_SMALL];
 #pragma unroll
@@ -540,7 +584,7 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
         uint32_t s = h.x;
         const SlotState &st = w.st[s];
         RowT used = used_mask<RowT>(st.T[ph]);
-        RowT *H = w.Hs<RowT>(ph, s);
+        const HV<RowT> H = w.Hs<RowT>(ph, s);
         RowT Rf = R::load(H + h.y);  // values <= l are final; concurrent l+1 writes don't change the masks
         RowT newc = R::eq(Rf, L) & used, oldc = R::lt(Rf, L) & used;
         bool collect = st.collect;
@@ -589,7 +633,7 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_pull(Gr
     typedef Row<RowT> R;
     const uint32_t s = w.pslots[blockIdx.y];
     const SlotState &st = w.st[s];
-    RowT *H = w.Hs<RowT>(ph, s);
+    const HV<RowT> H = w.Hs<RowT>(ph, s);
     const RowT used = used_mask<RowT>(st.T[ph]);
     const RowT FF = R::splat(0xFF), L = R::splat(l);
     const bool blocking = st.blocking, collect = st.collect;
@@ -626,7 +670,7 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_pull(Gr
             bool enq = false, id = false;
             if (found && lane == 0) {
                 RowT nr = (Rn & ~found) | (found & R::splat(l + 1));
-                H[n] = nr;
+                *(H + n) = nr;
                 enq = true;
                 id = collect && R::eq(nr, FF) == 0;
                 p_cells += R::ones(found);
@@ -670,7 +714,7 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_pull(Gr
                     }
                     if (found) {
                         RowT nr = (Rn & ~found) | (found & R::splat(l + 1));
-                        H[n] = nr;
+                        *(H + n) = nr;
                         enq = true;
                         id = collect && R::eq(nr, FF) == 0;
                         p_cells += R::ones(found);
@@ -692,6 +736,233 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_pull(Gr
         atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
         atomicAdd(&w.prof[P_ENQ], (unsigned long long)p_enq);
     }
+}
+
+// ====================================================================== joint traversal
+// Joint multi-query expansion (iBFS-style sharing of the adjacency reads
+// across the queries of a batch).  H is node-major: the rows of all SP slots of node n are
+// contiguous, so a warp reads them with one 16-byte load per lane (lane c owns slots
+// [c*16/RB, (c+1)*16/RB)).  The frontier is the union over slots (bit-packed flags dedup
+// it); each frontier node and each of its due edges is visited ONCE per level for the
+// whole batch, and every slot applies exactly its own Alg. 1 rule through byte masks: new
+// columns (h == l) relax edges with a <= l, old columns (h < l) edges with a == l, CF-blocked
+// slots and slots outside the run nothing.  Relaxation, first-writer and completion logic
+// per slot is the same atomicAnd as in k_expand, on the 32-bit word holding the slot rows.
+constexpr uint32_t JHEAVY = 512, JCHUNK = 512;
+
+template <int RB> __device__ __forceinline__ uint32_t slot_bytes(int h) {
+    return RB == 4 ? 0xFFFFFFFFu : (h ? 0xFFFF0000u : 0x0000FFFFu);
+}
+template <int RB> __device__ __forceinline__ uint32_t full_slots(uint32_t m) {  // slots whose bytes are all set
+    if (RB == 4) return m == 0xFFFFFFFFu ? 0xFFFFFFFFu : 0u;
+    return ((m & 0xFFFFu) == 0xFFFFu ? 0xFFFFu : 0u) | ((m >> 16) == 0xFFFFu ? 0xFFFF0000u : 0u);
+}
+template <int RB> __device__ __forceinline__ uint32_t any_slots(uint32_t m) {  // slots with any byte set
+    if (RB == 4) return m ? 0xFFFFFFFFu : 0u;
+    return ((m & 0xFFFFu) ? 0xFFFFu : 0u) | ((m & 0xFFFF0000u) ? 0xFFFF0000u : 0u);
+}
+__device__ __forceinline__ uint32_t u4w(const uint4 &v, int i) { return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w; }
+
+// push node n to the next union frontier (bit-packed dedup); convergent
+__device__ __forceinline__ void jq_push(const WsDev &w, bool want, uint32_t n, uint32_t nxt) {
+    bool app = false;
+    if (want) {
+        uint32_t bit = 1u << (n & 31);
+        app = !(atomicOr(w.JBM(nxt) + (n >> 5), bit) & bit);
+    }
+    uint32_t pos = warp_append(app, 0, &w.ctr[C_JQN0 + nxt], 0);
+    if (app) w.JQ(nxt)[pos] = n;
+}
+
+template <class RowT, bool HEAVYP>
+__global__ void __launch_bounds__(256) k_jexpand(GraphDev g, WsDev w, int ph, uint32_t l) {
+    constexpr int RB = sizeof(RowT), SPW = 4 / RB, PER = 16 / RB;
+    __shared__ uint32_t s_cnt[256];
+    __shared__ uint32_t s_info[256];
+    __shared__ uint8_t s_ne[256];
+    const uint32_t SP = w.SP, lane = lane_id();
+    for (uint32_t i = threadIdx.x; i < SP; i += blockDim.x) {
+        s_cnt[i] = 0;
+        s_ne[i] = 0;
+        uint32_t info = 0;
+        if (i < w.nslots) {
+            const SlotState &st = w.st[i];
+            info = st.in_phase | st.blocking << 1 | st.collect << 2 | st.T[ph] << 8;
+        }
+        s_info[i] = info;
+    }
+    __syncthreads();
+    // per-lane word masks of its slots: used columns of slots in the run, blocking, collect
+    uint32_t usedw[4], blkw[4], colw[4];
+    const bool lv = lane * 16 < SP * RB;
+#pragma unroll
+    for (int wi = 0; wi < 4; wi++) {
+        usedw[wi] = blkw[wi] = colw[wi] = 0;
+#pragma unroll
+        for (int h = 0; h < SPW; h++) {
+            uint32_t sl = lane * PER + wi * SPW + h;
+            uint32_t info = lv && sl < SP ? s_info[sl] : 0;
+            if (!(info & 1)) continue;
+            uint32_t T = min(info >> 8, (uint32_t)RB);
+            uint32_t um = T >= 4 ? 0xFFFFFFFFu : ((1u << (8 * T)) - 1);
+            usedw[wi] |= um << (8 * RB * h);
+            if (info & 2) blkw[wi] |= slot_bytes<RB>(h);
+            if (info & 4) colw[wi] |= slot_bytes<RB>(h);
+        }
+    }
+    const uint32_t L = l * 0x01010101u, L1 = (l + 1) * 0x01010101u;
+    const uint32_t cur = l & 1, nxt = cur ^ 1;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t nitems = HEAVYP ? min(w.ctr[C_JHEAVY], w.heavy_cap) : w.ctr[C_JQCUR];
+    uint8_t *Hb = w.H[ph];
+    const size_t rowb = (size_t)SP * RB;
+    uint32_t p_items = 0, p_edges = 0, p_cells = 0, p_enq = 0;
+    for (uint32_t it = gw; it < nitems; it += nw) {
+        uint32_t f, lo = 0, hi = 0, eqlo = 0;
+        if (HEAVYP) {
+            uint4 hh = w.heavy[it];
+            f = hh.x; lo = hh.y; hi = hh.z; eqlo = hh.w;
+        } else {
+            f = w.JQ(cur)[it];
+            if (lane == 0) w.JBM(cur)[f >> 5] = 0;  // every flag of this word is a node of this queue
+        }
+        const uint4 Rf = lv ? __ldcg((const uint4 *)(Hb + f * rowb) + lane) : make_uint4(0, 0, 0, 0);
+        uint32_t newc[4], oldc[4];
+#pragma unroll
+        for (int wi = 0; wi < 4; wi++) {
+            uint32_t R = u4w(Rf, wi);
+            uint32_t blocked = full_slots<RB>(__vcmpleu4(R, L)) & blkw[wi];  // CF per slot (R10)
+            newc[wi] = __vcmpeq4(R, L) & usedw[wi] & ~blocked;
+            oldc[wi] = __vcmpltu4(R, L) & usedw[wi] & ~blocked;
+        }
+        const bool any_new = __any_sync(FULLMASK, (newc[0] | newc[1] | newc[2] | newc[3]) != 0);
+        const bool any_old = __any_sync(FULLMASK, (oldc[0] | oldc[1] | oldc[2] | oldc[3]) != 0);
+        if (!any_new && !any_old) continue;
+        if (!HEAVYP) {
+            p_items++;
+            const uint4 d = __ldg(g.desc + f);
+            const uint32_t rb = d.x, re = d.x + d.y;
+            if (d.y <= 8) {
+                hi = rb + ((__popc(__vcmpleu4(d.z, L)) + __popc(__vcmpleu4(d.w, L))) >> 3);
+                eqlo = rb + ((__popc(__vcmpltu4(d.z, L)) + __popc(__vcmpltu4(d.w, L))) >> 3);
+            } else {
+                if (lane == 0) {
+                    hi = upper_bound_act(g.act, rb, re, l);
+                    eqlo = lower_bound_act(g.act, rb, hi, l);
+                }
+                hi = __shfl_sync(FULLMASK, hi, 0);
+                eqlo = __shfl_sync(FULLMASK, eqlo, 0);
+            }
+            lo = any_new ? rb : eqlo;
+            // per-slot relaxation counts and retention (Alg. 1 lines 9-11)
+            bool retain_any = false;
+#pragma unroll
+            for (int wi = 0; wi < 4; wi++) {
+#pragma unroll
+                for (int h = 0; h < SPW; h++) {
+                    uint32_t sb = slot_bytes<RB>(h);
+                    uint32_t nc = newc[wi] & sb, oc = oldc[wi] & sb;
+                    if (!(nc | oc)) continue;
+                    uint32_t sl = lane * PER + wi * SPW + h;
+                    uint32_t cnt = (hi - rb) * (__popc(nc) >> 3) + (hi - eqlo) * (__popc(oc) >> 3);
+                    if (cnt) atomicAdd(&s_cnt[sl], cnt);
+                    if (hi < re) { s_ne[sl] = 1; retain_any = true; }
+                }
+            }
+            const bool ret = __any_sync(FULLMASK, retain_any);
+            jq_push(w, ret && lane == 0, f, nxt);
+            p_enq += ret && lane == 0;
+            if (hi - lo > JHEAVY) {  // hub rows: chunks for the heavy pass
+                if (lane == 0) {
+                    uint32_t nch = (hi - lo + JCHUNK - 1) / JCHUNK;
+                    uint32_t p = atomicAdd(&w.ctr[C_JHEAVY], nch);
+                    if (p + nch <= w.heavy_cap) {
+                        for (uint32_t c = 0; c < nch; c++)
+                            w.heavy[p + c] = make_uint4(f, lo + c * JCHUNK, min(lo + (c + 1) * JCHUNK, hi), eqlo);
+                    } else {
+                        atomicOr(&w.st[0].err, (uint32_t)E_HEAVY);
+                    }
+                }
+                p_edges += hi - lo;
+                continue;
+            }
+            p_edges += hi - lo;
+        }
+        // edges: 4 per iteration, all 32 lanes on each edge (lane = slot group)
+        for (uint32_t e0 = lo; e0 < hi; e0 += 4) {
+            uint32_t nn[4];
+            uint4 Rn[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) nn[u] = e0 + u < hi ? __ldg(g.col + e0 + u) : 0;
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                Rn[u] = (lv && e0 + u < hi) ? __ldcg((const uint4 *)(Hb + nn[u] * rowb) + lane) : make_uint4(0, 0, 0, 0);
+            bool firstq[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const bool isold = e0 + u >= eqlo;
+                bool lane_first = false;
+                uint32_t cmpk = 0;  // bit k: slot k of this lane completed its row (identification)
+                if (e0 + u < hi) {
+#pragma unroll
+                    for (int wi = 0; wi < 4; wi++) {
+                        uint32_t need = (newc[wi] | (isold ? oldc[wi] : 0u)) & __vcmpeq4(u4w(Rn[u], wi), 0xFFFFFFFFu);
+                        if (!need) continue;
+                        uint32_t andm = ~need | (need & L1);
+                        uint32_t *addr = (uint32_t *)(Hb + nn[u] * rowb) + lane * 4 + wi;
+                        uint32_t old = atomicAnd(addr, andm);
+                        uint32_t changed = need & __vcmpeq4(old, 0xFFFFFFFFu);
+                        if (!changed) continue;
+                        p_cells += __popc(changed) >> 3;
+                        uint32_t chs = any_slots<RB>(changed);
+                        uint32_t fst = chs & ~any_slots<RB>(__vcmpeq4(old, L1));
+                        uint32_t cmp = chs & ~any_slots<RB>(__vcmpeq4(old & andm, 0xFFFFFFFFu)) & colw[wi];
+#pragma unroll
+                        for (int h = 0; h < SPW; h++) {
+                            uint32_t sb = slot_bytes<RB>(h);
+                            if (fst & sb) { s_ne[lane * PER + wi * SPW + h] = 1; lane_first = true; }
+                            if (cmp & sb) cmpk |= 1u << (wi * SPW + h);
+                        }
+                    }
+                }
+                firstq[u] = __any_sync(FULLMASK, lane_first);
+                if (__any_sync(FULLMASK, cmpk != 0)) {
+#pragma unroll
+                    for (int k = 0; k < PER; k++) cand_push(g, w, (cmpk >> k) & 1, lane * PER + k, nn[u], l + 1);
+                }
+            }
+            // union-frontier pushes for the (up to) 4 relaxed targets: lane u pushes edge u
+            bool want = false;
+            uint32_t tn = 0;
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                if (lane == (uint32_t)u) { want = firstq[u]; tn = nn[u]; }
+            jq_push(w, want, tn, nxt);
+            p_enq += want;
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < SP && i < w.nslots; i += blockDim.x) {
+        if (s_ne[i]) w.st[i].nq[nxt] = 1;  // Phi_{l+1}(slot) is not empty
+        if (s_cnt[i]) atomicAdd(&w.st[i].relax[ph], (unsigned long long)s_cnt[i]);
+    }
+    p_items = warp_sum(p_items);
+    p_edges = warp_sum(p_edges);
+    p_cells = warp_sum(p_cells);
+    p_enq = warp_sum(p_enq);
+    if (lane == 0 && (p_items | p_edges | p_cells)) {
+        atomicAdd(&w.prof[P_ITEMS], (unsigned long long)p_items);
+        atomicAdd(&w.prof[P_EDGES], (unsigned long long)p_edges);
+        atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
+        atomicAdd(&w.prof[P_ENQ], (unsigned long long)p_enq);
+    }
+}
+
+// clear the flags of the last (unconsumed) union frontier of a run
+__global__ void k_jclear(WsDev w, uint32_t b) {
+    uint32_t n = w.ctr[C_JQN0 + b];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        w.JBM(b)[w.JQ(b)[i] >> 5] = 0;
 }
 
 // ====================================================================== candidates
@@ -841,7 +1112,7 @@ constexpr unsigned long long NOT_READY = ~0ull;
 // Map entry (16 B): {key, -, (cnt, off) as one 64-bit word}; one 16-byte load finds a
 // published list.  List entries are 3 words: (n, caller edge id, h_n).  Called by a warp.
 template <class RowT>
-__device__ void dag_list(const GraphDev &g, const WsDev &w, uint32_t s, int ph, int j, const RowT *H, bool blocking,
+__device__ void dag_list(const GraphDev &g, const WsDev &w, uint32_t s, int ph, int j, const HV<RowT> H, bool blocking,
                          uint32_t q, uint32_t hq, uint32_t *off_out, uint32_t *cnt_out) {
     typedef Row<RowT> R;
     const uint32_t lane = lane_id();
@@ -934,7 +1205,7 @@ __device__ void dag_list(const GraphDev &g, const WsDev &w, uint32_t s, int ph, 
 // is in q's DAG list; n is continued from iff h_nj != 0 (line 10) and unvisited (R17).
 // hk.items (the queue) and qh hold the sources and their levels on entry.
 template <class G, class RowT>
-__device__ void bfs_column(const G &G_, const GraphDev &g, const WsDev &w, uint32_t s, int ph, int j, const RowT *H,
+__device__ void bfs_column(const G &G_, const GraphDev &g, const WsDev &w, uint32_t s, int ph, int j, const HV<RowT> H,
                            bool blocking, const ExBuf &b, ExShared &sh) {
     const uint32_t lane = lane_id(), warp = G_.warp(), nw = G_.nwarps();
     uint32_t head = 0, tail = min(sh.nk, b.hk.items_cap);
@@ -1002,7 +1273,7 @@ template <class G, class RowC> __device__ void extract_cg(const G &G_, const Gra
     typedef Row<RowC> R;
     const SlotState &st = w.st[s];
     Cand &cd = w.CD(s)[c];
-    const RowC *H = w.Hs<RowC>(0, s);
+    const HV<RowC> H = w.Hs<RowC>(0, s);
     const uint32_t T = st.T[0];
     const uint32_t v = cd.v;
     if (G_.rank() == 0) b.hu.insert(v, &sh.ovf);
@@ -1176,7 +1447,7 @@ template <class RowM> __global__ void __launch_bounds__(256) k_attach(WsDev w) {
         if (!st.in_phase) continue;
         Cand &cd = w.CD(s)[c];
         if (cd.attached) continue;
-        const RowM *H = w.Hs<RowM>(1, s);
+        const HV<RowM> H = w.Hs<RowM>(1, s);
         RowM mn = (RowM)~(RowM)0;
         for (uint32_t t = lane; t < cd.n_vc; t += 32) mn = vmin<RowM>(mn, R::load(H + w.arena[cd.vc_off + t]));
 #pragma unroll
@@ -1219,7 +1490,7 @@ template <class G, class RowM> __device__ void extract_rpg(const G &G_, const Gr
     typedef Row<RowM> R;
     SlotState &st = w.st[s];
     Cand &cd = w.CD(s)[c];
-    const RowM *H = w.Hs<RowM>(1, s);
+    const HV<RowM> H = w.Hs<RowM>(1, s);
     const uint32_t T = st.T[1];
     const bool blocking = T >= 2;
     if (cd.n_nodes > b.hu.items_cap || cd.n_nodes * 2 > b.hu.cap || cd.n_edges > b.cap_e) {
@@ -1554,7 +1825,7 @@ template <class RowC> __global__ void __launch_bounds__(256) k_final_lists(Graph
 // ====================================================================== debug boundary
 template <class RowT>
 __global__ void k_pack_H(GraphDev g, WsDev w, uint32_t T, uint8_t *Hout, uint8_t *blk, int blocking) {
-    const RowT *H = w.Hs<RowT>(0, 0);
+    const HV<RowT> H = w.Hs<RowT>(0, 0);
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < w.V; v += gridDim.x * blockDim.x) {
         RowT r = Row<RowT>::load(H + g.perm[v]);  // output indexed by caller id
         for (uint32_t j = 0; j < T; j++) Hout[(size_t)v * T + j] = (uint8_t)Row<RowT>::byte(r, j);
@@ -1567,11 +1838,12 @@ __global__ void k_pack_H(GraphDev g, WsDev w, uint32_t T, uint8_t *Hout, uint8_t
 // ====================================================================== host side
 struct Workspace {
     uint32_t track_reached = 0;
+    uint32_t hnode = 0, SP = 0;  // H layout of the current batch
     uint32_t cur = 0;  // slots used by the current batch (<= slots)
     uint32_t slots = 0, V = 0, W = 0, capc = 0, kmax = 0, heavy_cap = 0, ovf_cap = 0, big_ctas = 0;
     uint64_t arena_cap = 0, out_cap = 0, big_words = 0;
     uint8_t *H[2] = {nullptr, nullptr};
-    uint32_t *q = nullptr, *bm = nullptr, *offs = nullptr, *coffs = nullptr, *pslots = nullptr, *ctr = nullptr, *arena = nullptr,
+    uint32_t *q = nullptr, *bm = nullptr, *jq = nullptr, *jbm = nullptr, *offs = nullptr, *coffs = nullptr, *pslots = nullptr, *ctr = nullptr, *arena = nullptr,
              *big = nullptr, *resid = nullptr, *out = nullptr;
     uint4 *mtab = nullptr;
     uint64_t *ck = nullptr;
@@ -1627,8 +1899,8 @@ struct Workspace {
     WsDev dev() const {
         WsDev d;
         d.st = st; d.nslots = cur ? cur : slots; d.V = V; d.W = W; d.capc = capc; d.kmax = kmax;
-        d.H[0] = H[0]; d.H[1] = H[1]; d.rb[0] = last_rb[0]; d.rb[1] = last_rb[1];
-        d.q = q; d.bm = bm; d.ck = ck; d.cd = cd; d.rk = rk; d.offs = offs; d.coffs = coffs; d.pslots = pslots; d.track_reached = track_reached;
+        d.H[0] = H[0]; d.H[1] = H[1]; d.hnode = hnode; d.SP = SP; d.rb[0] = last_rb[0]; d.rb[1] = last_rb[1];
+        d.q = q; d.bm = bm; d.jq = jq; d.jbm = jbm; d.ck = ck; d.cd = cd; d.rk = rk; d.offs = offs; d.coffs = coffs; d.pslots = pslots; d.track_reached = track_reached;
         d.heavy = heavy; d.heavy_cap = heavy_cap; d.ctr = ctr; d.prof = prof;
         d.arena = arena; d.arena_used = arena_used; d.arena_cap = arena_cap;
         d.newatt = newatt; d.ovf = ovf; d.ovf2 = ovf2; d.ovf_cap = ovf_cap;
@@ -1680,6 +1952,9 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     ws->H[0] = ws->alloc<uint8_t>(S * V * 8);
     ws->H[1] = ws->alloc<uint8_t>(S * V * 8);
     ws->q = ws->alloc<uint32_t>(S * 2 * V);
+    ws->jq = ws->alloc<uint32_t>(2 * (size_t)V);
+    ws->jbm = ws->alloc<uint32_t>(2 * (size_t)ws->W);
+    CUDA_TRY(cudaMemset(ws->jbm, 0, 2 * (size_t)ws->W * 4));
     ws->ck = ws->alloc<uint64_t>(S * c.capc);
     ws->cd = ws->alloc<Cand>(S * c.capc);
     ws->rk = ws->alloc<u128>(S * c.capc);
@@ -1764,8 +2039,18 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
     WsDev wd = ws->dev();
     k_phase_begin<<<(wd.nslots + 127) / 128, 128, 0, s>>>(wd, ph, hitting_mode);
     L.check();
-    k_fill_H<RowT><<<dim3(grid_of(ws->V, 256, 64), wd.nslots), 256, 0, s>>>(wd, ph);
-    L.check();
+    bool joint = false;
+    if constexpr (sizeof(RowT) <= 4) joint = wd.hnode != 0;
+    if (joint) {
+        if constexpr (sizeof(RowT) <= 4) {
+            k_fill_H_nodemajor<RowT><<<148 * 16, 256, 0, s>>>(wd, ph);
+            L.check();
+        }
+        CUDA_TRY(cudaMemsetAsync(ws->ctr + C_JQN0, 0, 8, s));
+    } else {
+        k_fill_H<RowT><<<dim3(grid_of(ws->V, 256, 64), wd.nslots), 256, 0, s>>>(wd, ph);
+        L.check();
+    }
     k_seed<RowT><<<dim3(16, wd.nslots), 256, 0, s>>>(gd, wd, ph);
     L.check();
     for (uint32_t l = 0; l <= max_levels; l++) {
@@ -1793,10 +2078,20 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
         L.levels++;
         uint32_t total = ws->h_ctr[C_TOTAL];
         if (L.g->profiling) CUDA_TRY(cudaEventRecord(ws->event(L.nev++), s));
-        k_expand<RowT><<<grid_of(total, 256), 256, 0, s>>>(gd, wd, ph, l);
-        L.check();
-        k_expand_heavy<RowT><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
-        L.check();
+        if (joint) {
+            if constexpr (sizeof(RowT) <= 4) {
+                uint32_t nj = ws->h_ctr[C_JQCUR];
+                k_jexpand<RowT, false><<<grid_of(nj, 8, 148 * 8), 256, 0, s>>>(gd, wd, ph, l);
+                L.check();
+                k_jexpand<RowT, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
+                L.check();
+            }
+        } else {
+            k_expand<RowT><<<grid_of(total, 256), 256, 0, s>>>(gd, wd, ph, l);
+            L.check();
+            k_expand_heavy<RowT><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
+            L.check();
+        }
         if (uint32_t npull = ws->h_ctr[C_NPULL]) {
             uint32_t nbh = (gd.Vh + 7) / 8;
             uint32_t nbl = std::min<uint32_t>((ws->V - gd.Vh + 255) / 256, 148 * 8);
@@ -1807,6 +2102,11 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             CUDA_TRY(cudaEventRecord(ws->event(L.nev++), s));
             L.expand_launches += 2 + (ws->h_ctr[C_NPULL] ? 1 : 0);
         }
+    }
+    if (joint) {
+        k_jclear<<<64, 256, 0, s>>>(wd, 0);
+        k_jclear<<<64, 256, 0, s>>>(wd, 1);
+        L.check();
     }
 }
 
@@ -1867,6 +2167,16 @@ void run_batch(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
         case 4: run_batch_c<uint32_t>(L, g, ws, depth); break;
         default: run_batch_c<uint64_t>(L, g, ws, depth); break;
     }
+}
+
+// H layout of a batch: node-major (joint traversal) for large batches whose rows are <= 4
+// bytes and whose padded slot rows fit one warp-wide 512-byte read; slot-major otherwise.
+constexpr uint32_t JT_MIN_SLOTS = 32;
+void set_layout(riki_graph *g, Workspace *ws, uint32_t n) {
+    uint32_t rbmax = std::max(ws->last_rb[0], ws->last_rb[1]);
+    uint32_t SP = (n + 7) & ~7u;
+    ws->hnode = g->joint_on && rbmax <= 4 && n >= JT_MIN_SLOTS && SP * rbmax <= 512 ? 1 : 0;
+    ws->SP = ws->hnode ? SP : 0;
 }
 
 // bytes per H row for T keywords: 2 (T <= 2), 4 (T <= 4) or 8
@@ -2117,6 +2427,7 @@ void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, ui
                 ws->last_rb[0] = row_bytes(maxc);
                 ws->last_rb[1] = row_bytes(maxm);
                 ws->cur = n;
+                set_layout(g, ws, n);
                 std::vector<SlotState> h(n, tmpl);
                 for (uint32_t i = 0; i < n; i++) {
                     SlotState &x = h[i];
@@ -2176,6 +2487,7 @@ void engine_search_device(riki_graph *g, uint32_t nq, const uint64_t *d_cptr, co
         ws->last_rb[0] = row_bytes(maxc);
         ws->last_rb[1] = row_bytes(maxm);
         ws->cur = nq;
+        set_layout(g, ws, nq);
         k_slots_from_device<<<(nq + 127) / 128, 128, 0, L.s>>>(ws->st, nq, 0, nq, d_cptr, d_cterms,
                                                                       d_mptr, d_mterms, tmpl, g->d_tptr, g->n_terms);
         L.check();
@@ -2210,6 +2522,7 @@ void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uin
     Workspace *ws = g->ws;
     ws->last_rb[0] = row_bytes(T);
     ws->last_rb[1] = 4;
+    ws->hnode = 0;
     SlotState x = make_template(1, depth, riki_params{0.5, 0, 0, 0, 0, 0});
     x.w = 0xFFFFFFFFu;
     ws->cur = 1;

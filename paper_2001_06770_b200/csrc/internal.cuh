@@ -50,7 +50,7 @@ struct riki_graph {
     std::vector<uint64_t> h_tptr;
     uint64_t graph_bytes = 0;
     Workspace *ws = nullptr;
-    bool profiling = false, debug = false, pull_on = false;
+    bool profiling = false, debug = false, pull_on = false, joint_on = false;
     uint32_t batch_slots = 0;
     riki_stats stats{};
 

@@ -100,6 +100,7 @@ def load():
         "riki_reset_stats": (i32, [P]),
         "riki_set_debug": (i32, [P, i32]),
         "riki_set_direction": (i32, [P, i32]),
+        "riki_set_joint": (i32, [P, i32]),
         "riki_set_batch_slots": (i32, [P, u32]),
         "riki_memory_footprint": (i32, [P, P, P]),
         "riki_last_error": (C.c_char_p, []),
@@ -323,6 +324,10 @@ class Graph:
     def set_direction(self, mode):
         """0 = push (default), 1 = direction-optimising (pull for dense frontiers)."""
         _check(self.lib.riki_set_direction(self.h, mode))
+
+    def set_joint(self, on=True):
+        """Joint multi-query traversal for large batches (identical results)."""
+        _check(self.lib.riki_set_joint(self.h, int(on)))
 
     def set_batch_slots(self, n):
         _check(self.lib.riki_set_batch_slots(self.h, n))

@@ -331,3 +331,69 @@ def test_search_c3_dbpedia_shaped_sampled(P):
         ro = _oracle_run(og, kg.posting, qs.central[i], qs.marginal[i], qs.k, qs.depth, want_matrices=False)
         _cmp_results(res[i], ro)
         assert res[i].stats["relax_central"] == ro.relax_c and res[i].stats["relax_marginal"] == ro.relax_m
+
+
+def test_joint_traversal_c1_batch(P):
+    # joint multi-query traversal (node-major H, union frontier) == oracle, query by query
+    kg = synth.make_kg(1)
+    qs = synth.config_queries(kg, 1)
+    g = P.Graph(kg.n_nodes, kg.src, kg.dst, kg.label_class, kg.term_ptr, kg.postings)
+    g.set_label_weights(0.5, kg.avg_hops)
+    og = O.Graph(kg.n_nodes, kg.src, kg.dst, g.activation_levels())
+    g.set_joint(True)
+    res = g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)
+    for i, r in enumerate(res):
+        ro = _oracle_run(og, kg.posting, qs.central[i], qs.marginal[i], qs.k, qs.depth)
+        _cmp_results(r, ro)
+        assert r.stats["relax_central"] == ro.relax_c and r.stats["relax_marginal"] == ro.relax_m
+        assert r.stats["L_central"] == ro.Lc and r.stats["L_marginal"] == ro.Lm
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_joint_traversal_random_batches(P, seed):
+    rng = np.random.default_rng(9900 + seed)
+    V, src, dst, act, _ = random_instance(rng, 300, 2000, deg=3.0, amax=4)
+    post = [np.unique(rng.integers(0, V, int(rng.integers(1, 6)))).astype(np.uint32) for _ in range(24)]
+    g = _dev_graph(P, V, src, dst, act, post)
+    g.set_debug(True)
+    og = O.Graph(V, src, dst, act)
+    nq = int(rng.choice([40, 64, 100]))
+    Cs, Ms = [], []
+    maxt = int(rng.choice([2, 4]))
+    for _ in range(nq):
+        nc = int(rng.integers(1, maxt + 1))
+        nm = int(rng.integers(0, maxt + 1))
+        tt = rng.choice(24, nc + nm, replace=False)
+        Cs.append(tt[:nc].tolist())
+        Ms.append(tt[nc:].tolist())
+    k = int(rng.choice([1, 4]))
+    g.set_joint(True)
+    res = g.search_batch(Cs, Ms, k, 20)
+    g.set_joint(False)
+    ref = g.search_batch(Cs, Ms, k, 20)
+    for i in range(nq):
+        _cmp_results(res[i], ref[i])
+        assert res[i].candidates == ref[i].candidates and res[i].stats == ref[i].stats
+        if i % 7 == 0:
+            ro = _oracle_run(og, lambda t: post[t], Cs[i], Ms[i], k, 20)
+            _cmp_results(res[i], ro)
+            assert res[i].stats["relax_central"] == ro.relax_c and res[i].stats["relax_marginal"] == ro.relax_m
+
+
+@pytest.mark.slow
+def test_joint_traversal_c2_sampled(P):
+    kg = synth.make_kg(2)
+    qs = synth.config_queries(kg, 2)
+    g = P.Graph(kg.n_nodes, kg.src, kg.dst, kg.label_class, kg.term_ptr, kg.postings)
+    g.set_label_weights(0.5, kg.avg_hops)
+    g.set_joint(True)
+    res = g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)
+    g.set_joint(False)
+    ref = g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)
+    for i in range(len(res)):
+        _cmp_results(res[i], ref[i])
+        assert res[i].stats == ref[i].stats
+    og = O.Graph(kg.n_nodes, kg.src, kg.dst, g.activation_levels())
+    for i in (0, 99, 199):
+        _cmp_results(res[i], _oracle_run(og, kg.posting, qs.central[i], qs.marginal[i], qs.k, qs.depth,
+                                         want_matrices=False))
