@@ -1839,6 +1839,7 @@ __global__ void k_pack_H(GraphDev g, WsDev w, uint32_t T, uint8_t *Hout, uint8_t
 struct Workspace {
     uint32_t track_reached = 0;
     uint32_t hnode = 0, SP = 0;  // H layout of the current batch
+    uint32_t hcap[2] = {0, 0};   // bytes per H row allocated per run
     uint32_t cur = 0;  // slots used by the current batch (<= slots)
     uint32_t slots = 0, V = 0, W = 0, capc = 0, kmax = 0, heavy_cap = 0, ovf_cap = 0, big_ctas = 0;
     uint64_t arena_cap = 0, out_cap = 0, big_words = 0;
@@ -1934,13 +1935,15 @@ struct Tracer {  // RIKI_TRACE=<ms>: print the stage times of calls slower than 
 struct Caps {
     uint32_t slots, capc, kmax;
     uint64_t arena, out;
+    uint32_t rb[2];  // bytes per H row needed by each run
 };
 
 void ensure_workspace(riki_graph *g, const Caps &c) {
     Workspace *ws = g->ws;
     if (ws && ws->slots >= c.slots && ws->V == g->V && ws->capc >= c.capc && ws->kmax >= c.kmax &&
-        ws->arena_cap >= c.arena && ws->out_cap >= c.out)
+        ws->arena_cap >= c.arena && ws->out_cap >= c.out && ws->hcap[0] >= c.rb[0] && ws->hcap[1] >= c.rb[1])
         return;
+    uint32_t hb0 = std::max<uint32_t>(c.rb[0], ws ? ws->hcap[0] : 0), hb1 = std::max<uint32_t>(c.rb[1], ws ? ws->hcap[1] : 0);
     if (ws) { ws->release(); delete ws; g->ws = nullptr; }
     g->stats.reallocs++;
     ws = new Workspace();
@@ -1949,8 +1952,11 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     ws->slots = c.slots; ws->V = V; ws->W = (V + 31) / 32; ws->capc = c.capc; ws->kmax = c.kmax;
     ws->arena_cap = c.arena; ws->out_cap = c.out;
     const size_t S = c.slots;
-    ws->H[0] = ws->alloc<uint8_t>(S * V * 8);
-    ws->H[1] = ws->alloc<uint8_t>(S * V * 8);
+    ws->hcap[0] = hb0;
+    ws->hcap[1] = hb1;
+    const size_t S8 = (S + 7) & ~(size_t)7;  // node-major layout pads slots to a multiple of 8
+    ws->H[0] = ws->alloc<uint8_t>(S8 * V * hb0);
+    ws->H[1] = ws->alloc<uint8_t>(S8 * V * hb1);
     ws->q = ws->alloc<uint32_t>(S * 2 * V);
     ws->jq = ws->alloc<uint32_t>(2 * (size_t)V);
     ws->jbm = ws->alloc<uint32_t>(2 * (size_t)ws->W);
@@ -2228,13 +2234,14 @@ SlotState make_template(uint32_t k, uint32_t depth, const riki_params &p) {
     return t;
 }
 
-uint32_t auto_slots(riki_graph *g, uint32_t nq) {
+uint32_t auto_slots(riki_graph *g, uint32_t nq, uint32_t rb0, uint32_t rb1) {
     uint32_t want = g->batch_slots ? g->batch_slots : 256;
     want = std::min<uint32_t>(want, MAX_SLOTS);
     want = std::min<uint32_t>(want, std::max<uint32_t>(nq, 1));
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
-    uint64_t per = (uint64_t)g->V * (8 + 8 + 8) + 4096ull * (8 + sizeof(Cand) + 16 + 8) + 64 * 1024;
+    uint64_t per = (uint64_t)g->V * (rb0 + rb1 + 8) + 16384ull * (8 + sizeof(Cand) + 16 + 8) +
+                   16ull * 8192 * 16 + 64 * 1024;
     uint64_t budget = fr > (4ull << 30) ? (fr - (4ull << 30)) / 2 : fr / 4;
     uint32_t fit = (uint32_t)std::max<uint64_t>(1, budget / std::max<uint64_t>(per, 1));
     return std::max<uint32_t>(1, std::min(want, fit));
@@ -2380,9 +2387,11 @@ static void check_common(riki_graph *g, uint32_t k, uint32_t depth, const riki_p
     if (p.beam_w && p.beam_w < k) RIKI_THROW(RIKI_EINVAL, "beam width must be >= k (P:309)");
 }
 
-static Caps initial_caps(riki_graph *g, uint32_t nq, uint32_t k) {
+static Caps initial_caps(riki_graph *g, uint32_t nq, uint32_t k, uint32_t rb0, uint32_t rb1) {
     Caps c;
-    c.slots = auto_slots(g, nq);
+    c.rb[0] = rb0;
+    c.rb[1] = rb1;
+    c.slots = auto_slots(g, nq, rb0, rb1);
     c.capc = std::min<uint32_t>(16384, next_pow2(g->V + 1));
     c.kmax = std::max<uint32_t>(k, g->ws ? g->ws->kmax : 1);
     c.arena = std::max<uint64_t>(64ull << 20, g->ws ? g->ws->arena_cap : 0);
@@ -2398,7 +2407,9 @@ void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, ui
     out->assign(qs.size(), nullptr);
     if (qs.empty()) return;
     Tracer tr;
-    Caps caps = initial_caps(g, (uint32_t)qs.size(), k);
+    uint32_t maxc0 = 0, maxm0 = 0;
+    for (const QueryIn &q : qs) { maxc0 = std::max(maxc0, q.nc); maxm0 = std::max(maxm0, q.nm); }
+    Caps caps = initial_caps(g, (uint32_t)qs.size(), k, row_bytes(maxc0), row_bytes(std::max(maxm0, 1u)));
     tr("initial_caps");
     Launch L{g, stream ? stream : g->stream};
     if (stream) {
@@ -2464,22 +2475,23 @@ void engine_search_device(riki_graph *g, uint32_t nq, const uint64_t *d_cptr, co
                           const uint64_t *d_mptr, const uint32_t *d_mterms, uint32_t k, uint32_t depth,
                           const riki_params &p) {
     check_common(g, k, depth, p);
-    Caps caps = initial_caps(g, nq, k);
-    caps.slots = std::max(caps.slots, std::min<uint32_t>(nq, MAX_SLOTS));
-    ensure_workspace(g, caps);
-    if (nq > g->ws->slots) RIKI_THROW(RIKI_EINVAL, "device batch larger than the workspace slots");
-    Launch L{g, g->stream};
-    SlotState tmpl = make_template(k, depth, p);
     // row widths need the max term counts: read the (small) pointer arrays' extents on device
     std::vector<uint64_t> cp(nq + 1), mp(nq + 1);
-    CUDA_TRY(cudaMemcpyAsync(cp.data(), d_cptr, (nq + 1) * 8, cudaMemcpyDeviceToHost, L.s));
-    CUDA_TRY(cudaMemcpyAsync(mp.data(), d_mptr, (nq + 1) * 8, cudaMemcpyDeviceToHost, L.s));
-    CUDA_TRY(cudaStreamSynchronize(L.s));
+    CUDA_TRY(cudaMemcpyAsync(cp.data(), d_cptr, (nq + 1) * 8, cudaMemcpyDeviceToHost, g->stream));
+    CUDA_TRY(cudaMemcpyAsync(mp.data(), d_mptr, (nq + 1) * 8, cudaMemcpyDeviceToHost, g->stream));
+    CUDA_TRY(cudaStreamSynchronize(g->stream));
     uint32_t maxc = 0, maxm = 0;
     for (uint32_t q = 0; q < nq; q++) {
         maxc = std::max<uint32_t>(maxc, (uint32_t)(cp[q + 1] - cp[q]));
         maxm = std::max<uint32_t>(maxm, (uint32_t)(mp[q + 1] - mp[q]));
     }
+    if (maxc > RIKI_MAX_TERMS || maxm > RIKI_MAX_TERMS) RIKI_THROW(RIKI_EINVAL, "at most 8 terms per keyword class");
+    Caps caps = initial_caps(g, nq, k, row_bytes(std::max(maxc, 1u)), row_bytes(std::max(maxm, 1u)));
+    caps.slots = std::max(caps.slots, std::min<uint32_t>(nq, MAX_SLOTS));
+    ensure_workspace(g, caps);
+    if (nq > g->ws->slots) RIKI_THROW(RIKI_EINVAL, "device batch larger than the workspace slots");
+    Launch L{g, g->stream};
+    SlotState tmpl = make_template(k, depth, p);
     if (maxc == 0) RIKI_THROW(RIKI_EEMPTY_CENTRAL, "C must be non-empty (Def. RPQ, P:105)");
     std::vector<SlotState> stv;
     auto upload = [&]() {
@@ -2517,7 +2529,7 @@ void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uin
     q.nc = T;
     for (uint32_t j = 0; j < T; j++) q.c[j] = terms[j];
     check_query_host(g, q);
-    Caps caps = initial_caps(g, 1, 1);
+    Caps caps = initial_caps(g, 1, 1, row_bytes(T), 2);
     ensure_workspace(g, caps);
     Workspace *ws = g->ws;
     ws->last_rb[0] = row_bytes(T);

@@ -82,7 +82,7 @@ CONFIGS = {
     3: ConfigSpec("dbpedia-5M", 5_000_000, 20_000_000, 1000, 3, 3, 20, 20, 1000,
                   *_scaled(5, 6059, 5_000_000, 15.1e6), 8192, 3.87),
     4: ConfigSpec("wikidata-30M", 30_000_000, 150_000_000, 2000, 2, 4, 20, 20, 200,
-                  *_scaled(51, 87102, 30_000_000, 30.6e6), 8192, 3.68, True),
+                  *_scaled(51, 87102, 30_000_000, 30.6e6), 1024, 3.68, True),
 }
 
 
@@ -144,27 +144,33 @@ def make_graph(n_nodes: int, n_edges: int, n_labels: int, seed: int, *, in_exp: 
 
 
 def make_postings(n_nodes: int, n_terms: int, lo: int, hi: int, seed: int, degree=None):
-    """Inverted index with log-uniform posting sizes in [lo, hi] (Table 3 frequencies scaled)."""
+    """Inverted index with log-uniform posting sizes in [lo, hi] (Table 3 frequencies scaled);
+    members uniform, or proportional to degree ("high-degree keyword nodes", config 4)."""
     rng = np.random.default_rng(seed)
     hi = min(hi, n_nodes)
     lo = min(lo, hi)
     sizes = np.exp(rng.uniform(np.log(lo), np.log(hi + 1), n_terms)).astype(np.int64)
     sizes = np.clip(sizes, lo, hi)
+    cdf = None
     if degree is not None:
-        p = degree.astype(np.float64) + 1.0
-        p /= p.sum()
+        cdf = np.cumsum(degree.astype(np.float64) + 1.0)
+        cdf /= cdf[-1]
     ptr = np.zeros(n_terms + 1, np.uint64)
     lists = []
     for t in range(n_terms):
         s = int(sizes[t])
-        if degree is None:
-            nodes = rng.choice(n_nodes, size=s, replace=False) if s * 4 > n_nodes else \
-                np.unique(rng.integers(0, n_nodes, 2 * s))[:s]
-            if len(nodes) < s:
-                nodes = rng.choice(n_nodes, size=s, replace=False)
-        else:
-            nodes = np.unique(_sample(rng, p, 2 * s))[:s]
-        nodes = np.unique(nodes).astype(np.uint32)
+        nodes = np.zeros(0, np.int64)
+        for _ in range(8):  # draw with replacement, keep unique, top up
+            if cdf is None:
+                draw = rng.integers(0, n_nodes, 2 * s + 8)
+            else:
+                draw = np.searchsorted(cdf, rng.random(2 * s + 8), side="right")
+            nodes = np.unique(np.concatenate([nodes, draw]))
+            if len(nodes) >= s:
+                break
+        if len(nodes) > s:
+            nodes = np.sort(rng.choice(nodes, size=s, replace=False))
+        nodes = nodes.astype(np.uint32)
         lists.append(nodes)
         ptr[t + 1] = ptr[t] + len(nodes)
     return ptr, np.concatenate(lists).astype(np.uint32)
