@@ -368,6 +368,62 @@ __device__ __forceinline__ void frontier_push(const WsDev &w, bool want, uint32_
     }
 }
 
+// Per-warp staging of next-frontier entries in shared memory: pushes are warp-local (no
+// atomics on the edge loop's dependency chain); a flush appends each run of same-slot
+// entries with ONE atomicAdd on the slot's queue counter.
+constexpr uint32_t WQCAP = 256;
+struct WarpQ {
+    uint32_t *ent;
+    uint32_t *slot;
+    uint32_t cnt;  // warp-uniform
+};
+__device__ __forceinline__ void wq_flush(const WsDev &w, WarpQ &q, uint32_t nxt) {
+    __syncwarp();
+    const uint32_t lane = lane_id();
+    uint32_t i = 0;
+    while (i < q.cnt) {
+        const uint32_t s0 = q.slot[i];
+        uint32_t j = i;  // end of the run of slot s0
+        while (j < q.cnt) {
+            uint32_t k = j + lane;
+            uint32_t diff = __ballot_sync(FULLMASK, k < q.cnt && q.slot[k] != s0);
+            if (diff) { j += __ffs(diff) - 1; break; }
+            j = min(j + 32, q.cnt);
+        }
+        const uint32_t n = j - i;
+        uint32_t base = 0, fresh = 0;
+        for (uint32_t k = i + lane; k < j; k += 32) fresh += !(q.ent[k] & RETAINED);
+        fresh = warp_sum(fresh);
+        if (lane == 0) {
+            base = atomicAdd(&w.st[s0].nq[nxt], n);
+            if (w.track_reached && fresh) atomicAdd(&w.st[s0].reached, fresh);
+        }
+        base = __shfl_sync(FULLMASK, base, 0);
+        uint32_t *Qd = w.Q(s0, nxt);
+        for (uint32_t k = i + lane; k < j; k += 32) Qd[base + (k - i)] = q.ent[k];
+        i = j;
+    }
+    __syncwarp();
+    q.cnt = 0;
+}
+#ifndef EXP_WQ
+#define EXP_WQ 1
+#endif
+__device__ __forceinline__ void wq_push(const WsDev &w, WarpQ &q, bool want, uint32_t s, uint32_t entry, uint32_t nxt) {
+#if !EXP_WQ
+    frontier_push(w, want, s, entry, nxt);
+    return;
+#endif
+    const uint32_t m = __ballot_sync(FULLMASK, want);
+    if (want) {
+        uint32_t r = q.cnt + __popc(m & lanemask_lt());
+        q.ent[r] = entry;
+        q.slot[r] = s;
+    }
+    q.cnt += __popc(m);
+    if (q.cnt > WQCAP - 32) wq_flush(w, q, nxt);
+}
+
 __device__ __forceinline__ void cand_push(const GraphDev &g, const WsDev &w, bool want, uint32_t s, uint32_t n,
                                           uint32_t level) {
     uint32_t pos = warp_append(want, s, &w.st[0].ncand, sizeof(SlotState) / 4);
@@ -410,6 +466,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
     typedef Row<RowT> R;
     __shared__ uint32_t s_offs[MAX_SLOTS + 1];
     __shared__ uint32_t s_info[MAX_SLOTS];
+    __shared__ uint32_t s_wq[8][2][WQCAP];
     const uint32_t ns = w.nslots;
     for (uint32_t i = threadIdx.x; i <= ns; i += blockDim.x) s_offs[i] = w.offs[i];
     for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {
@@ -424,6 +481,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const RowT L = R::splat(l);
     uint32_t p_items = 0, p_edges = 0, p_cells = 0, p_enq = 0;
+    WarpQ wq{s_wq[threadIdx.x >> 5][0], s_wq[threadIdx.x >> 5][1], 0};
 
     for (uint32_t base = gw * 32; base < total; base += nw * 32) {
         uint32_t item = base + lane;
@@ -486,7 +544,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
                 if (lane == __ffs(peers) - 1 && sum) atomicAdd(&w.st[s].relax[ph], (unsigned long long)sum);
             }
         }
-        frontier_push(w, retain, s, f | RETAINED, nxt);
+        wq_push(w, wq, retain, s, f | RETAINED, nxt);
         p_enq += retain;
 #if EXP_SMALL > 0
         {   // short ranges (<= EXP_SMALL edges): the owning lane issues all its loads at once
@@ -551,12 +609,13 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
                     p_cells += r.cells;
                     p_enq += r.enq;
                 }
-                frontier_push(w, r.enq, o_s[u], n[u], nxt);
+                wq_push(w, wq, r.enq, o_s[u], n[u], nxt);
                 bool id = r.ident && ((s_info[ev[u] ? o_s[u] : 0] >> 1) & 1);
                 cand_push(g, w, id, o_s[u], n[u], l + 1);
             }
         }
     }
+    wq_flush(w, wq, nxt);
     p_items = warp_sum(p_items);
     p_edges = warp_sum(p_edges);
     p_cells = warp_sum(p_cells);
@@ -579,6 +638,8 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
     uint32_t nh = min(w.ctr[C_NHEAVY], w.heavy_cap);
     const RowT L = R::splat(l);
     uint32_t p_cells = 0, p_enq = 0;
+    __shared__ uint32_t s_wq[8][2][WQCAP];
+    WarpQ wq{s_wq[threadIdx.x >> 5][0], s_wq[threadIdx.x >> 5][1], 0};
     for (uint32_t it = gw; it < nh; it += nw) {
         uint4 h = w.heavy[it];
         uint32_t s = h.x;
@@ -608,11 +669,12 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
                     p_cells += r.cells;
                     p_enq += r.enq;
                 }
-                frontier_push(w, r.enq, s, n[u], nxt);
+                wq_push(w, wq, r.enq, s, n[u], nxt);
                 cand_push(g, w, r.ident && collect, s, n[u], l + 1);
             }
         }
     }
+    wq_flush(w, wq, nxt);
     p_cells = warp_sum(p_cells);
     p_enq = warp_sum(p_enq);
     if (lane == 0 && (p_cells | p_enq)) {
