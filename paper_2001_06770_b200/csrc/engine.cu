@@ -55,6 +55,7 @@ struct SlotState {
     int32_t L_end[2];
     unsigned long long relax[2];
     uint32_t n_attached, n_ptc_fail, nR, nres;
+    uint32_t first_unatt, nR_sorted;  // run-2 bookkeeping (monotone cursor, sorted prefix of R)
     uint32_t err, active;
 };
 
@@ -179,6 +180,8 @@ __global__ void k_phase_begin(WsDev w, int ph, int hitting_mode) {
         st.nR = 0;
         st.n_attached = 0;
         st.n_ptc_fail = 0;
+        st.first_unatt = 0;
+        st.nR_sorted = 0;
     }
 }
 
@@ -1758,10 +1761,18 @@ __global__ void k_decide_m(WsDev w, uint32_t l) {
     if (threadIdx.x == 0) first = EMPTY;
     __syncthreads();
     uint32_t nR = min(st.nR, w.capc);
-    cta_sort_u128(w.RK(s), nR, sm128, 1024);
-    for (uint32_t c = threadIdx.x; c < st.n_extract; c += blockDim.x)
-        if (!w.CD(s)[c].attached) atomicMin(&first, c);
+    if (nR != st.nR_sorted) cta_sort_u128(w.RK(s), nR, sm128, 1024);  // only when new RPGs arrived
+    // attachment is monotone, so the first unattached candidate only moves forward
+    for (uint32_t c0 = st.first_unatt; c0 < st.n_extract && first == EMPTY; c0 += blockDim.x) {
+        uint32_t c = c0 + threadIdx.x;
+        if (c < st.n_extract && !w.CD(s)[c].attached) atomicMin(&first, c);
+        __syncthreads();
+    }
     __syncthreads();
+    if (threadIdx.x == 0) {
+        st.nR_sorted = nR;
+        st.first_unatt = first == EMPTY ? st.n_extract : first;
+    }
     if (threadIdx.x == 0) {
         bool stop = l >= st.depth || st.nq[l & 1] == 0 || first == EMPTY;
         if (!stop && st.early_term != 2 && nR >= st.k) {
