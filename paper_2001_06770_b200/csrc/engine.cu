@@ -31,9 +31,14 @@ typedef unsigned __int128 u128;
 namespace {
 
 constexpr uint32_t MAX_SLOTS = 1024;
-constexpr uint32_t LEVEL_BATCH = 4;  // levels enqueued between host termination checks
-constexpr uint32_t HEAVY = 256;  // longer active ranges are split into CHUNK-edge work items
-constexpr uint32_t CHUNK = 256;
+#ifndef LEVEL_BATCH
+#define LEVEL_BATCH 4  // levels enqueued between host termination checks
+#endif
+#ifndef EXP_HEAVY
+#define EXP_HEAVY 128
+#endif
+constexpr uint32_t HEAVY = EXP_HEAVY;  // longer active ranges are split into CHUNK-edge work items
+constexpr uint32_t CHUNK = EXP_HEAVY;
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
 constexpr uint32_t SORT_SMEM = 8192;  // u32 keys sorted in shared memory
 
@@ -1763,10 +1768,14 @@ __global__ void k_decide_m(WsDev w, uint32_t l) {
     uint32_t nR = min(st.nR, w.capc);
     if (nR != st.nR_sorted) cta_sort_u128(w.RK(s), nR, sm128, 1024);  // only when new RPGs arrived
     // attachment is monotone, so the first unattached candidate only moves forward
-    for (uint32_t c0 = st.first_unatt; c0 < st.n_extract && first == EMPTY; c0 += blockDim.x) {
+    const uint32_t c_begin = st.first_unatt, c_end = st.n_extract;
+    for (uint32_t c0 = c_begin; c0 < c_end; c0 += blockDim.x) {
         uint32_t c = c0 + threadIdx.x;
-        if (c < st.n_extract && !w.CD(s)[c].attached) atomicMin(&first, c);
+        if (c < c_end && !w.CD(s)[c].attached) atomicMin(&first, c);
         __syncthreads();
+        const bool found = first != EMPTY;  // uniform: read between two barriers
+        __syncthreads();
+        if (found) break;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
