@@ -26,7 +26,7 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "build", os.path.basename(LIB).replace(".so", ""))
+    objdir = os.path.join("/tmp", "riki_build", os.path.basename(LIB).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []

@@ -387,6 +387,9 @@ struct WarpQ {
     uint32_t cnt;  // warp-uniform
 };
 __device__ __forceinline__ void wq_flush(const WsDev &w, WarpQ &q, uint32_t nxt) {
+#if !EXP_WQ
+    return;
+#endif
     __syncwarp();
     const uint32_t lane = lane_id();
     uint32_t i = 0;
@@ -475,7 +478,9 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
     typedef Row<RowT> R;
     __shared__ uint32_t s_offs[MAX_SLOTS + 1];
     __shared__ uint32_t s_info[MAX_SLOTS];
+#if EXP_WQ
     __shared__ uint32_t s_wq[8][2][WQCAP];
+#endif
     const uint32_t ns = w.nslots;
     for (uint32_t i = threadIdx.x; i <= ns; i += blockDim.x) s_offs[i] = w.offs[i];
     for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {
@@ -490,7 +495,11 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const RowT L = R::splat(l);
     uint32_t p_items = 0, p_edges = 0, p_cells = 0, p_enq = 0;
+#if EXP_WQ
     WarpQ wq{s_wq[threadIdx.x >> 5][0], s_wq[threadIdx.x >> 5][1], 0};
+#else
+    WarpQ wq{nullptr, nullptr, 0};
+#endif
 
     for (uint32_t base = gw * 32; base < total; base += nw * 32) {
         uint32_t item = base + lane;
@@ -647,8 +656,12 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
     uint32_t nh = min(w.ctr[C_NHEAVY], w.heavy_cap);
     const RowT L = R::splat(l);
     uint32_t p_cells = 0, p_enq = 0;
+#if EXP_WQ
     __shared__ uint32_t s_wq[8][2][WQCAP];
     WarpQ wq{s_wq[threadIdx.x >> 5][0], s_wq[threadIdx.x >> 5][1], 0};
+#else
+    WarpQ wq{nullptr, nullptr, 0};
+#endif
     for (uint32_t it = gw; it < nh; it += nw) {
         uint4 h = w.heavy[it];
         uint32_t s = h.x;
