@@ -106,8 +106,14 @@ def _dist():
     import torch.distributed as dist
     rank = int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # RIKI_BENCH_BACKEND=gloo lets several ranks share one GPU (tests of the multi-rank path);
+    # the contract run uses NCCL, one process per GPU
+    backend = os.environ.get("RIKI_BENCH_BACKEND", "nccl")
+    torch.cuda.set_device(local % torch.cuda.device_count())
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
     return rank, ws, dist
 
 
@@ -233,7 +239,8 @@ def main():
     st = g.stats()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = sum(step_ms)
-    tot_ms = max_over_ranks(tot_ms, device=f"cuda:{dev}")  # time = slowest rank (weak scaling)
+    rdev = f"cuda:{dev}" if not dist or dist.get_backend() == "nccl" else None
+    tot_ms = max_over_ranks(tot_ms, device=rdev)  # time = slowest rank (weak scaling)
     value = nq * world * args.steps / (tot_ms / 1000.0)
     res = g.fetch(nq, [len(c) for c in qs.central], [len(m) for m in qs.marginal])
     relax = sum(r.stats["relax_central"] + r.stats["relax_marginal"] for r in res)
@@ -260,7 +267,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     e2e_ms = sum(a.elapsed_time(b) for a, b in e2e_ev)
-    e2e_ms = max_over_ranks(e2e_ms, device=f"cuda:{dev}")
+    e2e_ms = max_over_ranks(e2e_ms, device=rdev)
     e2e_value = nq * world * args.steps / (e2e_ms / 1000.0)
 
     # ---------------- single-query latency (one query in flight, host API incl. D2H)
