@@ -159,6 +159,17 @@ __device__ __forceinline__ uint32_t find_slot(const uint32_t *offs, uint32_t n, 
     return lo;
 }
 
+// Warp-uniform form: largest s < n with offs[s] <= item for the same `item` in every lane
+// (n <= 32 * 32): a 32-way ballot over every stride-th boundary, then one over the stride.
+__device__ __forceinline__ uint32_t find_slot_warp(const uint32_t *offs, uint32_t n, uint32_t item) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t stride = (n + 31) >> 5;
+    const uint32_t j = lane * stride;
+    const uint32_t c = __popc(__ballot_sync(FULLMASK, j < n && offs[j] <= item)) - 1;
+    const uint32_t j2 = c * stride + lane;
+    return c * stride + __popc(__ballot_sync(FULLMASK, lane < stride && j2 < n && offs[j2] <= item)) - 1;
+}
+
 // ====================================================================== run setup
 __global__ void k_phase_begin(WsDev w, int ph, int hitting_mode) {
     uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
@@ -271,8 +282,9 @@ template <class RowT> __global__ void k_seed(GraphDev g, WsDev w, int ph) {
 __global__ void k_plan(WsDev w, int ph, uint32_t l, uint32_t pull_min) {
     __shared__ uint32_t sc[MAX_SLOTS];
     __shared__ uint32_t nact, npull;
+    __shared__ unsigned long long nenq;
     uint32_t s = threadIdx.x;
-    if (s == 0) { nact = 0; npull = 0; }
+    if (s == 0) { nact = 0; npull = 0; nenq = 0; }
     __syncthreads();
     uint32_t items = 0;
     if (s < w.nslots) {
@@ -280,6 +292,8 @@ __global__ void k_plan(WsDev w, int ph, uint32_t l, uint32_t pull_min) {
         if (st.in_phase) {
             st.level = l;
             uint32_t cur = l & 1;
+            // queue entries written by level l-1's expansion (profiling counter P_ENQ)
+            if (l > 0 && !w.hnode && st.nq[cur]) atomicAdd(&nenq, (unsigned long long)st.nq[cur]);
             bool stop;
             if (ph == 0)  // P:362 ">= w CGs", depth bound (R8), empty frontier
                 stop = st.ncand >= st.w || l >= st.depth || st.nq[cur] == 0;
@@ -318,6 +332,10 @@ __global__ void k_plan(WsDev w, int ph, uint32_t l, uint32_t pull_min) {
         w.ctr[C_TOTAL] = sc[MAX_SLOTS - 1];
         w.ctr[C_NHEAVY] = 0;
         w.ctr[C_NPULL] = npull;
+        if (!w.hnode) {  // profiling counters of the per-slot expansion (k_expand counts edges/cells)
+            w.prof[P_ITEMS] += sc[MAX_SLOTS - 1];
+            w.prof[P_ENQ] += nenq;
+        }
         // joint traversal: size of the union frontier of this level, reset the next one
         w.ctr[C_JQCUR] = w.ctr[C_JQN0 + (l & 1)];
         w.ctr[C_JQN0 + ((l & 1) ^ 1)] = 0;
@@ -362,7 +380,21 @@ constexpr uint32_t RETAINED = 0x80000000u;
 __device__ __forceinline__ void frontier_push(const WsDev &w, bool want, uint32_t s, uint32_t entry, uint32_t nxt) {
     // warp-aggregated append; new (untagged) entries are also counted in st.reached, the
     // visited estimate of the direction-optimising heuristic
-    uint32_t m = __ballot_sync(FULLMASK, want);
+    const uint32_t m = __ballot_sync(FULLMASK, want);
+    if (!m) return;
+    // usually every pushing lane is in one slot (items are slot-contiguous): no match_any
+    const uint32_t s0 = __shfl_sync(FULLMASK, s, __ffs(m) - 1);
+    if (__all_sync(FULLMASK, !want || s == s0)) {
+        const uint32_t leader = __ffs(m) - 1;
+        uint32_t base = 0;
+        if (lane_id() == leader) {
+            base = atomicAdd(&w.st[s0].nq[nxt], __popc(m));
+            if (w.track_reached && !(entry & RETAINED)) atomicAdd(&w.st[s0].reached, __popc(m));
+        }
+        base = __shfl_sync(FULLMASK, base, leader);
+        if (want) w.Q(s0, nxt)[base + __popc(m & lanemask_lt())] = entry;
+        return;
+    }
     if (want) {
         uint32_t peers = __match_any_sync(m, s);
         uint32_t leader = __ffs(peers) - 1;
@@ -375,65 +407,6 @@ __device__ __forceinline__ void frontier_push(const WsDev &w, bool want, uint32_
         base = __shfl_sync(peers, base, leader);
         w.Q(s, nxt)[base + rank] = entry;
     }
-}
-
-// Per-warp staging of next-frontier entries in shared memory: pushes are warp-local (no
-// atomics on the edge loop's dependency chain); a flush appends each run of same-slot
-// entries with ONE atomicAdd on the slot's queue counter.
-constexpr uint32_t WQCAP = 256;
-struct WarpQ {
-    uint32_t *ent;
-    uint32_t *slot;
-    uint32_t cnt;  // warp-uniform
-};
-__device__ __forceinline__ void wq_flush(const WsDev &w, WarpQ &q, uint32_t nxt) {
-#if !EXP_WQ
-    return;
-#endif
-    __syncwarp();
-    const uint32_t lane = lane_id();
-    uint32_t i = 0;
-    while (i < q.cnt) {
-        const uint32_t s0 = q.slot[i];
-        uint32_t j = i;  // end of the run of slot s0
-        while (j < q.cnt) {
-            uint32_t k = j + lane;
-            uint32_t diff = __ballot_sync(FULLMASK, k < q.cnt && q.slot[k] != s0);
-            if (diff) { j += __ffs(diff) - 1; break; }
-            j = min(j + 32, q.cnt);
-        }
-        const uint32_t n = j - i;
-        uint32_t base = 0, fresh = 0;
-        for (uint32_t k = i + lane; k < j; k += 32) fresh += !(q.ent[k] & RETAINED);
-        fresh = warp_sum(fresh);
-        if (lane == 0) {
-            base = atomicAdd(&w.st[s0].nq[nxt], n);
-            if (w.track_reached && fresh) atomicAdd(&w.st[s0].reached, fresh);
-        }
-        base = __shfl_sync(FULLMASK, base, 0);
-        uint32_t *Qd = w.Q(s0, nxt);
-        for (uint32_t k = i + lane; k < j; k += 32) Qd[base + (k - i)] = q.ent[k];
-        i = j;
-    }
-    __syncwarp();
-    q.cnt = 0;
-}
-#ifndef EXP_WQ
-#define EXP_WQ 0
-#endif
-__device__ __forceinline__ void wq_push(const WsDev &w, WarpQ &q, bool want, uint32_t s, uint32_t entry, uint32_t nxt) {
-#if !EXP_WQ
-    frontier_push(w, want, s, entry, nxt);
-    return;
-#endif
-    const uint32_t m = __ballot_sync(FULLMASK, want);
-    if (want) {
-        uint32_t r = q.cnt + __popc(m & lanemask_lt());
-        q.ent[r] = entry;
-        q.slot[r] = s;
-    }
-    q.cnt += __popc(m);
-    if (q.cnt > WQCAP - 32) wq_flush(w, q, nxt);
 }
 
 __device__ __forceinline__ void cand_push(const GraphDev &g, const WsDev &w, bool want, uint32_t s, uint32_t n,
@@ -467,20 +440,22 @@ __device__ __forceinline__ uint32_t lower_bound_act(const uint8_t *act, uint32_t
 #ifndef EXP_UNROLL
 #define EXP_UNROLL 2
 #endif
-#ifndef EXP_SMALL
-#define EXP_SMALL 0
-#endif
 #ifndef EXP_MINB
 #define EXP_MINB 8
 #endif
+// Item fields of one non-empty active range, compacted per warp in shared memory for the
+// edge walk: edge index e = delta + idx, and edges with idx >= thr also carry the old columns.
+template <class RowT> struct alignas(16) OwnF {
+    uint32_t delta, thr, s;
+    RowT nw, od;
+};
+
 template <class RowT>
 __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, int ph, uint32_t l) {
     typedef Row<RowT> R;
     __shared__ uint32_t s_offs[MAX_SLOTS + 1];
     __shared__ uint32_t s_info[MAX_SLOTS];
-#if EXP_WQ
-    __shared__ uint32_t s_wq[8][2][WQCAP];
-#endif
+    __shared__ OwnF<RowT> s_own[8][32];
     const uint32_t ns = w.nslots;
     for (uint32_t i = threadIdx.x; i <= ns; i += blockDim.x) s_offs[i] = w.offs[i];
     for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {
@@ -494,26 +469,27 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const RowT L = R::splat(l);
-    uint32_t p_items = 0, p_edges = 0, p_cells = 0, p_enq = 0;
-#if EXP_WQ
-    WarpQ wq{s_wq[threadIdx.x >> 5][0], s_wq[threadIdx.x >> 5][1], 0};
-#else
-    WarpQ wq{nullptr, nullptr, 0};
-#endif
+    RowT *const Hb = (RowT *)w.H[ph];  // slot-major: row (s, n) at Hb + s*V + n (never joint here)
+    const size_t V = w.V;
+    OwnF<RowT> *const own = s_own[threadIdx.x >> 5];
+    uint32_t p_edges = 0, p_cells = 0;  // items and queue entries are counted by k_plan
 
     for (uint32_t base = gw * 32; base < total; base += nw * 32) {
         uint32_t item = base + lane;
         bool valid = item < total;
-        uint32_t s = 0, f = 0, lo = 0, len = 0, relaxn = 0, eq0 = 0;
+        // slots of this warp's 32 items: two warp-uniform searches, then (rarely) a short
+        // per-lane search between them
+        const uint32_t sA = find_slot_warp(s_offs, ns, base);
+        const uint32_t sB = find_slot_warp(s_offs, ns, min(base + 31, total - 1));
+        uint32_t s = sA, f = 0, lo = 0, len = 0, relaxn = 0, eq0 = 0;
         RowT newc = 0, oldc = 0;
         bool retain = false;
         if (valid) {
-            s = find_slot(s_offs, ns, item);
+            if (sB != sA) s = find_slot(s_offs + sA, sB - sA + 1, item) + sA;
             uint32_t info = s_info[s];
             uint32_t ent = w.Q(s, cur)[item - s_offs[s]];
             f = ent & ~RETAINED;
-            const HV<RowT> H = w.Hs<RowT>(ph, s);
-            RowT Rf = R::load(H + f);
+            RowT Rf = R::load(Hb + (size_t)s * V + f);
             RowT used = used_mask<RowT>(info >> 8);
             bool dup = (ent & RETAINED) && (R::eq(Rf, L) & used);
             bool blocked = (info & 1) && R::le(Rf, L) == (RowT)~(RowT)0;  // CF: row complete, max <= l
@@ -552,97 +528,84 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
                     }
                 }
             }
-            p_items++;
         }
         {   // relaxation count per slot (aggregated)
-            uint32_t vm = __ballot_sync(FULLMASK, valid);
-            if (valid) {
-                uint32_t peers = __match_any_sync(vm, s);
-                uint32_t sum = __reduce_add_sync(peers, relaxn);
-                if (lane == __ffs(peers) - 1 && sum) atomicAdd(&w.st[s].relax[ph], (unsigned long long)sum);
-            }
-        }
-        wq_push(w, wq, retain, s, f | RETAINED, nxt);
-        p_enq += retain;
-#if EXP_SMALL > 0
-        {   // short ranges (<= EXP_SMALL edges): the owning lane issues all its loads at once
-            const bool small = len > 0 && len <= EXP_SMALL;
-            const bool collect = valid && ((s_info[s] >> 1) & 1);
-            const HV<RowT> H = w.Hs<RowT>(ph, s);
-            uint32_t nA[EXP_SMALL];
-            RowT hA[EXP_SMALL];
-#pragma unroll
-            for (int u = 0; u < EXP_SMALL; u++) nA[u] = (small && u < (int)len) ? __ldg(g.col + lo + u) : 0;
-#pragma unroll
-            for (int u = 0; u < EXP_SMALL; u++) hA[u] = (small && u < (int)len) ? R::load(H + nA[u]) : (RowT)0;
-#pragma unroll
-            for (int u = 0; u < EXP_SMALL; u++) {
-                Relax<RowT> r{false, false, 0};
-                if (small && u < (int)len) {
-                    RowT mask = newc | (lo + u >= eq0 ? oldc : (RowT)0);
-                    r = relax<RowT>(H, nA[u], hA[u], mask, l);
-                    p_cells += r.cells;
-                    p_enq += r.enq;
+            if (sA == sB) {
+                uint32_t sum = __reduce_add_sync(FULLMASK, relaxn);
+                if (lane == 0 && sum) atomicAdd(&w.st[sA].relax[ph], (unsigned long long)sum);
+            } else {
+                uint32_t vm = __ballot_sync(FULLMASK, valid);
+                if (valid) {
+                    uint32_t peers = __match_any_sync(vm, s);
+                    uint32_t sum = __reduce_add_sync(peers, relaxn);
+                    if (lane == __ffs(peers) - 1 && sum) atomicAdd(&w.st[s].relax[ph], (unsigned long long)sum);
                 }
-                frontier_push(w, r.enq, s, nA[u], nxt);
-                cand_push(g, w, r.ident && collect, s, nA[u], l + 1);
             }
-            if (small) len = 0;
         }
-#endif
-        // edge-parallel walk over the remaining active ranges, EXP_UNROLL edges per lane in flight
-        uint32_t incl = warp_incl_scan(len);
-        uint32_t tot = __shfl_sync(FULLMASK, incl, 31);
-        uint32_t excl = incl - len;
+        frontier_push(w, retain, s, f | RETAINED, nxt);
+        // Edge-parallel walk over the concatenated active ranges, EXP_UNROLL edges per lane in
+        // flight.  The non-empty ranges are compacted into s_own (rank order = start order);
+        // the owner of edge position p of a 32-wide chunk is found from the bit mask of range
+        // starts inside the chunk (one OR-reduction) instead of a per-edge binary search.
+        const uint32_t incl = warp_incl_scan(len);
+        const uint32_t tot = __shfl_sync(FULLMASK, incl, 31);
+        if (tot == 0) continue;
+        const uint32_t excl = incl - len;
+        {
+            const uint32_t NE = __ballot_sync(FULLMASK, len > 0);
+            __syncwarp();  // previous iteration's readers are done with s_own
+            if (len > 0) {
+                OwnF<RowT> o;
+                o.delta = lo - excl;
+                o.thr = eq0 - lo + excl;
+                o.s = s;
+                o.nw = newc;
+                o.od = oldc;
+                own[__popc(NE & lanemask_lt())] = o;
+            }
+            __syncwarp();
+        }
+        const uint32_t le_mask = lanemask_lt() | (1u << lane);
+        int own_last = -1;
         for (uint32_t eb = 0; eb < tot; eb += 32 * EXP_UNROLL) {
             uint32_t n[EXP_UNROLL], o_s[EXP_UNROLL];
             RowT mask[EXP_UNROLL], hn[EXP_UNROLL];
             bool ev[EXP_UNROLL];
 #pragma unroll
             for (int u = 0; u < EXP_UNROLL; u++) {
-                uint32_t idx = eb + 32 * u + lane;
+                const uint32_t cb = eb + 32 * u;
+                const uint32_t off = excl - cb;  // < 32 iff this lane's range starts in the chunk
+                const uint32_t M = __reduce_or_sync(FULLMASK, (len > 0 && off < 32) ? 1u << off : 0u);
+                const int own0 = own_last + (int)(M & 1u);
+                const int ow = own0 + __popc(M & ~1u & le_mask);
+                own_last = own0 + __popc(M & ~1u);
+                const uint32_t idx = cb + lane;
                 ev[u] = idx < tot;
-                uint32_t own = 0;  // owner lane: largest i with excl_i <= idx
-#pragma unroll
-                for (uint32_t step = 16; step > 0; step >>= 1) {
-                    uint32_t cand = own + step;
-                    if (__shfl_sync(FULLMASK, excl, cand) <= idx) own = cand;
-                }
-                uint32_t o_lo = __shfl_sync(FULLMASK, lo, own);
-                uint32_t o_ex = __shfl_sync(FULLMASK, excl, own);
-                uint32_t o_eq = __shfl_sync(FULLMASK, eq0, own);
-                o_s[u] = __shfl_sync(FULLMASK, s, own);
-                RowT o_new = shfl(newc, own), o_old = shfl(oldc, own);
-                uint32_t e = o_lo + (idx - o_ex);
-                n[u] = ev[u] ? __ldg(g.col + e) : 0;
-                mask[u] = o_new | (e >= o_eq ? o_old : (RowT)0);  // [eqlo, hi) are the edges with a == l
+                const OwnF<RowT> o = own[ev[u] ? ow : 0];
+                o_s[u] = o.s;
+                n[u] = ev[u] ? __ldg(g.col + (uint32_t)(o.delta + idx)) : 0;  // delta wraps: add in 32 bits
+                mask[u] = o.nw | (idx >= o.thr ? o.od : (RowT)0);  // [eqlo, hi) are the edges with a == l
             }
 #pragma unroll
-            for (int u = 0; u < EXP_UNROLL; u++) hn[u] = ev[u] ? R::load(w.Hs<RowT>(ph, o_s[u]) + n[u]) : (RowT)0;
+            for (int u = 0; u < EXP_UNROLL; u++) hn[u] = ev[u] ? R::load(Hb + (size_t)o_s[u] * V + n[u]) : (RowT)0;
 #pragma unroll
             for (int u = 0; u < EXP_UNROLL; u++) {
                 Relax<RowT> r{false, false, 0};
                 if (ev[u]) {
-                    r = relax<RowT>(w.Hs<RowT>(ph, o_s[u]), n[u], hn[u], mask[u], l);
+                    r = relax<RowT>(HV<RowT>{Hb + (size_t)o_s[u] * V, 1u}, n[u], hn[u], mask[u], l);
                     p_cells += r.cells;
-                    p_enq += r.enq;
                 }
-                wq_push(w, wq, r.enq, o_s[u], n[u], nxt);
-                bool id = r.ident && ((s_info[ev[u] ? o_s[u] : 0] >> 1) & 1);
+                frontier_push(w, r.enq, o_s[u], n[u], nxt);
+                bool id = r.ident && ((s_info[o_s[u]] >> 1) & 1);
                 cand_push(g, w, id, o_s[u], n[u], l + 1);
             }
         }
     }
-    wq_flush(w, wq, nxt);
-    p_items = warp_sum(p_items);
     p_edges = warp_sum(p_edges);
     p_cells = warp_sum(p_cells);
-    p_enq = warp_sum(p_enq);
-    if (lane == 0 && (p_items | p_edges)) {
-        atomicAdd(&w.prof[P_ITEMS], (unsigned long long)p_items);
+    if (lane == 0 && (p_edges | p_cells)) {
         atomicAdd(&w.prof[P_EDGES], (unsigned long long)p_edges);
         atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
-        atomicAdd(&w.prof[P_ENQ], (unsigned long long)p_enq);
     }
 }
 
@@ -655,20 +618,14 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     uint32_t nh = min(w.ctr[C_NHEAVY], w.heavy_cap);
     const RowT L = R::splat(l);
-    uint32_t p_cells = 0, p_enq = 0;
-#if EXP_WQ
-    __shared__ uint32_t s_wq[8][2][WQCAP];
-    WarpQ wq{s_wq[threadIdx.x >> 5][0], s_wq[threadIdx.x >> 5][1], 0};
-#else
-    WarpQ wq{nullptr, nullptr, 0};
-#endif
+    uint32_t p_cells = 0;
     for (uint32_t it = gw; it < nh; it += nw) {
         uint4 h = w.heavy[it];
         uint32_t s = h.x;
         const SlotState &st = w.st[s];
         RowT used = used_mask<RowT>(st.T[ph]);
-        const HV<RowT> H = w.Hs<RowT>(ph, s);
-        RowT Rf = R::load(H + h.y);  // values <= l are final; concurrent l+1 writes don't change the masks
+        RowT *const Hs = (RowT *)w.H[ph] + (size_t)s * w.V;  // slot-major (never joint here)
+        RowT Rf = R::load(Hs + h.y);  // values <= l are final; concurrent l+1 writes don't change the masks
         RowT newc = R::eq(Rf, L) & used, oldc = R::lt(Rf, L) & used;
         bool collect = st.collect;
         for (uint32_t e0 = h.z; e0 < h.w; e0 += 64) {
@@ -681,28 +638,22 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
                 a[u] = e < h.w ? __ldg(g.act + e) : 0xFF;
             }
 #pragma unroll
-            for (int u = 0; u < 2; u++) hn[u] = (e0 + 32 * u + lane < h.w) ? R::load(H + n[u]) : (RowT)0;
+            for (int u = 0; u < 2; u++) hn[u] = (e0 + 32 * u + lane < h.w) ? R::load(Hs + n[u]) : (RowT)0;
 #pragma unroll
             for (int u = 0; u < 2; u++) {
                 Relax<RowT> r{false, false, 0};
                 if (e0 + 32 * u + lane < h.w) {
                     RowT mask = newc | (a[u] == l ? oldc : (RowT)0);
-                    r = relax<RowT>(H, n[u], hn[u], mask, l);
+                    r = relax<RowT>(HV<RowT>{Hs, 1u}, n[u], hn[u], mask, l);
                     p_cells += r.cells;
-                    p_enq += r.enq;
                 }
-                wq_push(w, wq, r.enq, s, n[u], nxt);
+                frontier_push(w, r.enq, s, n[u], nxt);
                 cand_push(g, w, r.ident && collect, s, n[u], l + 1);
             }
         }
     }
-    wq_flush(w, wq, nxt);
     p_cells = warp_sum(p_cells);
-    p_enq = warp_sum(p_enq);
-    if (lane == 0 && (p_cells | p_enq)) {
-        atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
-        atomicAdd(&w.prof[P_ENQ], (unsigned long long)p_enq);
-    }
+    if (lane == 0 && p_cells) atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
 }
 
 // Bottom-up expansion of a dense level (direction-optimising BFS).  Node n with an infinite
@@ -722,7 +673,7 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_pull(Gr
     const RowT FF = R::splat(0xFF), L = R::splat(l);
     const bool blocking = st.blocking, collect = st.collect;
     const uint32_t nxt = (l & 1) ^ 1, lane = lane_id();
-    uint32_t p_nodes = 0, p_edges = 0, p_cells = 0, p_enq = 0;
+    uint32_t p_nodes = 0, p_edges = 0, p_cells = 0;
     if (blockIdx.x < nbh) {  // warp per heavy node
         const uint32_t nw = nbh * (blockDim.x >> 5);
         for (uint32_t n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < g.Vh; n += nw) {
@@ -758,7 +709,6 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_pull(Gr
                 enq = true;
                 id = collect && R::eq(nr, FF) == 0;
                 p_cells += R::ones(found);
-                p_enq++;
             }
             frontier_push(w, enq, s, n, nxt);
             cand_push(g, w, id, s, n, l + 1);
@@ -802,8 +752,7 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_pull(Gr
                         enq = true;
                         id = collect && R::eq(nr, FF) == 0;
                         p_cells += R::ones(found);
-                        p_enq++;
-                    }
+                            }
                 }
             }
             frontier_push(w, enq, s, n, nxt);
@@ -813,12 +762,10 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_pull(Gr
     p_nodes = warp_sum(p_nodes);
     p_edges = warp_sum(p_edges);
     p_cells = warp_sum(p_cells);
-    p_enq = warp_sum(p_enq);
     if (lane == 0 && (p_nodes | p_edges)) {
         atomicAdd(&w.prof[P_PULLNODES], (unsigned long long)p_nodes);
         atomicAdd(&w.prof[P_PULLEDGES], (unsigned long long)p_edges);
         atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
-        atomicAdd(&w.prof[P_ENQ], (unsigned long long)p_enq);
     }
 }
 

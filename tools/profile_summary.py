@@ -63,9 +63,11 @@ if os.path.exists(rep):
             "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
             "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__average_warp_latency_per_inst_issued.ratio",
             "launch__registers_per_thread", "sm__inst_executed.sum", "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum",
-            "l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum"]
+            "l1tex__t_requests_pipe_lsu_mem_global_op_atom.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
+            "lts__t_sectors_op_read.sum", "lts__t_sectors_op_atom.sum", "lts__t_sectors_op_red.sum", "lts__t_sectors_op_write.sum",
+            "smsp__inst_executed.sum", "smsp__sass_inst_executed_op_global_atom.sum"]
     with open(f"profiles/{R}_expand_full_summary.txt", "w") as f:
-        f.write("# ncu --set full --clock-control none -k k_expand -s 17 -c 1 (largest marginal flood level)\n")
+        f.write("# ncu --set full --clock-control none -k regex:k_expand -s <ordinal> -c 1: the longest k_expand launch of the run (marginal flood level), picked from the DRAM pass\n")
         for k in keys:
             if k in hdr:
                 f.write(f"{k} = {d[hdr.index(k)]} {units[hdr.index(k)]}\n")
