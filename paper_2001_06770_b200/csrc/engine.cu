@@ -409,6 +409,53 @@ __device__ __forceinline__ void frontier_push(const WsDev &w, bool want, uint32_
     }
 }
 
+// U pushes per lane at once (the unrolled edges of one chunk, after NR leading retained
+// entries): when every pushing (lane, u) is in one slot, a single queue-counter atomic
+// covers them all.
+template <int U, int NR = 0>
+__device__ __forceinline__ void frontier_push_n(const WsDev &w, const bool (&want)[U], const uint32_t (&s)[U],
+                                                const uint32_t (&entry)[U], uint32_t nxt) {
+    uint32_t m[U], any = 0;
+#pragma unroll
+    for (int u = 0; u < U; u++) any |= (m[u] = __ballot_sync(FULLMASK, want[u]));
+    if (!any) return;
+    int u0 = 0;
+#pragma unroll
+    for (int u = U - 1; u >= 0; u--)
+        if (m[u]) u0 = u;
+    uint32_t s0 = 0;
+#pragma unroll
+    for (int u = 0; u < U; u++)
+        if (u == u0) s0 = __shfl_sync(FULLMASK, s[u], __ffs(m[u]) - 1);
+    bool ok = true;
+#pragma unroll
+    for (int u = 0; u < U; u++) ok &= !want[u] || s[u] == s0;
+    if (__all_sync(FULLMASK, ok)) {
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int u = 0; u < U; u++) cnt += __popc(m[u]);
+        uint32_t base = 0;
+        if (lane_id() == 0) {
+            base = atomicAdd(&w.st[s0].nq[nxt], cnt);
+            uint32_t fresh = cnt;  // new (untagged) entries feed the visited estimate
+#pragma unroll
+            for (int u = 0; u < NR; u++) fresh -= __popc(m[u]);
+            if (w.track_reached && fresh) atomicAdd(&w.st[s0].reached, fresh);
+        }
+        base = __shfl_sync(FULLMASK, base, 0);
+        uint32_t *Qd = w.Q(s0, nxt);
+        const uint32_t lt = lanemask_lt();
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (want[u]) Qd[base + __popc(m[u] & lt)] = entry[u];
+            base += __popc(m[u]);
+        }
+        return;
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) frontier_push(w, want[u], s[u], entry[u], nxt);
+}
+
 __device__ __forceinline__ void cand_push(const GraphDev &g, const WsDev &w, bool want, uint32_t s, uint32_t n,
                                           uint32_t level) {
     uint32_t pos = warp_append(want, s, &w.st[0].ncand, sizeof(SlotState) / 4);
@@ -542,14 +589,16 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
                 }
             }
         }
-        frontier_push(w, retain, s, f | RETAINED, nxt);
         // Edge-parallel walk over the concatenated active ranges, EXP_UNROLL edges per lane in
         // flight.  The non-empty ranges are compacted into s_own (rank order = start order);
         // the owner of edge position p of a 32-wide chunk is found from the bit mask of range
         // starts inside the chunk (one OR-reduction) instead of a per-edge binary search.
         const uint32_t incl = warp_incl_scan(len);
         const uint32_t tot = __shfl_sync(FULLMASK, incl, 31);
-        if (tot == 0) continue;
+        if (tot == 0) {
+            frontier_push(w, retain, s, f | RETAINED, nxt);
+            continue;
+        }  // otherwise the retained entries go out with the first chunk's pushes
         const uint32_t excl = incl - len;
         {
             const uint32_t NE = __ballot_sync(FULLMASK, len > 0);
@@ -588,6 +637,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
             }
 #pragma unroll
             for (int u = 0; u < EXP_UNROLL; u++) hn[u] = ev[u] ? R::load(Hb + (size_t)o_s[u] * V + n[u]) : (RowT)0;
+            bool enq[EXP_UNROLL], idn[EXP_UNROLL];
 #pragma unroll
             for (int u = 0; u < EXP_UNROLL; u++) {
                 Relax<RowT> r{false, false, 0};
@@ -595,10 +645,27 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
                     r = relax<RowT>(HV<RowT>{Hb + (size_t)o_s[u] * V, 1u}, n[u], hn[u], mask[u], l);
                     p_cells += r.cells;
                 }
-                frontier_push(w, r.enq, o_s[u], n[u], nxt);
-                bool id = r.ident && ((s_info[o_s[u]] >> 1) & 1);
-                cand_push(g, w, id, o_s[u], n[u], l + 1);
+                enq[u] = r.enq;
+                idn[u] = r.ident;
             }
+            {
+                bool pw[EXP_UNROLL + 1];
+                uint32_t ps[EXP_UNROLL + 1], pe[EXP_UNROLL + 1];
+                pw[0] = retain;
+                ps[0] = s;
+                pe[0] = f | RETAINED;
+#pragma unroll
+                for (int u = 0; u < EXP_UNROLL; u++) {
+                    pw[u + 1] = enq[u];
+                    ps[u + 1] = o_s[u];
+                    pe[u + 1] = n[u];
+                }
+                frontier_push_n<EXP_UNROLL + 1, 1>(w, pw, ps, pe, nxt);
+                retain = false;
+            }
+#pragma unroll
+            for (int u = 0; u < EXP_UNROLL; u++)
+                cand_push(g, w, idn[u] && ((s_info[o_s[u]] >> 1) & 1), o_s[u], n[u], l + 1);
         }
     }
     p_edges = warp_sum(p_edges);
@@ -639,6 +706,8 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
             }
 #pragma unroll
             for (int u = 0; u < 2; u++) hn[u] = (e0 + 32 * u + lane < h.w) ? R::load(Hs + n[u]) : (RowT)0;
+            bool enq[2], idn[2];
+            const uint32_t ss[2] = {s, s};
 #pragma unroll
             for (int u = 0; u < 2; u++) {
                 Relax<RowT> r{false, false, 0};
@@ -647,9 +716,12 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
                     r = relax<RowT>(HV<RowT>{Hs, 1u}, n[u], hn[u], mask, l);
                     p_cells += r.cells;
                 }
-                frontier_push(w, r.enq, s, n[u], nxt);
-                cand_push(g, w, r.ident && collect, s, n[u], l + 1);
+                enq[u] = r.enq;
+                idn[u] = r.ident;
             }
+            frontier_push_n<2>(w, enq, ss, n, nxt);
+#pragma unroll
+            for (int u = 0; u < 2; u++) cand_push(g, w, idn[u] && collect, s, n[u], l + 1);
         }
     }
     p_cells = warp_sum(p_cells);
@@ -2155,6 +2227,19 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
         if (L.g->profiling) {  // events are read after the batch: no extra sync per level
             CUDA_TRY(cudaEventRecord(ws->event(L.nev++), s));
             L.expand_launches += 2 + (ws->h_ctr[C_NPULL] ? 1 : 0);
+        }
+        static const bool trace_levels = getenv("RIKI_LEVELS") != nullptr;
+        if (trace_levels) {  // diagnostics: per-level frontier / edge / new-cell counts (syncs every level)
+            static unsigned long long last[P_NPROF];
+            unsigned long long pr[P_NPROF];
+            uint32_t c[C_NCTR];
+            CUDA_TRY(cudaMemcpyAsync(c, ws->ctr, sizeof(c), cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(pr, ws->prof, sizeof(pr), cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            if (l == 0) memcpy(last, pr, sizeof(pr));
+            fprintf(stderr, "[riki-level] ph=%d l=%u active=%u items=%u heavy_chunks=%u edges=%llu cells=%llu\n", ph, l,
+                    c[C_ACTIVE], c[C_TOTAL], c[C_NHEAVY], pr[P_EDGES] - last[P_EDGES], pr[P_NEWCELLS] - last[P_NEWCELLS]);
+            memcpy(last, pr, sizeof(pr));
         }
     }
     if (joint) {
