@@ -480,6 +480,28 @@ __device__ __forceinline__ uint32_t lower_bound_act(const uint8_t *act, uint32_t
     return lo;
 }
 
+// Gate ranges of out-row d at level l (activation-sorted row [rb, re)): hi = first edge with
+// a > l, eqlo = first edge with a >= l.  Rows <= 8 edges: byte-SIMD over the packed
+// activations in the descriptor; longer rows: the gate offset table (two loads, one line),
+// binary search only past AOFF_LEVELS.
+__device__ __forceinline__ void gate_range(const GraphDev &g, const uint4 &d, uint32_t l, uint32_t &hi,
+                                           uint32_t &eqlo) {
+    const uint32_t rb = d.x, re = d.x + d.y;
+    if (d.y <= 8) {  // padding 0xFF never passes the gate
+        const uint32_t L4 = l * 0x01010101u;
+        hi = rb + ((__popc(__vcmpleu4(d.z, L4)) + __popc(__vcmpleu4(d.w, L4))) >> 3);
+        eqlo = rb + ((__popc(__vcmpltu4(d.z, L4)) + __popc(__vcmpltu4(d.w, L4))) >> 3);
+    } else if (l < AOFF_LEVELS) {
+        const uint32_t *t = g.aoff + (size_t)d.z * AOFF_LEVELS;
+        hi = __ldg(t + l);
+        eqlo = l ? __ldg(t + l - 1) : rb;
+    } else {
+        const uint32_t b = __ldg(g.aoff + (size_t)d.z * AOFF_LEVELS + AOFF_LEVELS - 1);
+        hi = upper_bound_act(g.act, b, re, l);
+        eqlo = lower_bound_act(g.act, b, hi, l);
+    }
+}
+
 // Work item = one frontier node of one slot.  Each warp takes 32 items: lane i does the
 // per-node part (row bounds, CF check, retention, activation range by binary search in the
 // activation-sorted row), then the warp walks the concatenated active ranges edge-parallel,
@@ -537,24 +559,17 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
             uint32_t ent = w.Q(s, cur)[item - s_offs[s]];
             f = ent & ~RETAINED;
             RowT Rf = R::load(Hb + (size_t)s * V + f);
+            const uint4 d = __ldg(g.desc + f);  // issued with the row load (dropped if dup / blocked)
             RowT used = used_mask<RowT>(info >> 8);
             bool dup = (ent & RETAINED) && (R::eq(Rf, L) & used);
             bool blocked = (info & 1) && R::le(Rf, L) == (RowT)~(RowT)0;  // CF: row complete, max <= l
             if (!dup && !blocked) {
                 newc = R::eq(Rf, L) & used;   // reached at level l (or seeds at l = 0)
                 oldc = R::lt(Rf, L) & used;   // reached earlier: only edges with a == l are due now
-                const uint4 d = __ldg(g.desc + f);
                 const uint32_t rb = d.x, re = d.x + d.y;
                 if (re > rb && (newc | oldc)) {
                     uint32_t hi, eqlo;
-                    if (d.y <= 8) {  // packed activations (padding 0xFF never passes the gate)
-                        const uint32_t L4 = l * 0x01010101u;
-                        hi = rb + ((__popc(__vcmpleu4(d.z, L4)) + __popc(__vcmpleu4(d.w, L4))) >> 3);
-                        eqlo = rb + ((__popc(__vcmpltu4(d.z, L4)) + __popc(__vcmpltu4(d.w, L4))) >> 3);
-                    } else {
-                        hi = upper_bound_act(g.act, rb, re, l);
-                        eqlo = oldc ? lower_bound_act(g.act, rb, hi, l) : hi;
-                    }
+                    gate_range(g, d, l, hi, eqlo);
                     retain = hi < re;  // Alg. 1 lines 9-11: some a_fn > l keeps f a frontier
                     lo = newc ? rb : eqlo;
                     eq0 = eqlo;
@@ -945,17 +960,7 @@ __global__ void __launch_bounds__(256) k_jexpand(GraphDev g, WsDev w, int ph, ui
             p_items++;
             const uint4 d = __ldg(g.desc + f);
             const uint32_t rb = d.x, re = d.x + d.y;
-            if (d.y <= 8) {
-                hi = rb + ((__popc(__vcmpleu4(d.z, L)) + __popc(__vcmpleu4(d.w, L))) >> 3);
-                eqlo = rb + ((__popc(__vcmpltu4(d.z, L)) + __popc(__vcmpltu4(d.w, L))) >> 3);
-            } else {
-                if (lane == 0) {
-                    hi = upper_bound_act(g.act, rb, re, l);
-                    eqlo = lower_bound_act(g.act, rb, hi, l);
-                }
-                hi = __shfl_sync(FULLMASK, hi, 0);
-                eqlo = __shfl_sync(FULLMASK, eqlo, 0);
-            }
+            gate_range(g, d, l, hi, eqlo);
             lo = any_new ? rb : eqlo;
             // per-slot relaxation counts and retention (Alg. 1 lines 9-11)
             bool retain_any = false;

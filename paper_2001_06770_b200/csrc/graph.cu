@@ -125,7 +125,16 @@ __global__ void k_gather_in(const uint64_t *key, const uint32_t *eid, const uint
 // Node descriptor: one 16-byte load gives the row start, the degree and, for rows of at most
 // 8 edges, all their (sorted) activations packed in bytes (padding 0xFF), so the expansion
 // finds the gate ranges a <= l / a == l with byte-SIMD compares instead of a binary search.
-__global__ void k_desc(const uint32_t *row, const uint8_t *act, uint32_t V, uint4 *desc) {
+// Longer rows get a slot in the gate offset table (AOFF_LEVELS entries, see internal.cuh).
+__device__ __forceinline__ uint32_t ub_act(const uint8_t *act, uint32_t lo, uint32_t hi, uint32_t k) {
+    while (lo < hi) {  // first index with act > k
+        uint32_t m = (lo + hi) >> 1;
+        if (act[m] <= k) lo = m + 1; else hi = m;
+    }
+    return lo;
+}
+__global__ void k_desc(const uint32_t *row, const uint8_t *act, uint32_t V, uint4 *desc, uint32_t *aoff,
+                       uint32_t *ncnt) {
     for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
         uint32_t rb = row[v], deg = row[v + 1] - rb;
         uint32_t lo = 0xFFFFFFFFu, hi = 0xFFFFFFFFu;
@@ -135,9 +144,19 @@ __global__ void k_desc(const uint32_t *row, const uint8_t *act, uint32_t V, uint
                 if (i < 4) lo = (lo & ~(0xFFu << (8 * i))) | (b << (8 * i));
                 else hi = (hi & ~(0xFFu << (8 * (i - 4)))) | (b << (8 * (i - 4)));
             }
+        } else {
+            lo = atomicAdd(ncnt, 1u);  // table slot (any order: only the mapping matters)
+            hi = 0;
+            uint32_t *t = aoff + (size_t)lo * AOFF_LEVELS;
+            uint32_t b = rb;
+            for (uint32_t k = 0; k < AOFF_LEVELS; k++) t[k] = b = ub_act(act, b, rb + deg, k);
         }
         desc[v] = make_uint4(rb, deg, lo, hi);
     }
+}
+__global__ void k_count_long_rows(const uint32_t *row, uint32_t V, uint32_t *cnt) {
+    for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x)
+        if (row[v + 1] - row[v] > 8) atomicAdd(cnt, 1u);
 }
 
 // Node relabeling for L2 locality: internal id = rank by total degree (descending, then
@@ -205,7 +224,13 @@ void build_csr(riki_graph *g) {
     k_act_keys<<<grid_for(E), 256, 0, s>>>(g->d_src, g->d_act_e, E, keys, vals);
     sort_pairs(s, keys, vals, E, eb);
     k_gather_out<<<grid_for(E), 256, 0, s>>>(keys, vals, g->d_dst, E, g->d_col, g->d_act);
-    k_desc<<<grid_for(g->V), 256, 0, s>>>(g->d_row, g->d_act, g->V, g->d_desc);
+    {
+        uint32_t *ncnt = dmalloc<uint32_t>(1);
+        CUDA_TRY(cudaMemsetAsync(ncnt, 0, 4, s));
+        k_desc<<<grid_for(g->V), 256, 0, s>>>(g->d_row, g->d_act, g->V, g->d_desc, g->d_aoff, ncnt);
+        sync_check(s);
+        cudaFree(ncnt);
+    }
     // in-CSR
     k_act_keys<<<grid_for(E), 256, 0, s>>>(g->d_dst, g->d_act_e, E, keys, vals);
     sort_pairs(s, keys, vals, E, eb);
@@ -317,12 +342,21 @@ void graph_load(riki_graph *g, uint32_t V, uint64_t E, const uint32_t *src, cons
     }
     row_pointers(s, g->d_src, E, V, g->d_row);
     row_pointers(s, g->d_dst, E, V, g->d_irow);
+    {   // gate offset table for out-rows longer than 8 edges
+        uint32_t *cnt = dmalloc<uint32_t>(1);
+        CUDA_TRY(cudaMemsetAsync(cnt, 0, 4, s));
+        k_count_long_rows<<<grid_for(V), 256, 0, s>>>(g->d_row, V, cnt);
+        CUDA_TRY(cudaMemcpyAsync(&g->n_aoff, cnt, 4, cudaMemcpyDeviceToHost, s));
+        sync_check(s);
+        cudaFree(cnt);
+        g->d_aoff = dmalloc<uint32_t>((size_t)std::max<uint32_t>(g->n_aoff, 1) * AOFF_LEVELS, acc);
+    }
     sync_check(s);
 }
 
 void graph_free(riki_graph *g) {
     void *ps[] = {g->d_src, g->d_dst, g->d_cls, g->d_act_e, g->d_row, g->d_col, g->d_act, g->d_desc,
-                  g->d_irow, g->d_isrc, g->d_ieid, g->d_iact, g->d_tptr, g->d_post, g->d_perm, g->d_iperm};
+                  g->d_irow, g->d_isrc, g->d_ieid, g->d_iact, g->d_tptr, g->d_post, g->d_perm, g->d_iperm, g->d_aoff};
     for (void *p : ps) if (p) cudaFree(p);
     if (g->stream) cudaStreamDestroy(g->stream);
 }

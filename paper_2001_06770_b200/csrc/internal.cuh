@@ -14,12 +14,19 @@ struct Workspace;  // engine.cu
 // ascending (then by edge id), so the Alg. 1 gate a <= l reads a row prefix.  In-rows
 // (Alg. 2 line 5, N_i) are sorted the same way and carry the forward edge's activation
 // and the caller's edge id.
+// Gate offset table: for out-rows longer than 8 edges (activation-sorted), entry k is the index
+// of the first edge with activation > k, k < AOFF_LEVELS: the expansion's gate ranges a <= l and
+// a == l are two loads from one 64-byte line instead of two binary searches.
+#define AOFF_LEVELS 16
+
 struct GraphDev {
     uint32_t V;
     uint64_t E;
     const uint32_t *row, *col;  // out-CSR
     const uint8_t *act;
-    const uint4 *desc;          // per node: {row start, degree, packed activations of rows <= 8 edges}
+    const uint4 *desc;          // per node: {row start, degree, packed activations of rows <= 8 edges
+                                //            | index into aoff for longer rows}
+    const uint32_t *aoff;       // per row of > 8 edges: AOFF_LEVELS gate offsets (first edge with a > k)
     const uint32_t *irow, *isrc, *ieid;  // in-CSR
     const uint8_t *iact;
     const uint32_t *src, *dst;  // caller's edge list by edge id
@@ -41,6 +48,8 @@ struct riki_graph {
     uint32_t *d_row = nullptr, *d_col = nullptr;
     uint8_t *d_act = nullptr;
     uint4 *d_desc = nullptr;
+    uint32_t *d_aoff = nullptr;  // AOFF_LEVELS entries per out-row of more than 8 edges
+    uint32_t n_aoff = 0;         // number of such rows
     uint32_t *d_irow = nullptr, *d_isrc = nullptr, *d_ieid = nullptr;
     uint8_t *d_iact = nullptr;
     uint64_t *d_tptr = nullptr;
@@ -57,7 +66,7 @@ struct riki_graph {
     GraphDev dev() const {
         GraphDev g;
         g.V = V; g.E = E;
-        g.row = d_row; g.col = d_col; g.act = d_act; g.desc = d_desc;
+        g.row = d_row; g.col = d_col; g.act = d_act; g.desc = d_desc; g.aoff = d_aoff;
         g.irow = d_irow; g.isrc = d_isrc; g.ieid = d_ieid; g.iact = d_iact;
         g.src = d_src; g.dst = d_dst; g.tptr = d_tptr; g.post = d_post; g.perm = d_perm; g.iperm = d_iperm; g.Vh = Vh;
         return g;

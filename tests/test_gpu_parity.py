@@ -87,6 +87,42 @@ def test_hitting_levels_random(P, seed):
         assert L == Lo and rel == relo
 
 
+@pytest.mark.parametrize("seed", range(12))
+def test_hitting_levels_long_rows_high_activations(P, seed):
+    """Rows longer than 8 edges with activations past the gate offset table (a >= 16): the table
+    lookup and the binary search above it must give the oracle's hitting levels (Alg. 1 gate)."""
+    rng = np.random.default_rng(3500 + seed)
+    V, src, dst, act, terms = random_instance(rng, 20, 160, deg=14.0, amax=40, T_hi=5, post_hi=4)
+    g = _dev_graph(P, V, src, dst, act, terms)
+    og = O.Graph(V, src, dst, act)
+    T = len(terms)
+    for D in (7, 17, 60):
+        for mode in (0, 1, 2):
+            H, blk, rel, L = g.hitting_levels(np.arange(T, dtype=np.uint32), D, mode)
+            Ho, bo, Lo, relo = O.phase(og, terms, D, mode)
+            assert (H == Ho).all(), (D, mode, np.argwhere(H != Ho)[:5])
+            assert (blk == bo).all() and L == Lo and rel == relo
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_search_long_rows_high_activations(P, seed):
+    rng = np.random.default_rng(5500 + seed)
+    V, src, dst, act, _ = random_instance(rng, 30, 120, deg=12.0, amax=30)
+    nterm = 8
+    post = [np.unique(rng.integers(0, V, int(rng.integers(1, 4)))).astype(np.uint32) for _ in range(nterm)]
+    g = _dev_graph(P, V, src, dst, act, post)
+    og = O.Graph(V, src, dst, act)
+    for _ in range(3):
+        nc = int(rng.integers(1, 3))
+        nm = int(rng.integers(1, 3))
+        tt = rng.choice(nterm, nc + nm, replace=False)
+        C, M = tt[:nc], tt[nc:]
+        r = g.search(C, M, 5, 60)
+        ro = _oracle_run(og, lambda t: post[t], C, M, 5, 60)
+        _cmp_results(r, ro)
+        assert r.stats["relax_central"] == ro.relax_c and r.stats["relax_marginal"] == ro.relax_m
+
+
 def test_hitting_levels_c1_all_terms(P):
     kg = synth.make_kg(1)
     g = P.Graph(kg.n_nodes, kg.src, kg.dst, kg.label_class, kg.term_ptr, kg.postings)
