@@ -7,6 +7,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import re
+from collections.abc import Sequence
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -44,6 +45,15 @@ class QueryStats(C.Structure):
     _fields_ = [("L_central", C.c_int32), ("L_marginal", C.c_int32), ("n_candidates", C.c_uint32),
                 ("n_attached", C.c_uint32), ("n_ptc_fail", C.c_uint32), ("relax_central", C.c_uint64),
                 ("relax_marginal", C.c_uint64)]
+
+
+# numpy view of QueryStats (same layout as the C struct, checked at import)
+_STATS_DT = np.dtype([(f, np.dtype(t)) for f, t in (("L_central", np.int32), ("L_marginal", np.int32),
+                                                    ("n_candidates", np.uint32), ("n_attached", np.uint32),
+                                                    ("n_ptc_fail", np.uint32), ("relax_central", np.uint64),
+                                                    ("relax_marginal", np.uint64))], align=True)
+assert _STATS_DT.itemsize == C.sizeof(QueryStats) and all(
+    _STATS_DT.fields[f][1] == getattr(QueryStats, f).offset for f, _ in QueryStats._fields_)
 
 
 class ExportSizes(C.Structure):
@@ -173,8 +183,57 @@ def _take_results(lib, h, nc, nm) -> Result:
         lib.riki_results_free(h)
 
 
-def _take_batch(lib, hs, n, ncs, nms) -> list:
-    """Bulk export of n result handles (one C call), then free them."""
+class BatchResult(Sequence):
+    """Results of a batch in columnar form (what riki_results_export fills): per-query RPG
+    counts, RPG headers / scores and the concatenated node, edge, V_C and distance arrays.
+    Behaves as a read-only list of Result; a query's Result is built on first access."""
+
+    def __init__(self, n, ncs, nms, cnt, hdr, score, nodes, edges, vc, cd, md, stats):
+        self.n, self.ncs, self.nms = n, ncs, nms
+        self.cnt, self.hdr, self.score = cnt, hdr, score
+        self.nodes, self.edges, self.vc, self.cd, self.md = nodes, edges, vc, cd, md
+        self.stats = stats  # numpy structured array (QueryStats fields)
+        self.rpg_off = np.zeros(n + 1, np.int64)
+        np.cumsum(cnt, out=self.rpg_off[1:])
+        nrpg = int(self.rpg_off[-1])
+        self.node_off = np.zeros(nrpg + 1, np.int64)
+        self.edge_off = np.zeros(nrpg + 1, np.int64)
+        self.vc_off = np.zeros(nrpg + 1, np.int64)
+        if nrpg:
+            np.cumsum(hdr[:nrpg, 4], out=self.node_off[1:])
+            np.cumsum(hdr[:nrpg, 5], out=self.edge_off[1:])
+            np.cumsum(hdr[:nrpg, 6], out=self.vc_off[1:])
+        self._cache = {}
+
+    def __len__(self):
+        return self.n
+
+    def _build(self, i):
+        rp = []
+        for r in range(int(self.rpg_off[i]), int(self.rpg_off[i + 1])):
+            h = self.hdr[r]
+            rp.append(RPG(int(h[0]), int(h[1]), int(h[2]), float(self.score[r]), int(h[3]),
+                          self.nodes[self.node_off[r]:self.node_off[r + 1]],
+                          self.edges[self.edge_off[r]:self.edge_off[r + 1]],
+                          self.vc[self.vc_off[r]:self.vc_off[r + 1]],
+                          self.cd[r, :self.ncs[i]], self.md[r, :self.nms[i]]))
+        st = self.stats[i]
+        return Result(rp, {f: int(st[f]) for f in self.stats.dtype.names})
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[j] for j in range(*i.indices(self.n))]
+        if i < 0:
+            i += self.n
+        if not 0 <= i < self.n:
+            raise IndexError(i)
+        if i not in self._cache:
+            self._cache[i] = self._build(i)
+        return self._cache[i]
+
+
+def _take_batch(lib, hs, n, ncs, nms) -> BatchResult:
+    """Bulk export of n result handles (one C call into preallocated arrays), then free them."""
     try:
         z = ExportSizes()
         _check(lib.riki_results_export_sizes(C.cast(hs, C.c_void_p), n, C.byref(z)))
@@ -186,23 +245,10 @@ def _take_batch(lib, hs, n, ncs, nms) -> list:
         vc = np.zeros(max(z.n_vc, 1), np.uint32)
         cd = np.zeros((max(z.n_rpg, 1), 8), np.uint8)
         md = np.zeros((max(z.n_rpg, 1), 8), np.uint8)
-        stats = (QueryStats * max(n, 1))()
+        stats = np.zeros(max(n, 1), dtype=_STATS_DT)
         _check(lib.riki_results_export(C.cast(hs, C.c_void_p), n, _p(cnt), _p(hdr), _p(score), _p(nodes), _p(edges),
-                                       _p(vc), _p(cd), _p(md), C.cast(stats, C.c_void_p)))
-        out = []
-        r = on = oe = ov = 0
-        names = [f for f, _ in QueryStats._fields_]
-        for i in range(n):
-            rp = []
-            for _ in range(int(cnt[i])):
-                h = hdr[r]
-                a, b, c = int(h[4]), int(h[5]), int(h[6])
-                rp.append(RPG(int(h[0]), int(h[1]), int(h[2]), float(score[r]), int(h[3]), nodes[on:on + a],
-                              edges[oe:oe + b], vc[ov:ov + c], cd[r, :ncs[i]], md[r, :nms[i]]))
-                on += a; oe += b; ov += c; r += 1
-            st = stats[i]
-            out.append(Result(rp, {f: getattr(st, f) for f in names}))
-        return out
+                                       _p(vc), _p(cd), _p(md), C.c_void_p(stats.ctypes.data)))
+        return BatchResult(n, list(ncs), list(nms), cnt, hdr, score, nodes, edges, vc, cd, md, stats[:n])
     finally:
         for i in range(n):
             lib.riki_results_free(C.c_void_p(hs[i]))
