@@ -45,7 +45,7 @@ constexpr uint32_t SORT_SMEM = 8192;  // u32 keys sorted in shared memory
 enum Ctr { C_NHEAVY = 0, C_NNEWATT, C_NOVF, C_ACTIVE, C_TOTAL, C_NCAND_TOTAL, C_NOVF2, C_NPULL, C_JQN0, C_JQN1,
            C_JQCUR, C_JHEAVY, C_NCTR = 16 };
 enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_PULLNODES, P_PULLEDGES, P_NPROF = 8 };
-enum Err { E_CAND = 1, E_HEAVY = 2, E_ARENA = 4, E_EXTRACT = 8, E_OUT = 16, E_UNRESOLVED = 32 };
+enum Err { E_CAND = 1, E_HEAVY = 2, E_ARENA = 4, E_EXTRACT = 8, E_OUT = 16, E_UNRESOLVED = 32, E_QUEUE = 64 };
 
 struct SlotState {
     uint32_t T[2];
@@ -94,6 +94,7 @@ struct WsDev {
     uint8_t *H[2];
     uint32_t rb[2];
     uint32_t *q, *bm;
+    uint32_t qcap;  // entries per level queue: V, or 2V after an overflow (a node can be retained and new)
     uint32_t *jq, *jbm;  // joint traversal: union frontier queues [2][V] and bit-packed flags [2][W]
     uint64_t *ck;
     Cand *cd;
@@ -116,7 +117,7 @@ struct WsDev {
     uint32_t *out;
     unsigned long long *out_used, out_cap;
 
-    __device__ __forceinline__ uint32_t *Q(uint32_t s, uint32_t b) const { return q + ((size_t)s * 2 + b) * V; }
+    __device__ __forceinline__ uint32_t *Q(uint32_t s, uint32_t b) const { return q + ((size_t)s * 2 + b) * qcap; }
     __device__ __forceinline__ uint32_t *JQ(uint32_t b) const { return jq + (size_t)b * V; }
     __device__ __forceinline__ uint32_t *JBM(uint32_t b) const { return jbm + (size_t)b * W; }
     uint32_t hnode, SP;  // H layout: 0 slot-major, 1 node-major with SP (padded) slots per node
@@ -392,6 +393,10 @@ __device__ __forceinline__ void frontier_push(const WsDev &w, bool want, uint32_
             if (w.track_reached && !(entry & RETAINED)) atomicAdd(&w.st[s0].reached, __popc(m));
         }
         base = __shfl_sync(FULLMASK, base, leader);
+        if (base + __popc(m) > w.qcap) {  // more entries than the queue holds: flag, retry bigger
+            if (lane_id() == leader) atomicOr(&w.st[s0].err, (uint32_t)E_QUEUE);
+            return;
+        }
         if (want) w.Q(s0, nxt)[base + __popc(m & lanemask_lt())] = entry;
         return;
     }
@@ -405,7 +410,11 @@ __device__ __forceinline__ void frontier_push(const WsDev &w, bool want, uint32_
             if (w.track_reached && !(entry & RETAINED)) atomicAdd(&w.st[s].reached, __popc(peers));
         }
         base = __shfl_sync(peers, base, leader);
-        w.Q(s, nxt)[base + rank] = entry;
+        if (base + __popc(peers) > w.qcap) {
+            if (lane_id() == leader) atomicOr(&w.st[s].err, (uint32_t)E_QUEUE);
+        } else {
+            w.Q(s, nxt)[base + rank] = entry;
+        }
     }
 }
 
@@ -443,6 +452,10 @@ __device__ __forceinline__ void frontier_push_n(const WsDev &w, const bool (&wan
             if (w.track_reached && fresh) atomicAdd(&w.st[s0].reached, fresh);
         }
         base = __shfl_sync(FULLMASK, base, 0);
+        if (base + cnt > w.qcap) {
+            if (lane_id() == 0) atomicOr(&w.st[s0].err, (uint32_t)E_QUEUE);
+            return;
+        }
         uint32_t *Qd = w.Q(s0, nxt);
         const uint32_t lt = lanemask_lt();
 #pragma unroll
@@ -484,22 +497,28 @@ __device__ __forceinline__ uint32_t lower_bound_act(const uint8_t *act, uint32_t
 // a > l, eqlo = first edge with a >= l.  Rows <= 8 edges: byte-SIMD over the packed
 // activations in the descriptor; longer rows: the gate offset table (two loads, one line),
 // binary search only past AOFF_LEVELS.
-__device__ __forceinline__ void gate_range(const GraphDev &g, const uint4 &d, uint32_t l, uint32_t &hi,
-                                           uint32_t &eqlo) {
+__device__ __forceinline__ void gate_range_t(const uint8_t *act, const uint32_t *aoff, const uint4 &d, uint32_t l,
+                                             uint32_t &hi, uint32_t &eqlo) {
     const uint32_t rb = d.x, re = d.x + d.y;
     if (d.y <= 8) {  // padding 0xFF never passes the gate
         const uint32_t L4 = l * 0x01010101u;
         hi = rb + ((__popc(__vcmpleu4(d.z, L4)) + __popc(__vcmpleu4(d.w, L4))) >> 3);
         eqlo = rb + ((__popc(__vcmpltu4(d.z, L4)) + __popc(__vcmpltu4(d.w, L4))) >> 3);
     } else if (l < AOFF_LEVELS) {
-        const uint32_t *t = g.aoff + (size_t)d.z * AOFF_LEVELS;
+        const uint32_t *t = aoff + (size_t)d.z * AOFF_LEVELS;
         hi = __ldg(t + l);
         eqlo = l ? __ldg(t + l - 1) : rb;
     } else {
-        const uint32_t b = __ldg(g.aoff + (size_t)d.z * AOFF_LEVELS + AOFF_LEVELS - 1);
-        hi = upper_bound_act(g.act, b, re, l);
-        eqlo = lower_bound_act(g.act, b, hi, l);
+        const uint32_t b = __ldg(aoff + (size_t)d.z * AOFF_LEVELS + AOFF_LEVELS - 1);
+        hi = upper_bound_act(act, b, re, l);
+        eqlo = lower_bound_act(act, b, hi, l);
     }
+}
+__device__ __forceinline__ void gate_range(const GraphDev &g, const uint4 &d, uint32_t l, uint32_t &hi, uint32_t &eqlo) {
+    gate_range_t(g.act, g.aoff, d, l, hi, eqlo);
+}
+__device__ __forceinline__ void gate_range_in(const GraphDev &g, const uint4 &d, uint32_t l, uint32_t &hi, uint32_t &eqlo) {
+    gate_range_t(g.iact, g.iaoff, d, l, hi, eqlo);
 }
 
 // Work item = one frontier node of one slot.  Each warp takes 32 items: lane i does the
@@ -704,6 +723,8 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
     for (uint32_t it = gw; it < nh; it += nw) {
         uint4 h = w.heavy[it];
         uint32_t s = h.x;
+        // after an overflow (E_HEAVY, fatal) entries past the last write are stale: stay in bounds
+        if (s >= w.nslots || h.y >= w.V || h.z > h.w || h.w > g.E) continue;
         const SlotState &st = w.st[s];
         RowT used = used_mask<RowT>(st.T[ph]);
         RowT *const Hs = (RowT *)w.H[ph] + (size_t)s * w.V;  // slot-major (never joint here)
@@ -1253,10 +1274,10 @@ __device__ void dag_list(const GraphDev &g, const WsDev &w, uint32_t s, int ph, 
         return;
     }
     slot = __shfl_sync(FULLMASK, slot, 0);
-    uint32_t rb = __ldg(g.irow + q), re = __ldg(g.irow + q + 1);
-    uint32_t hi = 0;
-    if (lane == 0) hi = upper_bound_act(g.iact, rb, re, hq - 1);  // in-rows are activation-sorted
-    hi = __shfl_sync(FULLMASK, hi, 0);
+    const uint4 d = __ldg(g.idesc + q);  // in-rows are activation-sorted: gate a <= hq - 1
+    const uint32_t rb = d.x;
+    uint32_t hi, eqlo;
+    gate_range_in(g, d, hq - 1, hi, eqlo);
     uint32_t off = 0;
     if (lane == 0) {
         unsigned long long p = atomicAdd(w.arena_used, 3ull * (hi - rb));
@@ -1964,6 +1985,7 @@ struct Workspace {
     uint32_t slots = 0, V = 0, W = 0, capc = 0, kmax = 0, heavy_cap = 0, ovf_cap = 0, big_ctas = 0;
     uint64_t arena_cap = 0, out_cap = 0, big_words = 0;
     uint8_t *H[2] = {nullptr, nullptr};
+    uint32_t qcap = 0;  // entries per level queue
     uint32_t *q = nullptr, *bm = nullptr, *jq = nullptr, *jbm = nullptr, *offs = nullptr, *coffs = nullptr, *pslots = nullptr, *ctr = nullptr, *arena = nullptr,
              *big = nullptr, *resid = nullptr, *out = nullptr;
     uint4 *mtab = nullptr;
@@ -2021,7 +2043,7 @@ struct Workspace {
         WsDev d;
         d.st = st; d.nslots = cur ? cur : slots; d.V = V; d.W = W; d.capc = capc; d.kmax = kmax;
         d.H[0] = H[0]; d.H[1] = H[1]; d.hnode = hnode; d.SP = SP; d.rb[0] = last_rb[0]; d.rb[1] = last_rb[1];
-        d.q = q; d.bm = bm; d.jq = jq; d.jbm = jbm; d.ck = ck; d.cd = cd; d.rk = rk; d.offs = offs; d.coffs = coffs; d.pslots = pslots; d.track_reached = track_reached;
+        d.q = q; d.qcap = qcap; d.bm = bm; d.jq = jq; d.jbm = jbm; d.ck = ck; d.cd = cd; d.rk = rk; d.offs = offs; d.coffs = coffs; d.pslots = pslots; d.track_reached = track_reached;
         d.heavy = heavy; d.heavy_cap = heavy_cap; d.ctr = ctr; d.prof = prof;
         d.arena = arena; d.arena_used = arena_used; d.arena_cap = arena_cap;
         d.newatt = newatt; d.ovf = ovf; d.ovf2 = ovf2; d.ovf_cap = ovf_cap;
@@ -2053,7 +2075,7 @@ struct Tracer {  // RIKI_TRACE=<ms>: print the stage times of calls slower than 
 };
 
 struct Caps {
-    uint32_t slots, capc, kmax;
+    uint32_t slots, capc, kmax, qcap;
     uint64_t arena, out;
     uint32_t rb[2];  // bytes per H row needed by each run
 };
@@ -2061,7 +2083,8 @@ struct Caps {
 void ensure_workspace(riki_graph *g, const Caps &c) {
     Workspace *ws = g->ws;
     if (ws && ws->slots >= c.slots && ws->V == g->V && ws->capc >= c.capc && ws->kmax >= c.kmax &&
-        ws->arena_cap >= c.arena && ws->out_cap >= c.out && ws->hcap[0] >= c.rb[0] && ws->hcap[1] >= c.rb[1])
+        ws->arena_cap >= c.arena && ws->out_cap >= c.out && ws->hcap[0] >= c.rb[0] && ws->hcap[1] >= c.rb[1] &&
+        ws->qcap >= c.qcap)
         return;
     uint32_t hb0 = std::max<uint32_t>(c.rb[0], ws ? ws->hcap[0] : 0), hb1 = std::max<uint32_t>(c.rb[1], ws ? ws->hcap[1] : 0);
     if (ws) { ws->release(); delete ws; g->ws = nullptr; }
@@ -2077,7 +2100,8 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     const size_t S8 = (S + 7) & ~(size_t)7;  // node-major layout pads slots to a multiple of 8
     ws->H[0] = ws->alloc<uint8_t>(S8 * V * hb0);
     ws->H[1] = ws->alloc<uint8_t>(S8 * V * hb1);
-    ws->q = ws->alloc<uint32_t>(S * 2 * V);
+    ws->qcap = c.qcap;
+    ws->q = ws->alloc<uint32_t>(S * 2 * (size_t)c.qcap);
     ws->jq = ws->alloc<uint32_t>(2 * (size_t)V);
     ws->jbm = ws->alloc<uint32_t>(2 * (size_t)ws->W);
     CUDA_TRY(cudaMemset(ws->jbm, 0, 2 * (size_t)ws->W * 4));
@@ -2446,6 +2470,7 @@ std::string err_text(uint32_t e) {
     if (e & E_EXTRACT) m += " recovery-scratch";
     if (e & E_OUT) m += " output";
     if (e & E_UNRESOLVED) m += " unresolved-term";
+    if (e & E_QUEUE) m += " frontier-queue";
     return m;
 }
 
@@ -2472,6 +2497,7 @@ void run_with_retry(riki_graph *g, Launch &L, uint32_t depth, Caps &caps, uint32
         if (err & E_CAND) caps.capc = std::min<uint32_t>(caps.capc * 4, next_pow2(g->V + 1));
         if (err & (E_ARENA | E_EXTRACT)) caps.arena *= 4;
         if (err & E_OUT) caps.out *= 4;
+        if (err & E_QUEUE) caps.qcap = 2 * g->V;  // exact bound: one retained + one new entry per node
         if (err & E_HEAVY) RIKI_THROW(RIKI_ENOMEM, "heavy work queue overflow");
     }
 }
@@ -2538,6 +2564,7 @@ static Caps initial_caps(riki_graph *g, uint32_t nq, uint32_t k, uint32_t rb0, u
     c.arena = std::max<uint64_t>(64ull << 20, g->ws ? g->ws->arena_cap : 0);
     c.out = std::max<uint64_t>(16ull << 20, g->ws ? g->ws->out_cap : 0);
     if (g->ws) c.capc = std::max(c.capc, g->ws->capc);
+    c.qcap = std::max<uint32_t>(g->V, g->ws ? g->ws->qcap : 0);
     return c;
 }
 
@@ -2677,6 +2704,7 @@ void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uin
     for (uint32_t j = 0; j < T; j++) q.c[j] = terms[j];
     check_query_host(g, q);
     Caps caps = initial_caps(g, 1, 1, row_bytes(T), 2);
+    for (int attempt = 0;; attempt++) {  // grows the frontier queues on E_QUEUE (see run_with_retry)
     ensure_workspace(g, caps);
     Workspace *ws = g->ws;
     ws->last_rb[0] = row_bytes(T);
@@ -2716,6 +2744,13 @@ void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uin
         SlotState s0;
         CUDA_TRY(cudaMemcpyAsync(&s0, ws->st, sizeof(SlotState), cudaMemcpyDeviceToHost, L.s));
         CUDA_TRY(cudaStreamSynchronize(L.s));
+        if ((s0.err & E_QUEUE) && caps.qcap < 2 * g->V && attempt < 2) {
+            caps.qcap = 2 * g->V;
+            g->stats.retries++;
+            cudaFree(dH);
+            cudaFree(dB);
+            continue;
+        }
         if (s0.err) RIKI_THROW(RIKI_ENOMEM, "workspace overflow:" + err_text(s0.err));
         if (relax_out) *relax_out = s0.relax[0];
         if (L_out) *L_out = s0.L_end[0];
@@ -2727,6 +2762,8 @@ void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uin
     }
     cudaFree(dH);
     cudaFree(dB);
+    return;
+    }
 }
 
 void engine_free(riki_graph *g) {

@@ -235,6 +235,13 @@ void build_csr(riki_graph *g) {
     k_act_keys<<<grid_for(E), 256, 0, s>>>(g->d_dst, g->d_act_e, E, keys, vals);
     sort_pairs(s, keys, vals, E, eb);
     k_gather_in<<<grid_for(E), 256, 0, s>>>(keys, vals, g->d_src, E, g->d_isrc, g->d_ieid, g->d_iact);
+    {
+        uint32_t *ncnt = dmalloc<uint32_t>(1);
+        CUDA_TRY(cudaMemsetAsync(ncnt, 0, 4, s));
+        k_desc<<<grid_for(g->V), 256, 0, s>>>(g->d_irow, g->d_iact, g->V, g->d_idesc, g->d_iaoff, ncnt);
+        sync_check(s);
+        cudaFree(ncnt);
+    }
     sync_check(s);
     cudaFree(keys);
     cudaFree(vals);
@@ -348,15 +355,21 @@ void graph_load(riki_graph *g, uint32_t V, uint64_t E, const uint32_t *src, cons
         k_count_long_rows<<<grid_for(V), 256, 0, s>>>(g->d_row, V, cnt);
         CUDA_TRY(cudaMemcpyAsync(&g->n_aoff, cnt, 4, cudaMemcpyDeviceToHost, s));
         sync_check(s);
-        cudaFree(cnt);
         g->d_aoff = dmalloc<uint32_t>((size_t)std::max<uint32_t>(g->n_aoff, 1) * AOFF_LEVELS, acc);
+        CUDA_TRY(cudaMemsetAsync(cnt, 0, 4, s));
+        k_count_long_rows<<<grid_for(V), 256, 0, s>>>(g->d_irow, V, cnt);
+        CUDA_TRY(cudaMemcpyAsync(&g->n_iaoff, cnt, 4, cudaMemcpyDeviceToHost, s));
+        sync_check(s);
+        g->d_iaoff = dmalloc<uint32_t>((size_t)std::max<uint32_t>(g->n_iaoff, 1) * AOFF_LEVELS, acc);
+        g->d_idesc = dmalloc<uint4>(V, acc);
+        cudaFree(cnt);
     }
     sync_check(s);
 }
 
 void graph_free(riki_graph *g) {
     void *ps[] = {g->d_src, g->d_dst, g->d_cls, g->d_act_e, g->d_row, g->d_col, g->d_act, g->d_desc,
-                  g->d_irow, g->d_isrc, g->d_ieid, g->d_iact, g->d_tptr, g->d_post, g->d_perm, g->d_iperm, g->d_aoff};
+                  g->d_irow, g->d_isrc, g->d_ieid, g->d_iact, g->d_tptr, g->d_post, g->d_perm, g->d_iperm, g->d_aoff, g->d_idesc, g->d_iaoff};
     for (void *p : ps) if (p) cudaFree(p);
     if (g->stream) cudaStreamDestroy(g->stream);
 }

@@ -29,6 +29,8 @@ struct GraphDev {
     const uint32_t *aoff;       // per row of > 8 edges: AOFF_LEVELS gate offsets (first edge with a > k)
     const uint32_t *irow, *isrc, *ieid;  // in-CSR
     const uint8_t *iact;
+    const uint4 *idesc;         // in-rows: same layout as desc
+    const uint32_t *iaoff;      // in-rows of > 8 edges: gate offsets
     const uint32_t *src, *dst;  // caller's edge list by edge id
     const uint64_t *tptr;       // inverted index (internal ids)
     const uint32_t *post;
@@ -50,6 +52,9 @@ struct riki_graph {
     uint4 *d_desc = nullptr;
     uint32_t *d_aoff = nullptr;  // AOFF_LEVELS entries per out-row of more than 8 edges
     uint32_t n_aoff = 0;         // number of such rows
+    uint4 *d_idesc = nullptr;    // in-CSR descriptors and gate offsets (recovery, pull)
+    uint32_t *d_iaoff = nullptr;
+    uint32_t n_iaoff = 0;
     uint32_t *d_irow = nullptr, *d_isrc = nullptr, *d_ieid = nullptr;
     uint8_t *d_iact = nullptr;
     uint64_t *d_tptr = nullptr;
@@ -66,7 +71,7 @@ struct riki_graph {
     GraphDev dev() const {
         GraphDev g;
         g.V = V; g.E = E;
-        g.row = d_row; g.col = d_col; g.act = d_act; g.desc = d_desc; g.aoff = d_aoff;
+        g.row = d_row; g.col = d_col; g.act = d_act; g.desc = d_desc; g.aoff = d_aoff; g.idesc = d_idesc; g.iaoff = d_iaoff;
         g.irow = d_irow; g.isrc = d_isrc; g.ieid = d_ieid; g.iact = d_iact;
         g.src = d_src; g.dst = d_dst; g.tptr = d_tptr; g.post = d_post; g.perm = d_perm; g.iperm = d_iperm; g.Vh = Vh;
         return g;
