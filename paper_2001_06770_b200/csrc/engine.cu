@@ -44,7 +44,13 @@ constexpr uint32_t SORT_SMEM = 8192;  // u32 keys sorted in shared memory
 
 enum Ctr { C_NHEAVY = 0, C_NNEWATT, C_NOVF, C_ACTIVE, C_TOTAL, C_NCAND_TOTAL, C_NOVF2, C_NPULL, C_JQN0, C_JQN1,
            C_JQCUR, C_JHEAVY, C_NCTR = 16 };
-enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_PULLNODES, P_PULLEDGES, P_NPROF = 8 };
+enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_PULLNODES, P_PULLEDGES,
+            // recovery diagnostics (compiled in with -DREC_STATS=1)
+            P_R_BUILDS = 8, P_R_BEDGES, P_R_BCYC, P_R_WAITS, P_R_WCYC, P_R_CANDS, P_R_CANDCYC, P_R_CANDMAX, P_R_BMAX,
+            P_R_ITEMS, P_R_WARPMAX, P_R_H0, P_NPROF = 32 };  // P_R_H0..+5: candidate-time histogram
+#ifndef REC_STATS
+#define REC_STATS 0
+#endif
 enum Err { E_CAND = 1, E_HEAVY = 2, E_ARENA = 4, E_EXTRACT = 8, E_OUT = 16, E_UNRESOLVED = 32, E_QUEUE = 64 };
 
 struct SlotState {
@@ -1262,8 +1268,15 @@ __device__ void dag_list(const GraphDev &g, const WsDev &w, uint32_t s, int ph, 
             }
         }
         if (state == 2 && v == NOT_READY) {
+#if REC_STATS
+            const long long t0 = clock64();
+#endif
             volatile unsigned long long *vv = (volatile unsigned long long *)&tab[slot].z;
             while ((v = *vv) == NOT_READY) __nanosleep(32);
+#if REC_STATS
+            atomicAdd(&w.prof[P_R_WAITS], 1ull);
+            atomicAdd(&w.prof[P_R_WCYC], (unsigned long long)(clock64() - t0));
+#endif
         }
     }
     state = __shfl_sync(FULLMASK, state, 0);
@@ -1274,6 +1287,9 @@ __device__ void dag_list(const GraphDev &g, const WsDev &w, uint32_t s, int ph, 
         return;
     }
     slot = __shfl_sync(FULLMASK, slot, 0);
+#if REC_STATS
+    const long long tb0 = clock64();
+#endif
     const uint4 d = __ldg(g.idesc + q);  // in-rows are activation-sorted: gate a <= hq - 1
     const uint32_t rb = d.x;
     uint32_t hi, eqlo;
@@ -1326,6 +1342,14 @@ __device__ void dag_list(const GraphDev &g, const WsDev &w, uint32_t s, int ph, 
         __threadfence();
         atomicExch((unsigned long long *)&tab[slot].z, off == EMPTY ? 0ull : ((unsigned long long)off << 32 | cnt));
     }
+#if REC_STATS
+    if (lane == 0) {
+        atomicAdd(&w.prof[P_R_BUILDS], 1ull);
+        atomicAdd(&w.prof[P_R_BEDGES], (unsigned long long)(hi - rb));
+        atomicMax(&w.prof[P_R_BMAX], (unsigned long long)(hi - rb));
+        atomicAdd(&w.prof[P_R_BCYC], (unsigned long long)(clock64() - tb0));
+    }
+#endif
     *off_out = off == EMPTY ? 0 : off;
     *cnt_out = off == EMPTY ? 0 : cnt;
 }
@@ -1343,6 +1367,9 @@ __device__ void bfs_column(const G &G_, const GraphDev &g, const WsDev &w, uint3
             uint32_t q = b.hk.items[it];
             uint32_t hq = b.qh[it];
             if (hq == 0 || hq == 0xFF) continue;
+#if REC_STATS
+            if (lane == 0) atomicAdd(&w.prof[P_R_ITEMS], 1ull);
+#endif
             uint32_t off, cnt;
             dag_list<RowT>(g, w, s, ph, j, H, blocking, q, hq, &off, &cnt);
             for (uint32_t t = lane; t < cnt; t += 32) {
@@ -1452,7 +1479,13 @@ template <class G, class RowC> __device__ void extract_cg(const G &G_, const Gra
 // 1 = one CTA (256 threads) per candidate with 58 KB; 2 = global scratch sized by V.  A
 // candidate that overflows a tier is re-run by the next one, so recovery is exact at any size.
 template <int TIER> struct Tier;
-template <> struct Tier<0> { static constexpr uint32_t FU = 256, FUI = 128, FK = 256, FKI = 128, FE = 512, GROUPS = 4; };
+#ifndef T0_FE
+#define T0_FE 256
+#endif
+#ifndef T0_GROUPS
+#define T0_GROUPS 6
+#endif
+template <> struct Tier<0> { static constexpr uint32_t FU = 256, FUI = 128, FK = 256, FKI = 128, FE = T0_FE, GROUPS = T0_GROUPS; };
 template <> struct Tier<1> { static constexpr uint32_t FU = 2048, FUI = 1024, FK = 2048, FKI = 1024, FE = 4096, GROUPS = 1; };
 template <int TIER> constexpr size_t smem_group() {
     return ((size_t)(Tier<TIER>::FU + 2 * Tier<TIER>::FUI + Tier<TIER>::FK + 2 * Tier<TIER>::FKI + Tier<TIER>::FE +
@@ -1520,14 +1553,36 @@ template <class RowC, int TIER> __global__ void __launch_bounds__(tier_threads<T
         GroupWarp G_;
         if (first >= total) return;
         ex_init(G_, b, sh);
+#if REC_STATS
+        unsigned long long wsum = 0;
+#endif
+        // cyclic distribution: concurrent warps share queries (their H arrays and memo lists stay
+        // hot in L2), which measured faster than spreading warps over queries
         for (uint32_t item = first; item < total; item += stride) {
             uint32_t s = find_slot(w.coffs, w.nslots, item), c = item - w.coffs[s];
             bool ovf = false;
+#if REC_STATS
+            const long long tc0 = clock64();
+#endif
             extract_cg<GroupWarp, RowC>(G_, g, w, s, c, b, sh, &ovf);
+#if REC_STATS
+            if (G_.rank() == 0) {
+                const unsigned long long dt = clock64() - tc0;
+                atomicAdd(&w.prof[P_R_CANDS], 1ull);
+                atomicAdd(&w.prof[P_R_CANDCYC], dt);
+                atomicMax(&w.prof[P_R_CANDMAX], dt);
+                const int bk = dt < 16384 ? 0 : dt < 65536 ? 1 : dt < 262144 ? 2 : dt < 1048576 ? 3 : dt < 4194304 ? 4 : 5;
+                atomicAdd(&w.prof[P_R_H0 + bk], 1ull);
+                wsum += dt;
+            }
+#endif
             if (ovf && G_.rank() == 0) { sh.dirty = 1; push_overflow(w, 0, make_uint2(s, c)); }
             G_.sync();
             ex_reset(G_, b, sh);
         }
+#if REC_STATS
+        if (G_.rank() == 0) atomicMax(&w.prof[P_R_WARPMAX], wsum);
+#endif
     } else {
         GroupCTA G_;
         if (first >= total) return;
@@ -2179,6 +2234,18 @@ struct Launch {
     }
 };
 
+// Resident tier-0 recovery blocks per SM (one full wave), from the occupancy calculator.
+template <class K> uint32_t tier0_blocks_per_sm(K kernel) {
+    static uint32_t cached = 0;  // per kernel instantiation
+    if (!cached) {
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, tier_threads<0>(), smem_ex<0>()) != cudaSuccess || nb < 1)
+            nb = 1;
+        cached = (uint32_t)nb;
+    }
+    return cached;
+}
+
 // Runs one exploration loop over all slots (lock-step).  For run 2 the per-level attach /
 // RPG recovery / decide kernels run before the plan.  Returns when no slot expands.
 template <class RowT, class RowC>
@@ -2213,7 +2280,7 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             if (total_cands) {
                 k_attach<RowT><<<grid_of(total_cands * 32, 256), 256, 0, s>>>(wd);
                 L.check();
-                k_extract_rpg<RowT, 0><<<148 * 7, tier_threads<0>(), smem_ex<0>(), s>>>(gd, wd);
+                k_extract_rpg<RowT, 0><<<148 * tier0_blocks_per_sm(k_extract_rpg<RowT, 0>), tier_threads<0>(), smem_ex<0>(), s>>>(gd, wd);
                 L.check();
                 k_extract_rpg<RowT, 1><<<148 * 3, 256, smem_ex<1>(), s>>>(gd, wd);
                 L.check();
@@ -2300,7 +2367,8 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     CUDA_TRY(cudaStreamSynchronize(s));
     uint64_t total_cands = ws->h_ctr[C_NCAND_TOTAL];
     if (total_cands) {
-        k_extract_cg<RowC, 0><<<grid_of(total_cands, Tier<0>::GROUPS, 148 * 7), tier_threads<0>(), smem_ex<0>(), s>>>(gd, wd);
+        k_extract_cg<RowC, 0><<<grid_of(total_cands, Tier<0>::GROUPS, 148 * tier0_blocks_per_sm(k_extract_cg<RowC, 0>)), tier_threads<0>(),
+                                 smem_ex<0>(), s>>>(gd, wd);
         L.check();
         k_extract_cg<RowC, 1><<<148 * 3, 256, smem_ex<1>(), s>>>(gd, wd);
         L.check();
@@ -2512,6 +2580,13 @@ void add_stats(riki_graph *g, Workspace *ws, Launch &L, uint32_t nq) {
         L.expand_ms += ms;
     }
     L.nev = 0;
+#if REC_STATS
+    fprintf(stderr, "[riki-rec] builds %llu edges %llu max %llu build_cyc %llu | waits %llu wait_cyc %llu | items %llu | "
+                    "cg cands %llu cand_cyc %llu cand_max %llu warp_max %llu hist %llu %llu %llu %llu %llu %llu\n",
+            prof[P_R_BUILDS], prof[P_R_BEDGES], prof[P_R_BMAX], prof[P_R_BCYC], prof[P_R_WAITS], prof[P_R_WCYC],
+            prof[P_R_ITEMS], prof[P_R_CANDS], prof[P_R_CANDCYC], prof[P_R_CANDMAX], prof[P_R_WARPMAX],
+            prof[P_R_H0], prof[P_R_H0 + 1], prof[P_R_H0 + 2], prof[P_R_H0 + 3], prof[P_R_H0 + 4], prof[P_R_H0 + 5]);
+#endif
     uint64_t rb = ws->last_rb[0];  // bytes per H row (approximation when phases differ)
     g->stats.expand_launches += L.expand_launches;
     g->stats.expand_ms += L.expand_ms;

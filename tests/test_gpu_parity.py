@@ -123,6 +123,35 @@ def test_search_long_rows_high_activations(P, seed):
         assert r.stats["relax_central"] == ro.relax_c and r.stats["relax_marginal"] == ro.relax_m
 
 
+def _double_entry_graph(V=48):
+    """Every node is both retained (pending a = 30 edge) and newly reached at level 2, so the
+    level-2 frontier holds ~2V entries (one retained + one new per node)."""
+    src, dst, act = [], [], []
+    for i in range(2, V):
+        src += [0, 1, i]; dst += [i, i, 2 + (i - 1) % (V - 2)]; act += [0, 1, 30]
+    return V, np.array(src, np.uint32), np.array(dst, np.uint32), np.array(act, np.uint8)
+
+
+def test_frontier_queue_overflow_retried(P):
+    """A level queue may need 2V entries (Alg. 1 lines 9-11 retention + first-writer enqueue):
+    the overflow is detected, the queues regrow to 2V, and the answer equals the oracle's."""
+    V, src, dst, act = _double_entry_graph()
+    terms = [np.array([0], np.uint32), np.array([1], np.uint32)]
+    g = _dev_graph(P, V, src, dst, act, terms)
+    og = O.Graph(V, src, dst, act)
+    g.reset_stats()
+    for mode in (0, 1, 2):
+        H, blk, rel, L = g.hitting_levels(np.arange(2, dtype=np.uint32), 40, mode)
+        Ho, bo, Lo, relo = O.phase(og, terms, 40, mode)
+        assert (H == Ho).all() and (blk == bo).all() and L == Lo and rel == relo
+    assert g.stats()["retries"] >= 1
+    g2 = _dev_graph(P, V, src, dst, act, terms)
+    r = g2.search([0], [1], 3, 40)
+    ro = _oracle_run(og, lambda t: terms[t], [0], [1], 3, 40)
+    _cmp_results(r, ro)
+    assert r.stats["relax_central"] == ro.relax_c and r.stats["relax_marginal"] == ro.relax_m
+
+
 def test_hitting_levels_c1_all_terms(P):
     kg = synth.make_kg(1)
     g = P.Graph(kg.n_nodes, kg.src, kg.dst, kg.label_class, kg.term_ptr, kg.postings)
