@@ -1625,7 +1625,7 @@ template <class RowM> __global__ void __launch_bounds__(256) k_attach(WsDev w) {
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     uint32_t total = w.coffs[w.nslots];
     for (uint32_t item = gw; item < total; item += nw) {
-        uint32_t s = find_slot(w.coffs, w.nslots, item);
+        uint32_t s = find_slot_warp(w.coffs, w.nslots, item);
         uint32_t c = item - w.coffs[s];
         SlotState &st = w.st[s];
         if (!st.in_phase) continue;
@@ -2353,7 +2353,11 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     CUDA_TRY(cudaMemsetAsync(ws->arena_used, 0, 8, s));
     CUDA_TRY(cudaMemsetAsync(ws->out_used, 0, 8, s));
     CUDA_TRY(cudaMemsetAsync(ws->ctr, 0, C_NCTR * 4, s));
-    CUDA_TRY(cudaMemsetAsync(ws->mtab, 0xFF, (size_t)wd.nslots * 16 * MAPCAP * 16, s));
+    {   // memo maps: clear only the keyword columns this batch can use (row words bound them)
+        const size_t col = (size_t)MAPCAP * 16, pitch = 16 * col;
+        CUDA_TRY(cudaMemset2DAsync(ws->mtab, pitch, 0xFF, sizeof(RowC) * col, wd.nslots, s));
+        CUDA_TRY(cudaMemset2DAsync((uint8_t *)ws->mtab + 8 * col, pitch, 0xFF, sizeof(RowM) * col, wd.nslots, s));
+    }
     // ---- run 1: central keywords
     L.t0 = std::chrono::steady_clock::now();
     run_phase<RowC, RowC>(L, gd, ws, 0, -1, depth + 1, 0);
