@@ -34,7 +34,7 @@ typedef enum {
     RIKI_EUNRESOLVED = -5,     /* a query term has an empty posting list (message names it)      */
     RIKI_ENOWEIGHTS = -6,      /* search before activation levels were set                       */
     RIKI_EDEPTH = -7,          /* depth > 254                                                    */
-    RIKI_ENCCL = -8,           /* reserved for distributed mode                                  */
+    RIKI_ENCCL = -8,           /* NCCL could not be loaded or a collective failed (riki_dist_*)  */
     RIKI_ENOSYS = -9           /* not implemented in this build                                  */
 } riki_status;
 
@@ -236,6 +236,44 @@ riki_status riki_set_joint(riki_graph *g, int on);
 riki_status riki_set_batch_slots(riki_graph *g, uint32_t slots);
 /* device memory footprint of the resident graph and of the search workspace (bytes) */
 riki_status riki_memory_footprint(const riki_graph *g, uint64_t *graph_bytes, uint64_t *workspace_bytes);
+
+/* ---------------------------------------------------------------------------------------
+ * Multi-GPU.  One process per GPU, each with its own graph
+ * handle (graph replicated: riki_load_graph on every rank).
+ *
+ * mode 0, replicated: queries are independent units (Def. RPQ); each rank runs
+ *   its shard of a batch and no collective touches the data path (results are gathered by
+ *   the caller).  riki_dist_init with mode 0 only records nranks/rank.
+ * mode 1, vertex-partitioned: rank r owns the contiguous internal-node range
+ *   [bounds[r], bounds[r+1]) (balanced by in-degree + 1, riki_dist_partition) and performs
+ *   the level-l relaxations INTO its nodes bottom-up over their in-edges (a node takes
+ *   h = l+1 in column j iff some in-edge (f -> n) has a <= l, h_fj <= l and f not blocked
+ *   at l; the same H as Alg. 1's push, by Def. expansionBehavior).
+ *   The reached cells of level l+1 travel as bit planes (one bit per node and keyword), one
+ *   in-place ncclAllGather per level on the search stream (NCCL has no bitwise-OR
+ *   reduction); every rank then applies all slices, so H, blocks, candidates, termination
+ *   and results are identical on every rank without further collectives.  Every rank must
+ *   issue the same searches in the same order (collective semantics).
+ *
+ * riki_dist_unique_id: out128 (host, 128 bytes) receives a fresh NCCL unique id (call on
+ *   one rank, broadcast it, e.g. with torch.distributed).  RIKI_ENCCL if NCCL is missing.
+ * riki_dist_init: nranks in [1, 1024], rank in [0, nranks), nccl_unique_id = the 128-byte
+ *   id (host) or NULL.  With mode 1 and NULL id and nranks > 1, the nranks partitions are
+ *   SIMULATED inside this process on its one device (every partition's pull runs here and
+ *   the exchange is the identity): the single-GPU test of the partitioned arithmetic.  A
+ *   graph's previous distributed state is released first.  Disables the joint traversal.
+ *   Errors: RIKI_EINVAL (ranges, mode), RIKI_ENCCL, RIKI_ENOMEM.
+ * riki_dist_partition: HOST-only helper (no device needed): bounds[nranks + 1] for an
+ *   in-CSR row pointer irow[V + 1] (internal ids); bounds[0] = 0, bounds[nranks] = V, every
+ *   bound a multiple of 32 or V, non-decreasing (ranges may be empty).
+ * riki_dist_info: nranks, rank, mode, bounds (may be NULL; nranks + 1 entries, internal
+ *   ids), exchanges and exchanged bytes so far (may be NULL).
+ * ------------------------------------------------------------------------------------- */
+riki_status riki_dist_unique_id(void *out128);
+riki_status riki_dist_init(riki_graph *g, int nranks, int rank, const void *nccl_unique_id, int mode);
+riki_status riki_dist_partition(const uint32_t *irow, uint32_t n_nodes, uint32_t nranks, uint32_t *bounds);
+riki_status riki_dist_info(const riki_graph *g, int *nranks, int *rank, int *mode, uint32_t *bounds,
+                           uint64_t *exchanges, uint64_t *exchanged_bytes);
 
 const char *riki_last_error(void);
 const char *riki_version(void);

@@ -1,5 +1,6 @@
 // api.cu -- the C-ABI entry points of libriki.so (include/riki.h): argument checks,
 // exception-to-status translation, thread-local error text and host result objects.
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <string>
@@ -101,6 +102,7 @@ void riki_free_graph(riki_graph *g) {
     if (!g) return;
     cudaSetDevice(g->device);
     engine_free(g);
+    dist_free(g);
     graph_free(g);
     delete g;
 }
@@ -298,7 +300,49 @@ riki_status riki_set_direction(riki_graph *g, int mode) {
     });
 }
 riki_status riki_set_joint(riki_graph *g, int on) {
-    return guard([&] { need(g, "null graph"); g->joint_on = on != 0; });
+    return guard([&] {
+        need(g, "null graph");
+        need(!(on && g->vp()), "joint traversal is not available in vertex-partitioned mode");
+        g->joint_on = on != 0;
+    });
+}
+
+riki_status riki_dist_unique_id(void *out128) {
+    return guard([&] {
+        need(out128 != nullptr, "null output");
+        dist_unique_id(out128);
+    });
+}
+riki_status riki_dist_init(riki_graph *g, int nranks, int rank, const void *uid, int mode) {
+    return guard([&] {
+        need(g, "null graph");
+        CUDA_TRY(cudaSetDevice(g->device));
+        dist_init(g, nranks, rank, uid, mode);
+    });
+}
+riki_status riki_dist_partition(const uint32_t *irow, uint32_t n_nodes, uint32_t nranks, uint32_t *bounds) {
+    return guard([&] {
+        need(irow && bounds, "null argument");
+        need(nranks >= 1 && nranks <= 1024, "nranks must be in [1, 1024]");
+        for (uint32_t v = 0; v < n_nodes; v++) need(irow[v] <= irow[v + 1], "row pointer must be non-decreasing");
+        dist_partition(irow, n_nodes, nranks, bounds);
+    });
+}
+riki_status riki_dist_info(const riki_graph *g, int *nranks, int *rank, int *mode, uint32_t *bounds, uint64_t *exchanges,
+                           uint64_t *bytes) {
+    return guard([&] {
+        need(g, "null graph");
+        const DistState *d = g->dist;
+        if (nranks) *nranks = d ? d->nranks : 1;
+        if (rank) *rank = d ? d->rank : 0;
+        if (mode) *mode = d ? d->mode : 0;
+        if (bounds) {
+            if (d && !d->bounds.empty()) std::copy(d->bounds.begin(), d->bounds.end(), bounds);
+            else { bounds[0] = 0; bounds[1] = g->V; }
+        }
+        if (exchanges) *exchanges = d ? d->exchanges : 0;
+        if (bytes) *bytes = d ? d->exchanged_bytes : 0;
+    });
 }
 riki_status riki_set_batch_slots(riki_graph *g, uint32_t slots) {
     return guard([&] {

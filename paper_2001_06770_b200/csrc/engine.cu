@@ -318,7 +318,7 @@ __global__ void k_plan(WsDev w, int ph, uint32_t l, uint32_t pull_min) {
                 // with what is still unvisited (estimate: V*T minus new-node events)
                 uint64_t total = (uint64_t)w.V * st.T[ph];
                 uint64_t unvisited = total > st.reached ? total - st.reached : 0;
-                st.pull = items >= pull_min && (uint64_t)items * PULL_ALPHA > unvisited;
+                st.pull = pull_min == 0 || (items >= pull_min && (uint64_t)items * PULL_ALPHA > unvisited);
                 if (st.pull) w.pslots[atomicAdd(&npull, 1u)] = s;
             }
         }
@@ -770,6 +770,62 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
     if (lane == 0 && p_cells) atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
 }
 
+// Vertex-partitioned exchange slice: bit plane j of pull slot p holds, for each node of the
+// rank's range (offset i), whether column j was reached at level l + 1.
+template <class RowT>
+__device__ __forceinline__ void vp_set_bits(uint32_t *x, uint32_t p, uint32_t wc, uint32_t i, RowT found) {
+    constexpr uint32_t RB = sizeof(RowT);
+#pragma unroll
+    for (uint32_t j = 0; j < RB; j++)
+        if ((found >> (8 * j)) & 0xFF) atomicOr(x + ((size_t)p * RB + j) * wc + (i >> 5), 1u << (i & 31));
+}
+
+// Vertex-partitioned mode, after the all-gather: every rank applies every rank's slice to its
+// replicated H (identical H, blocks, frontiers and candidates on all ranks), with the same
+// write, next-frontier append and identification at l + 1 as the single-GPU pull.  Thread
+// per (rank, node offset); x = [rank][pull slot][plane][wc].
+template <class RowT>
+__global__ void __launch_bounds__(256) k_vp_apply(GraphDev g, WsDev w, int ph, uint32_t l, const uint32_t *x,
+                                                  uint32_t wc, uint32_t nranks, const uint32_t *bounds, uint32_t npull) {
+    typedef Row<RowT> R;
+    constexpr uint32_t RB = sizeof(RowT);
+    const uint32_t p = blockIdx.y, s = w.pslots[p];
+    const HV<RowT> H = w.Hs<RowT>(ph, s);
+    const bool collect = w.st[s].collect;
+    const uint32_t nxt = (l & 1) ^ 1;
+    const size_t chunk = (size_t)npull * RB * wc;
+    const uint64_t total = (uint64_t)nranks * wc * 32;
+    uint32_t p_cells = 0;
+    for (uint64_t b = (uint64_t)blockIdx.x * blockDim.x; b < total; b += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t t = b + threadIdx.x;
+        bool enq = false, id = false;
+        uint32_t n = 0;
+        if (t < total) {
+            const uint32_t r = (uint32_t)(t / ((uint64_t)wc * 32)), i = (uint32_t)(t % ((uint64_t)wc * 32));
+            n = __ldg(bounds + r) + i;
+            if (n < __ldg(bounds + r + 1)) {
+                const uint32_t *xs = x + r * chunk + (size_t)p * RB * wc + (i >> 5);
+                RowT found = 0;
+#pragma unroll
+                for (uint32_t j = 0; j < RB; j++)
+                    if ((__ldg(xs + (size_t)j * wc) >> (i & 31)) & 1u) found |= (RowT)0xFF << (8 * j);
+                if (found) {
+                    const RowT Rn = R::load(H + n);
+                    const RowT nr = (Rn & ~found) | (found & R::splat(l + 1));
+                    *(H + n) = nr;
+                    enq = true;
+                    id = collect && R::eq(nr, R::splat(0xFF)) == 0;
+                    p_cells += R::ones(found);
+                }
+            }
+        }
+        frontier_push(w, enq, s, n, nxt);
+        cand_push(g, w, id, s, n, l + 1);
+    }
+    p_cells = warp_sum(p_cells);
+    if (lane_id() == 0 && p_cells) atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
+}
+
 // Bottom-up expansion of a dense level (direction-optimising BFS).  Node n with an infinite
 // column j takes h_nj = l + 1 iff some in-edge (f -> n) has a <= l, h_fj <= l and f is not
 // blocked at l.  This is exactly Alg. 1's push at level l: an unblocked f with
@@ -777,8 +833,14 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
 // thread writes its row (no atomics); in-rows are activation-sorted so the scan stops at
 // a > l, and as soon as every infinite column found a parent.  Heavy in-rows (internal ids
 // < Vh) are scanned by a warp, the rest by one thread each.
+//
+// Vertex-partitioned mode (vpx != nullptr): only nodes of [lo, hi) are pulled (the in-edges
+// this rank owns) and a node's new columns are not written to H but set in bit plane j of
+// the rank's exchange slice, vpx[(pull slot * RB + j) * wc + (n - lo) / 32]; k_vp_apply
+// writes them on every rank after the all-gather.
 template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_pull(GraphDev g, WsDev w, int ph, uint32_t l,
-                                                                             uint32_t nbh) {
+                                                                             uint32_t nbh, uint32_t lo, uint32_t hi,
+                                                                             uint32_t *vpx, uint32_t wc) {
     typedef Row<RowT> R;
     const uint32_t s = w.pslots[blockIdx.y];
     const SlotState &st = w.st[s];
@@ -789,8 +851,8 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_pull(Gr
     const uint32_t nxt = (l & 1) ^ 1, lane = lane_id();
     uint32_t p_nodes = 0, p_edges = 0, p_cells = 0;
     if (blockIdx.x < nbh) {  // warp per heavy node
-        const uint32_t nw = nbh * (blockDim.x >> 5);
-        for (uint32_t n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < g.Vh; n += nw) {
+        const uint32_t nw = nbh * (blockDim.x >> 5), hh = min(hi, g.Vh);
+        for (uint32_t n = lo + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); n < hh; n += nw) {
             RowT Rn = R::load(H + n);
             RowT inf = R::eq(Rn, FF) & used;
             RowT found = 0;
@@ -818,21 +880,25 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_pull(Gr
             }
             bool enq = false, id = false;
             if (found && lane == 0) {
-                RowT nr = (Rn & ~found) | (found & R::splat(l + 1));
-                *(H + n) = nr;
-                enq = true;
-                id = collect && R::eq(nr, FF) == 0;
-                p_cells += R::ones(found);
+                if (vpx) {
+                    vp_set_bits<RowT>(vpx, blockIdx.y, wc, n - lo, found);
+                } else {
+                    RowT nr = (Rn & ~found) | (found & R::splat(l + 1));
+                    *(H + n) = nr;
+                    enq = true;
+                    id = collect && R::eq(nr, FF) == 0;
+                    p_cells += R::ones(found);
+                }
             }
             frontier_push(w, enq, s, n, nxt);
             cand_push(g, w, id, s, n, l + 1);
         }
     } else {  // thread per light node
         const uint32_t stride = (gridDim.x - nbh) * blockDim.x;
-        for (uint32_t n0 = g.Vh + (blockIdx.x - nbh) * blockDim.x; n0 < w.V; n0 += stride) {
+        for (uint32_t n0 = max(lo, g.Vh) + (blockIdx.x - nbh) * blockDim.x; n0 < hi; n0 += stride) {
             uint32_t n = n0 + threadIdx.x;
             bool enq = false, id = false;
-            if (n < w.V) {
+            if (n < hi) {
                 RowT Rn = R::load(H + n);
                 RowT inf = R::eq(Rn, FF) & used;
                 if (inf) {
@@ -860,13 +926,15 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_pull(Gr
                         }
                         if (!ok[3]) break;  // activation-sorted: past the gate (or the row end)
                     }
-                    if (found) {
+                    if (found && vpx) {
+                        vp_set_bits<RowT>(vpx, blockIdx.y, wc, n - lo, found);
+                    } else if (found) {
                         RowT nr = (Rn & ~found) | (found & R::splat(l + 1));
                         *(H + n) = nr;
                         enq = true;
                         id = collect && R::eq(nr, FF) == 0;
                         p_cells += R::ones(found);
-                            }
+                    }
                 }
             }
             frontier_push(w, enq, s, n, nxt);
@@ -2246,12 +2314,43 @@ template <class K> uint32_t tier0_blocks_per_sm(K kernel) {
     return cached;
 }
 
+// One vertex-partitioned level: pull over this rank's node range into its
+// slice of the bit-plane buffer (every range, in simulated mode), one in-place all-gather
+// on the search stream, then every rank applies all slices.  Identical H, blocks, frontiers
+// and candidates on every rank, so termination needs no further collective.
+template <class RowT>
+void vp_level(Launch &L, const GraphDev &gd, const WsDev &wd, int ph, uint32_t l, uint32_t npull) {
+    DistState *d = L.g->dist;
+    cudaStream_t s = L.s;
+    const size_t chunk = (size_t)npull * sizeof(RowT) * d->wc;
+    uint32_t *x = dist_exchange_buffer(L.g, chunk);
+    CUDA_TRY(cudaMemsetAsync(x, 0, chunk * 4 * d->nranks, s));
+    for (int r = 0; r < d->nranks; r++) {
+        if (!d->simulated && r != d->rank) continue;
+        const uint32_t lo = d->bounds[r], hi = d->bounds[r + 1];
+        if (hi <= lo) continue;
+        const uint32_t hh = std::min(hi, gd.Vh);
+        const uint32_t nbh = hh > lo ? std::min<uint32_t>((hh - lo + 7) / 8, 148 * 8) : 0;
+        const uint32_t ll = std::max(lo, gd.Vh);
+        const uint32_t nbl = hi > ll ? std::min<uint32_t>((hi - ll + 255) / 256, 148 * 8) : 0;
+        k_pull<RowT><<<dim3(nbh + nbl, npull), 256, 0, s>>>(gd, wd, ph, l, nbh, lo, hi, x + chunk * r, d->wc);
+        L.check();
+    }
+    dist_allgather(L.g, x, chunk, s);
+    const uint64_t total = (uint64_t)d->nranks * d->wc * 32;
+    k_vp_apply<RowT><<<dim3((uint32_t)std::min<uint64_t>((total + 255) / 256, 148 * 8), npull), 256, 0, s>>>(
+        gd, wd, ph, l, x, d->wc, d->nranks, d->d_bounds, npull);
+    L.check();
+}
+
 // Runs one exploration loop over all slots (lock-step).  For run 2 the per-level attach /
 // RPG recovery / decide kernels run before the plan.  Returns when no slot expands.
 template <class RowT, class RowC>
 void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting_mode, uint32_t max_levels,
                uint64_t total_cands) {
     cudaStream_t s = L.s;
+    const bool vp = L.g->vp();  // vertex-partitioned: every level is a partitioned pull + all-gather
+    const bool pull = L.g->pull_on || vp;
     ws->track_reached = L.g->pull_on ? 1 : 0;
     WsDev wd = ws->dev();
     k_phase_begin<<<(wd.nslots + 127) / 128, 128, 0, s>>>(wd, ph, hitting_mode);
@@ -2290,9 +2389,9 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             k_decide_m<<<wd.nslots, 256, 1024 * 16, s>>>(wd, l);
             L.check();
         }
-        k_plan<<<1, MAX_SLOTS, 0, s>>>(wd, ph, l, !L.g->pull_on ? 0xFFFFFFFFu : std::max<uint32_t>(ws->V / PULL_MIN_DIV, 1));
+        k_plan<<<1, MAX_SLOTS, 0, s>>>(wd, ph, l, vp ? 0u : !L.g->pull_on ? 0xFFFFFFFFu : std::max<uint32_t>(ws->V / PULL_MIN_DIV, 1));
         L.check();
-        if (l % LEVEL_BATCH == LEVEL_BATCH - 1 || l == max_levels || L.g->pull_on) {
+        if (l % LEVEL_BATCH == LEVEL_BATCH - 1 || l == max_levels || pull) {
             CUDA_TRY(cudaMemcpyAsync(ws->h_ctr, ws->ctr, C_NCTR * 4, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
             if (ws->h_ctr[C_ACTIVE] == 0) break;
@@ -2312,11 +2411,14 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             k_expand_heavy<RowT><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
             L.check();
         }
-        if (L.g->pull_on) {
+        if (vp) {
+            if (uint32_t npull = ws->h_ctr[C_NPULL]) vp_level<RowT>(L, gd, wd, ph, l, npull);
+        } else if (L.g->pull_on) {
             if (uint32_t npull = ws->h_ctr[C_NPULL]) {
                 uint32_t nbh = (gd.Vh + 7) / 8;
                 uint32_t nbl = std::min<uint32_t>((ws->V - gd.Vh + 255) / 256, 148 * 8);
-                k_pull<RowT><<<dim3(nbh + std::max<uint32_t>(nbl, 1), npull), 256, 0, s>>>(gd, wd, ph, l, nbh);
+                k_pull<RowT><<<dim3(nbh + std::max<uint32_t>(nbl, 1), npull), 256, 0, s>>>(gd, wd, ph, l, nbh, 0u, ws->V,
+                                                                                           nullptr, 0u);
                 L.check();
             }
         }

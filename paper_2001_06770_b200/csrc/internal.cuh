@@ -10,6 +10,26 @@
 
 struct Workspace;  // engine.cu
 
+// Vertex-partitioned mode (dist.cu).  Rank r owns the internal-id range
+// [bounds[r], bounds[r+1]) and relaxes only the in-edges of its own nodes (pull, owner
+// computes); the nodes it reached at level l+1 go into its slice of a bit-plane buffer that
+// one in-place all-gather per level makes identical on every rank, after which every rank
+// applies all slices to its replicated H.  `simulated`: nranks partitions driven by ONE
+// process on one device (every partition's pull runs here, the all-gather is the identity
+// because all slices already live in the same buffer) -- the single-GPU test of the
+// partitioned arithmetic.
+struct DistState {
+    int nranks = 1, rank = 0, mode = 0;  // mode 0 replicated (no data-path collective), 1 vertex-partitioned
+    bool simulated = false;
+    void *comm = nullptr;                // ncclComm_t (real mode)
+    std::vector<uint32_t> bounds;        // nranks + 1 internal-id bounds; each a multiple of 32 or V
+    uint32_t *d_bounds = nullptr;
+    uint32_t wc = 0;                     // u32 words per rank, per slot and bit plane
+    uint32_t *d_x = nullptr;             // exchange buffer [rank][pull slot][plane][wc]
+    size_t x_words = 0;
+    uint64_t exchanges = 0, exchanged_bytes = 0;
+};
+
 // Device view of the resident graph (P:339 CSR).  Out-rows are sorted by activation
 // ascending (then by edge id), so the Alg. 1 gate a <= l reads a row prefix.  In-rows
 // (Alg. 2 line 5, N_i) are sorted the same way and carry the forward edge's activation
@@ -67,6 +87,8 @@ struct riki_graph {
     bool profiling = false, debug = false, pull_on = false, joint_on = false;
     uint32_t batch_slots = 0;
     riki_stats stats{};
+    DistState *dist = nullptr;  // set by riki_dist_init
+    bool vp() const { return dist && dist->mode == 1; }
 
     GraphDev dev() const {
         GraphDev g;
@@ -116,4 +138,12 @@ void engine_fetch(riki_graph *g, uint32_t nq, std::vector<riki_results *> *out);
 void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uint32_t depth, int block_mode,
                            uint8_t *H_out, uint8_t *block_out, uint64_t *relax_out, int32_t *L_out);
 void engine_free(riki_graph *g);
+
+// dist.cu
+void dist_unique_id(void *out128);
+void dist_init(riki_graph *g, int nranks, int rank, const void *uid, int mode);
+void dist_partition(const uint32_t *irow, uint32_t V, uint32_t nranks, uint32_t *bounds);
+uint32_t *dist_exchange_buffer(riki_graph *g, size_t chunk_words);  // [nranks][chunk_words], zeroed by the caller
+void dist_allgather(riki_graph *g, uint32_t *x, size_t chunk_words, cudaStream_t s);
+void dist_free(riki_graph *g);
 uint64_t engine_workspace_bytes(const riki_graph *g);

@@ -31,6 +31,20 @@ def search_sharded(search_fn, centrals, marginals, k, depth, group=None, **kw):
     return [r for p in parts for r in p]
 
 
+def init_vertex_partitioned(graph, group=None, unique_id_fn=None):
+    """Vertex-partitioned mode over the ranks of `group`: rank 0 draws the NCCL
+    unique id (riki_dist_unique_id), the process group broadcasts it, and every rank binds its
+    graph handle to one NCCL communicator (riki_dist_init, mode 1).  Every rank then issues the
+    same searches; each gets the identical result.  Returns (rank, world)."""
+    from .riki import dist_unique_id
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    uid = [(unique_id_fn or dist_unique_id)() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    graph.dist_init(world, rank, uid[0], mode=1)
+    return rank, world
+
+
 def max_over_ranks(x: float, group=None, device=None) -> float:
     """Max of a host float over the ranks (NCCL needs a CUDA tensor, gloo a CPU one)."""
     if not dist.is_initialized() or dist.get_world_size(group) == 1:

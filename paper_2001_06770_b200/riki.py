@@ -113,6 +113,10 @@ def load():
         "riki_set_joint": (i32, [P, i32]),
         "riki_set_batch_slots": (i32, [P, u32]),
         "riki_memory_footprint": (i32, [P, P, P]),
+        "riki_dist_unique_id": (i32, [P]),
+        "riki_dist_init": (i32, [P, i32, i32, P, i32]),
+        "riki_dist_partition": (i32, [P, u32, u32, P]),
+        "riki_dist_info": (i32, [P, P, P, P, P, P, P]),
         "riki_last_error": (C.c_char_p, []),
         "riki_version": (C.c_char_p, []),
     }
@@ -122,6 +126,21 @@ def load():
         f.argtypes = args
     _lib = lib
     return lib
+
+
+def dist_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (riki_dist_unique_id) for riki_dist_init."""
+    buf = C.create_string_buffer(128)
+    _check(load().riki_dist_unique_id(buf))
+    return buf.raw
+
+
+def dist_partition(irow, nranks) -> np.ndarray:
+    """Vertex-partition bounds for an in-CSR row pointer (host-only, riki_dist_partition)."""
+    irow = np.ascontiguousarray(irow, np.uint32)
+    b = np.zeros(nranks + 1, np.uint32)
+    _check(load().riki_dist_partition(_p(irow), len(irow) - 1, nranks, _p(b)))
+    return b
 
 
 def _check(rc):
@@ -387,6 +406,25 @@ class Graph:
 
     def reset_stats(self):
         _check(self.lib.riki_reset_stats(self.h))
+
+    # -- multi-GPU (include/riki.h riki_dist_*)
+    def dist_init(self, nranks, rank, unique_id=None, mode=1):
+        """mode 1 = vertex-partitioned (unique_id: 128 bytes from dist_unique_id(); None with
+        nranks > 1 simulates the nranks partitions in this process), mode 0 = replicated."""
+        buf = None
+        if unique_id is not None:
+            assert len(unique_id) == 128
+            buf = C.create_string_buffer(bytes(unique_id), 128)
+        _check(self.lib.riki_dist_init(self.h, int(nranks), int(rank), buf, int(mode)))
+
+    def dist_info(self) -> dict:
+        n, r, m = C.c_int(), C.c_int(), C.c_int()
+        _check(self.lib.riki_dist_info(self.h, C.byref(n), C.byref(r), C.byref(m), None, None, None))
+        b = np.zeros(n.value + 1, np.uint32)
+        x, xb = C.c_uint64(), C.c_uint64()
+        _check(self.lib.riki_dist_info(self.h, None, None, None, _p(b), C.byref(x), C.byref(xb)))
+        return {"nranks": n.value, "rank": r.value, "mode": m.value, "bounds": b, "exchanges": x.value,
+                "exchanged_bytes": xb.value}
 
     def memory_footprint(self):
         a, b = C.c_uint64(), C.c_uint64()
