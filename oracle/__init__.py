@@ -62,6 +62,7 @@ def _load():
         "orc_res_cand": (None, [P, u32, P, P, P, P, P, P, P, P, P]),
         "orc_res_cand_lists": (None, [P, u32, P, P, P]),
         "orc_res_get": (None, [P, u32, P, P, P, P, P, P, P, P, P]),
+        "orc_res_wsum": (C.c_uint64, [P, u32]),
         "orc_res_lists": (None, [P, u32, P, P, P, P, P]),
         "orc_res_matrix": (i32, [P, i32, P, P]),
     }
@@ -79,7 +80,7 @@ def _ptr(a: np.ndarray):
 
 class _Params(C.Structure):
     _fields_ = [("gamma", C.c_double), ("beam_w", C.c_uint32), ("beam_mode", C.c_int),
-                ("ptc_mode", C.c_int), ("early_term", C.c_int)]
+                ("ptc_mode", C.c_int), ("early_term", C.c_int), ("tie_break", C.c_int), ("wfine", C.c_void_p)]
 
 
 # ---------------------------------------------------------------- weighting
@@ -178,6 +179,7 @@ class RPG:
     vc: np.ndarray
     cdist: np.ndarray
     mdist: np.ndarray
+    wsum: int = 0  # tie_break 1: W(G^r) in units of 2^-32 (R29)
 
 
 @dataclass
@@ -212,9 +214,11 @@ class SearchResult:
 
 def search(g: Graph, central_nodes, marginal_nodes, k: int, depth: int, gamma: float = 0.5, beam_w: int = 0,
            beam_mode: int = 0, ptc_mode: int = 0, early_term: int = 0, want_matrices: bool = True,
-           want_candidates: bool = True) -> SearchResult:
+           want_candidates: bool = True, tie_break: int = 0, wfine=None) -> SearchResult:
     """Full RPQ search (Def. RPKSP).  central_nodes / marginal_nodes are
-    lists of posting lists (one per keyword)."""
+    lists of posting lists (one per keyword).  tie_break 1 (R29) ranks equal
+    (S^r, S^c) by the weight sum of the result's distinct edges; wfine = the fine edge
+    weights (f64 by edge id) it needs."""
     if not central_nodes:
         raise ValueError("C must be non-empty (Def. RPQ, P:105)")
     if k < 1:
@@ -222,7 +226,13 @@ def search(g: Graph, central_nodes, marginal_nodes, k: int, depth: int, gamma: f
     lib = g.lib
     cp, cf = _postings_csr(central_nodes)
     mp, mf = _postings_csr(marginal_nodes)
-    prm = _Params(gamma, beam_w, beam_mode, ptc_mode, early_term)
+    wf = None
+    if tie_break:
+        if wfine is None:
+            raise ValueError("tie_break 1 needs the fine edge weights")
+        wf = np.ascontiguousarray(wfine, np.float64)
+        assert len(wf) == g.E
+    prm = _Params(gamma, beam_w, beam_mode, ptc_mode, early_term, tie_break, wf.ctypes.data if wf is not None else None)
     r = lib.orc_search(g.h, len(central_nodes), _ptr(cp), _ptr(cf), len(marginal_nodes), _ptr(mp), _ptr(mf),
                        k, depth, C.byref(prm))
     try:
@@ -243,7 +253,8 @@ def search(g: Graph, central_nodes, marginal_nodes, k: int, depth: int, gamma: f
             cd = np.zeros(nc, np.uint8)
             md = np.zeros(nm, np.uint8)
             lib.orc_res_lists(r, i, _ptr(nodes), _ptr(edges), _ptr(vc), _ptr(cd), _ptr(md))
-            out.rpgs.append(RPG(v.value, sc.value, sm.value, sr.value, ptc.value, nodes, edges, vc, cd, md))
+            out.rpgs.append(RPG(v.value, sc.value, sm.value, sr.value, ptc.value, nodes, edges, vc, cd, md,
+                                int(lib.orc_res_wsum(r, i))))
         if want_candidates:
             for i in range(lib.orc_res_ncand(r)):
                 v, sc, sm = u32(), u32(), u32()

@@ -18,6 +18,7 @@
  *   orc_phase         P:343-464      initialisation, enqueue, identification,
  *                                    Alg. 1 expansion (literal, with re-scans)
  *   orc_search        P:301-381,503-561  two runs + Alg. 2 recovery + PTC + rank
+ *                     P:293              optional weight-sum tie-break (tie_break 1, R29)
  *
  * Every floating-point expression is evaluated in IEEE fp64 in exactly the
  * order written here; the file must be compiled with -ffp-contract=off.
@@ -421,6 +422,8 @@ typedef struct {
     int beam_mode;     /* 0 keep ties at the terminating level (R13 default), 1 truncate to w */
     int ptc_mode;      /* 0 filter (R19/R20), 1 flag only, 2 filter G^m-only, 3 filter SPEC-exclusive */
     int early_term;    /* 0 exact bound (R21), 1 paper-literal inequality, 2 none (exhaustive) */
+    int tie_break;     /* 0 (S^r, S^c, v) (R23); 1 (S^r, S^c, W, v), W = edge-weight sum (R29) */
+    const double *wfine; /* tie_break 1: fine edge weights w01[e] by caller edge id */
 } orc_params;
 
 typedef struct {
@@ -431,6 +434,7 @@ typedef struct {
     vu32 cnodes; vu64 cedges;          /* CG part */
     vu32 mnodes; vu64 medges;          /* G^m part */
     uint8_t *cdist, *mdist;
+    uint64_t wsum;                     /* tie_break 1: W of the CG (beam) or of the RPG (ranking) */
 } cand_t;
 
 typedef struct orc_result {
@@ -444,16 +448,30 @@ typedef struct orc_result {
     uint32_t n_attached, n_ptc_fail;
 } orc_result;
 
-static int key_less(const cand_t *a, const cand_t *b) { /* (S^r, S^c, v) ascending (R23) */
+static int key_less(const cand_t *a, const cand_t *b, int tie) {
+    /* (S^r, S^c, v) ascending (R23); tie_break 1: (S^r, S^c, W, v) -- P:293 "break the ties
+       by a re-ranking operation, e.g. using the sum of edge weights" (R29: smaller W first) */
     if (a->sr != b->sr) return a->sr < b->sr;
     if (a->sc != b->sc) return a->sc < b->sc;
+    if (tie && a->wsum != b->wsum) return a->wsum < b->wsum;
     return a->v < b->v;
 }
 
+/* R29: a fine weight w in [0,1] as the integer round(w * 2^32) (w * 2^32 is exact in fp64,
+   so the sum below is exact and independent of the summation order). */
+static uint64_t weight_fixed(double w) { return (uint64_t)floor(w * 4294967296.0 + 0.5); }
+
+/* W(G) = sum of the fine weights of the DISTINCT edges of G (edges sorted, unique). */
+static uint64_t edge_weight_sum(const vu64 *edges, const double *wfine) {
+    uint64_t W = 0;
+    for (uint64_t i = 0; i < edges->n; i++) W += weight_fixed(wfine[edges->a[i]]);
+    return W;
+}
+
 /* Insertion into the running k-best list (indices into cand), ascending keys. */
-static void kbest_insert(uint32_t *kb, uint32_t *nkb, uint32_t k, cand_t *cand, uint32_t c) {
+static void kbest_insert(uint32_t *kb, uint32_t *nkb, uint32_t k, cand_t *cand, uint32_t c, int tie) {
     uint32_t pos = *nkb;
-    while (pos > 0 && key_less(&cand[c], &cand[kb[pos - 1]])) pos--;
+    while (pos > 0 && key_less(&cand[c], &cand[kb[pos - 1]], tie)) pos--;
     if (pos >= k) return;
     uint32_t end = *nkb < k ? *nkb : k - 1;
     for (uint32_t i = end; i > pos; i--) kb[i] = kb[i - 1];
@@ -474,8 +492,9 @@ orc_result *orc_search(const orc_graph *g,
                        uint32_t nc, const uint64_t *cptr, const uint32_t *cnodes,
                        uint32_t nm, const uint64_t *mptr, const uint32_t *mnodes,
                        uint32_t k, uint32_t depth, const orc_params *prm) {
-    orc_params P = {0.5, 0, 0, 0, 0};
+    orc_params P = {0.5, 0, 0, 0, 0, 0, NULL};
     if (prm) P = *prm;
+    const int tie = P.tie_break == 1 && P.wfine != NULL;
     uint32_t w = P.beam_w ? P.beam_w : k;
     orc_result *r = calloc(1, sizeof(orc_result));
     r->nc = nc; r->nm = nm; r->k = k; r->V = g->V; r->Lc = -1; r->Lm = -1;
@@ -498,7 +517,7 @@ orc_result *orc_search(const orc_graph *g,
     /* candidates: all CGs identified by the terminating level, ordered by (S^c, v) (R13) */
     sort_unique_u64(&ids);
     uint32_t ncand = (uint32_t)ids.n;
-    if (P.beam_mode == 1 && ncand > w) ncand = w;
+    if (P.beam_mode == 1 && ncand > w && !tie) ncand = w;  /* (tie-break: truncated after recovery) */
     r->ncand = ncand;
     r->cand = calloc(ncand + 1, sizeof(cand_t));
     for (uint32_t i = 0; i < ncand; i++) {
@@ -515,8 +534,34 @@ orc_result *orc_search(const orc_graph *g,
             uint32_t v = c->cnodes.a[t];
             for (uint32_t j = 0; j < nc; j++) if (pc.H[(uint64_t)v * nc + j] == 0) { vu32_push(&c->vc, v); break; }
         }
+        if (tie) c->wsum = edge_weight_sum(&c->cedges, P.wfine);
     }
     free(ids.a);
+    if (tie && P.beam_mode == 1 && ncand > w) {
+        /* beam of width w with the tie-break (R29): the w smallest (S^c, W(CG), v), then back
+           to (S^c, v) order; the dropped candidates are released */
+        for (uint32_t i = 1; i < ncand; i++)        /* insertion sort by (S^c, W, v) */
+            for (uint32_t j = i; j > 0; j--) {
+                cand_t *a = &r->cand[j - 1], *b = &r->cand[j];
+                int less = b->sc != a->sc ? b->sc < a->sc : b->wsum != a->wsum ? b->wsum < a->wsum : b->v < a->v;
+                if (!less) break;
+                cand_t t = *a; *a = *b; *b = t;
+            }
+        for (uint32_t i = w; i < ncand; i++) {
+            cand_t *c = &r->cand[i];
+            free(c->cnodes.a); free(c->cedges.a); free(c->vc.a); free(c->cdist); free(c->mdist);
+            memset(c, 0, sizeof(*c));
+        }
+        ncand = w;
+        r->ncand = w;
+        for (uint32_t i = 1; i < ncand; i++)        /* (S^c, v) order */
+            for (uint32_t j = i; j > 0; j--) {
+                cand_t *a = &r->cand[j - 1], *b = &r->cand[j];
+                int less = b->sc != a->sc ? b->sc < a->sc : b->v < a->v;
+                if (!less) break;
+                cand_t t = *a; *a = *b; *b = t;
+            }
+    }
 
     uint32_t *kb = calloc(k + 1, 4), nkb = 0;
     if (nm == 0) {
@@ -525,7 +570,8 @@ orc_result *orc_search(const orc_graph *g,
             cand_t *c = &r->cand[i];
             c->attached = 1; c->ptc = 1; c->sm = 0; c->sr = (double)c->sc;
             merge_sets(c);
-            kbest_insert(kb, &nkb, k, r->cand, i);
+            if (tie) c->wsum = edge_weight_sum(&c->edges, P.wfine);
+            kbest_insert(kb, &nkb, k, r->cand, i, tie);
         }
     } else {
         /* ---- second run: marginal keywords with a fresh H (R12) ---- */
@@ -564,9 +610,10 @@ orc_result *orc_search(const orc_graph *g,
                 }
                 sort_unique_u32(&c->mnodes); sort_unique_u64(&c->medges);
                 merge_sets(c);
+                if (tie) c->wsum = edge_weight_sum(&c->edges, P.wfine);  /* W(G^r), G^r = CG u G^m */
                 c->ptc = ptc_check(g, &c->nodes, &c->edges, &c->vc, pm.H, nm, P.ptc_mode, &c->medges, &c->mnodes);
                 if (!c->ptc) r->n_ptc_fail++;
-                if (c->ptc || P.ptc_mode == 1) kbest_insert(kb, &nkb, k, r->cand, ci);
+                if (c->ptc || P.ptc_mode == 1) kbest_insert(kb, &nkb, k, r->cand, ci, tie);
             }
             /* termination (P:375-381 with R21) */
             int stop = (l == depth) || (pm.nphi == 0) || (unattached == 0);
@@ -579,7 +626,11 @@ orc_result *orc_search(const orc_graph *g,
                         if (c->attached) continue;
                         cand_t best = *c;
                         best.sr = orc_rpg_score(P.gamma, c->sc, l + 1);
-                        if (!key_less(kth, &best)) all_worse = 0;   /* best <= kth: could still enter */
+                        /* best <= kth: could still enter.  With the tie-break its W is unknown
+                           until it attaches, so only a strictly larger (S^r, S^c) excludes it */
+                        if (tie ? !(kth->sr < best.sr || (kth->sr == best.sr && kth->sc < best.sc))
+                                : !key_less(kth, &best, 0))
+                            all_worse = 0;
                     }
                     stop = all_worse;
                 } else {
@@ -638,6 +689,7 @@ void orc_res_cand_lists(const orc_result *r, uint32_t i, uint32_t *cnodes, uint6
     if (vc) memcpy(vc, c->vc.a, c->vc.n * 4);
 }
 /* ranked result i: candidate index, sizes */
+uint64_t orc_res_wsum(const orc_result *r, uint32_t i) { return r->cand[r->res[i]].wsum; }
 void orc_res_get(const orc_result *r, uint32_t i, uint32_t *cand_index, uint32_t *v, uint32_t *sc, uint32_t *sm,
                  double *sr, int *ptc, uint64_t *n_nodes, uint64_t *n_edges, uint64_t *n_vc) {
     const cand_t *c = &r->cand[r->res[i]];

@@ -222,10 +222,21 @@ def ptc_brute(V, src, dst, nodes, edges, vc, Hm, n_marg, max_len=30):
     return False
 
 
-def search_plain(V, src, dst, act, central, marginal, k, depth, gamma=0.5):
+def weight_sum(edges, wfine):
+    """R29: sum over the distinct edges of round-half-up(w * 2^32), in exact rationals."""
+    from fractions import Fraction
+    tot = 0
+    for e in set(int(x) for x in edges):
+        q = Fraction(float(wfine[e])) * (1 << 32) + Fraction(1, 2)
+        tot += q.numerator // q.denominator
+    return tot
+
+
+def search_plain(V, src, dst, act, central, marginal, k, depth, gamma=0.5, wfine=None):
     """Plain-definition form of the search (after R21):
     candidates = CGs identified by the central terminating level (ties kept, R13);
-    marginal run exhaustive to depth D; attach all; PTC filter; sort (S^r, S^c, v); take k."""
+    marginal run exhaustive to depth D; attach all; PTC filter; sort (S^r, S^c, v); take k.
+    With wfine (tie-break R29) the sort is (S^r, S^c, W(result edges), v)."""
     src = np.asarray(src)
     dst = np.asarray(dst)
     nc, nm = len(central), len(marginal)
@@ -277,5 +288,8 @@ def search_plain(V, src, dst, act, central, marginal, k, depth, gamma=0.5):
             sr = gamma * float(sc) + (1.0 - gamma) * float(sm)
             res.append((sr, sc, v, sm, sorted(nodes), sorted(edges), vcl, p))
     res = [r for r in res if r[7]]
-    res.sort(key=lambda r: (r[0], r[1], r[2]))
+    if wfine is None:
+        res.sort(key=lambda r: (r[0], r[1], r[2]))
+    else:
+        res.sort(key=lambda r: (r[0], r[1], weight_sum(r[5], wfine), r[2]))
     return res[:k], cands

@@ -314,3 +314,71 @@ def test_search_plain_definition_marginal_heavy(seed):
     got = [(x.score, x.sc, x.central_node, x.sm, x.nodes.tolist(), sorted(int(e) for e in x.edge_ids))
            for x in r.rpgs]
     assert got == [(x[0], x[1], x[2], x[3], x[4], x[5]) for x in ref]
+
+
+# ----------------------------------------------------------------- weight-sum tie-break (R29)
+def _tie_fixture():
+    d = load_golden("tie_break_weight_sum.json")
+    e = d["directed_edges"]
+    src = np.array([x[0] for x in e], np.uint32)
+    dst = np.array([x[1] for x in e], np.uint32)
+    wf = np.array([x[2] for x in e], np.float64)
+    act = np.full(len(e), d["activation"], np.uint8)
+    return d, src, dst, wf, act
+
+
+def test_tie_break_golden_fixture():
+    d, src, dst, wf, act = _tie_fixture()
+    g = O.Graph(d["nodes"], src, dst, act)
+    C = [np.array(x, np.uint32) for x in d["central"]]
+    for case in d["cases"]:
+        M = [np.array(x, np.uint32) for x in d["marginal"]] if case["marginal"] else []
+        r = O.search(g, C, M, case["k"], d["depth"], gamma=d["gamma"], tie_break=case["tie_break"], wfine=wf,
+                     beam_w=case.get("beam_w", 0), beam_mode=case.get("beam_mode", 0))
+        assert [x.central_node for x in r.rpgs] == case["expect"], case
+        for x, ws in zip(r.rpgs, case.get("wsum", [])):
+            assert abs(x.wsum / 2.0 ** 32 - ws) < 1e-8, (case, x.wsum)
+        for x, ed in zip(r.rpgs, case.get("edges", [])):
+            assert x.edge_ids.tolist() == ed
+
+
+def test_tie_break_exact_fixed_point():
+    # R29: W is exact (integer units of 2^-32), so it does not depend on the summation order
+    from fractions import Fraction
+    for w in (0.0, 1.0, 0.5, 0.1, 0.3, 1 / 3, 2 ** -33, 1 - 2 ** -40):
+        q = Fraction(w) * (1 << 32) + Fraction(1, 2)
+        assert brute.weight_sum([0], [w]) == q.numerator // q.denominator
+    assert brute.weight_sum([0, 0, 1], [0.25, 0.5]) == (1 << 30) + (1 << 31)  # distinct edges only
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_tie_break_matches_plain_definition(seed):
+    # weights from a coarse grid (k/8) so equal-score results often tie on W too (then v decides)
+    rng = np.random.default_rng(7700 + seed)
+    V, src, dst, act, _ = random_instance(rng, 6, 16, deg=2.4, amax=2)
+    wf = rng.integers(0, 9, len(src)) / 8.0
+    C, M = _random_query(rng, V, src, dst, act)
+    k = int(rng.choice([1, 2, 3, 5]))
+    g = O.Graph(V, src, dst, act)
+    r = O.search(g, C, M, k, 20, tie_break=1, wfine=wf)
+    ref, _ = brute.search_plain(V, src, dst, act, C, M, k, 20, wfine=wf)
+    got = [(x.score, x.sc, x.central_node, sorted(int(e) for e in x.edge_ids)) for x in r.rpgs]
+    assert got == [(x[0], x[1], x[2], x[5]) for x in ref]
+    assert [x.wsum for x in r.rpgs] == [brute.weight_sum(x[5], wf) for x in ref]
+    r2 = O.search(g, C, M, k, 20, tie_break=1, wfine=wf, early_term=2)
+    assert [(x.central_node, x.wsum) for x in r2.rpgs] == [(x.central_node, x.wsum) for x in r.rpgs]
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_tie_break_beam_truncation(seed):
+    # beam_mode 1 + tie-break keeps the w smallest (S^c, W(CG), v) of the tie-kept candidate set
+    rng = np.random.default_rng(7900 + seed)
+    V, src, dst, act, _ = random_instance(rng, 6, 18, deg=2.4, amax=2)
+    wf = rng.integers(0, 9, len(src)) / 8.0
+    C, M = _random_query(rng, V, src, dst, act)
+    g = O.Graph(V, src, dst, act)
+    bw = int(rng.integers(1, 4))
+    full = O.search(g, C, M, 1, 20, beam_w=bw, early_term=2)
+    keys = sorted((c.sc, brute.weight_sum(c.cg_edges, wf), c.v) for c in full.candidates)[:bw]
+    r = O.search(g, C, M, 1, 20, beam_w=bw, beam_mode=1, tie_break=1, wfine=wf, early_term=2)
+    assert [(c.sc, c.v) for c in r.candidates] == sorted((sc, v) for sc, _, v in keys)
