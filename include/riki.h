@@ -90,7 +90,10 @@ riki_status riki_get_activation_levels(const riki_graph *g, uint8_t *a);
  *   beam_w     beam width w of the first level [0 -> w = k]
  *   beam_mode  0 = keep every CG identified by the terminating level (ties, R13) [0];
  *              1 = truncate the candidate CGs to the first w by (S^c, v)
- *   tie_break  0 = (S^r, S^c, v) ascending (R23) [0]; others RIKI_ENOSYS
+ *   tie_break  0 = (S^r, S^c, v) ascending (R23) [0]; 1 = (S^r, S^c, W, v), W = sum of the
+ *              fine weights of the result's distinct edges as round(w * 2^32) (P:293 re-ranking,
+ *              R29; needs set_edge/node/label_weights, else RIKI_ENOWEIGHTS; with beam_mode 1
+ *              RIKI_ENOSYS)
  *   ptc_mode   0 = filter PTC failures, RPG-wide endpoint-inclusive (R19') [0];
  *              1 = keep failures, flagged ptc = 0; 2 = filter, PTC evaluated on G^m only;
  *              3 = filter, SPEC's exclusive form (V_C-resident marginal nodes never qualify)

@@ -57,7 +57,7 @@ struct SlotState {
     uint32_t T[2];
     uint32_t term[2][RIKI_MAX_TERMS];
     uint32_t k, w, depth;
-    uint32_t beam_mode, ptc_mode, early_term;
+    uint32_t beam_mode, ptc_mode, early_term, tie_break;
     double gamma;
     uint32_t in_phase, level;
     uint32_t nq[2];
@@ -68,6 +68,7 @@ struct SlotState {
     uint32_t n_attached, n_ptc_fail, nR, nres;
     uint32_t first_unatt, nR_sorted;  // run-2 bookkeeping (monotone cursor, sorted prefix of R)
     uint32_t err, active;
+    uint32_t ntie;  // tie-break (R29): results [0, ntie) whose order needs the weight sums
 };
 
 struct Cand {
@@ -75,6 +76,7 @@ struct Cand {
     uint32_t nodes_off, n_nodes, edges_off, n_edges, vc_off, n_vc;
     uint32_t attached, ptc, sm, ext;  // ext = caller id of v (ordering and output use caller ids)
     double sr;
+    unsigned long long wsum;  // tie-break (R29): W(G^r) (W(CG) when M is empty)
     uint8_t mdist[RIKI_MAX_TERMS];
 };
 
@@ -119,6 +121,7 @@ struct WsDev {
     unsigned long long big_words;
     uint4 *mtab;
     OutHdr *hdr;
+    uint2 *tie;  // tie-break scratch per slot (capc): (candidate, tie-group start)
     uint32_t *resid;
     uint32_t *out;
     unsigned long long *out_used, out_cap;
@@ -1970,7 +1973,9 @@ __global__ void k_decide_m(WsDev w, uint32_t l) {
             const u128 kth = w.RK(s)[st.k - 1];
             if (st.early_term == 0) {
                 u128 best = rkey(rpg_score(st.gamma, fu.sc, l + 1), fu.sc, fu.ext);
-                stop = kth < best;
+                // tie-break (R29): a candidate's W is unknown until it attaches, so only a
+                // strictly larger (S^r, S^c) excludes it
+                stop = st.tie_break ? (kth >> 32) < (best >> 32) : kth < best;
             } else {  // paper-literal inequality (Theorem earlyTermination)
                 uint64_t ck = (uint64_t)kth;  // (S^c << 32 | v) locates the k-th RPG's candidate
                 uint32_t lo = 0, hi = st.n_extract;
@@ -1994,7 +1999,14 @@ __global__ void k_final_select(WsDev w) {
         if (threadIdx.x == 0) st.nres = 0;
         return;
     }
-    if (st.T[1] == 0) {  // M = empty: top-k CGs by (S^c, v)
+    if (st.T[1] == 0 && st.tie_break) {  // M = empty with the tie-break: rank the CGs as keys
+        for (uint32_t i = threadIdx.x; i < st.n_extract; i += blockDim.x) {
+            const Cand &cd = w.CD(s)[i];
+            w.RK(s)[i] = rkey((double)cd.sc, cd.sc, cd.ext);  // already in (S^c, v) order
+        }
+        if (threadIdx.x == 0) st.nR = st.n_extract;
+        __syncthreads();
+    } else if (st.T[1] == 0) {  // M = empty: top-k CGs by (S^c, v)
         uint32_t n = min(st.k, st.n_extract);
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) w.resid[(size_t)s * w.kmax + i] = i;
         if (threadIdx.x == 0) st.nres = n;
@@ -2003,6 +2015,18 @@ __global__ void k_final_select(WsDev w) {
     uint32_t nR = min(st.nR, w.capc);
     cta_sort_u128(w.RK(s), nR, sm128, 1024);
     uint32_t n = min(st.k, nR);
+    if (st.tie_break) {  // R29: the order of [0, end of the k-th key's (S^r, S^c) group) needs W
+        if (threadIdx.x == 0) {
+            uint32_t e = n;
+            if (n) {
+                const u128 g = w.RK(s)[n - 1] >> 32;
+                while (e < nR && (w.RK(s)[e] >> 32) == g) e++;
+            }
+            st.ntie = e;
+            st.nres = n;
+        }
+        return;  // k_tie_weights + k_tie_select finish the selection
+    }
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
         u128 key = w.RK(s)[i];
         uint64_t ck = (uint64_t)key;  // (sc << 32 | v)
@@ -2012,6 +2036,77 @@ __global__ void k_final_select(WsDev w) {
         w.resid[(size_t)s * w.kmax + i] = lo;
     }
     if (threadIdx.x == 0) st.nres = n;
+}
+
+// Candidate index of an (S^r, S^c, v) key: CK is sorted by (S^c << 32 | caller id).
+__device__ __forceinline__ uint32_t cand_of_key(const WsDev &w, const SlotState &st, uint32_t s, u128 key) {
+    const uint64_t ck = (uint64_t)key;
+    uint32_t lo = 0, hi = st.n_extract;
+    const uint64_t *K = w.CK(s);
+    while (lo < hi) { uint32_t m = (lo + hi) >> 1; if (K[m] < ck) lo = m + 1; else hi = m; }
+    return lo;
+}
+
+// Tie-break (R29): W = sum of round(w * 2^32) over the DISTINCT edges of each result
+// in [0, ntie) (its edge list may repeat an edge shared by the CG and G^m).  Block per
+// result: the list is sorted in shared memory (arena for long lists), then reduced.
+__global__ void __launch_bounds__(256) k_tie_weights(GraphDev g, WsDev w) {
+    extern __shared__ __align__(16) uint32_t sm32[];
+    __shared__ unsigned long long acc;
+    __shared__ uint32_t s_buf;
+    const uint32_t s = blockIdx.y;
+    const SlotState &st = w.st[s];
+    if (!st.active || st.err || !st.tie_break) return;
+    for (uint32_t i = blockIdx.x; i < st.ntie; i += gridDim.x) {
+        const uint32_t c = cand_of_key(w, st, s, w.RK(s)[i]);
+        Cand &cd = w.CD(s)[c];
+        const uint32_t n = cd.n_edges;
+        uint32_t *buf = sm32;
+        if (next_pow2(n) > SORT_SMEM) {
+            if (threadIdx.x == 0) s_buf = arena_alloc(w, next_pow2(n), s);
+            __syncthreads();
+            if (s_buf == EMPTY) return;  // E_ARENA raised: the batch is re-run with a larger arena
+            buf = w.arena + s_buf;
+        }
+        if (threadIdx.x == 0) acc = 0;
+        for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) buf[j] = w.arena[cd.edges_off + j];
+        __syncthreads();
+        cta_bitonic_sort(buf, n);
+        unsigned long long part = 0;
+        for (uint32_t j = threadIdx.x; j < n; j += blockDim.x)
+            if (j == 0 || buf[j] != buf[j - 1]) part += g.wfix[buf[j]];
+        atomicAdd(&acc, part);
+        __syncthreads();
+        if (threadIdx.x == 0) cd.wsum = acc;
+        __syncthreads();
+    }
+}
+
+// Tie-break order: every tie group (equal (S^r, S^c)) of [0, ntie) re-sorted by (W, v); the
+// sort key is (group start << 96 | W << 32 | candidate index) -- within a group S^c is fixed,
+// so candidate index order is caller-id order.
+__global__ void k_tie_select(WsDev w) {
+    extern __shared__ __align__(16) u128 sm128[];
+    const uint32_t s = blockIdx.x;
+    const SlotState &st = w.st[s];
+    if (!st.active || st.err || !st.tie_break) return;
+    const uint32_t nt = st.ntie;
+    uint2 *T = w.tie + (size_t)s * w.capc;
+    u128 *K = w.RK(s);
+    for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) {
+        const u128 key = K[i], grp = key >> 32;
+        uint32_t lo = 0, hi = i;  // first index of i's group
+        while (lo < hi) { uint32_t m = (lo + hi) >> 1; if ((K[m] >> 32) < grp) lo = m + 1; else hi = m; }
+        T[i] = make_uint2(cand_of_key(w, st, s, key), lo);
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nt; i += blockDim.x) {
+        const uint2 t = T[i];
+        K[i] = (u128)t.y << 96 | (u128)w.CD(s)[t.x].wsum << 32 | t.x;
+    }
+    __syncthreads();
+    cta_sort_u128(K, nt, sm128, 1024);
+    for (uint32_t i = threadIdx.x; i < st.nres; i += blockDim.x) w.resid[(size_t)s * w.kmax + i] = (uint32_t)K[i];
 }
 
 // sort + unique a u32 list into the output buffer; returns (offset, count) via sh
@@ -2102,6 +2197,7 @@ __global__ void k_pack_H(GraphDev g, WsDev w, uint32_t T, uint8_t *Hout, uint8_t
 // ====================================================================== host side
 struct Workspace {
     uint32_t track_reached = 0;
+    uint32_t tie_break = 0;  // current batch uses the weight-sum tie-break (R29)
     uint32_t hnode = 0, SP = 0;  // H layout of the current batch
     uint32_t hcap[2] = {0, 0};   // bytes per H row allocated per run
     uint32_t cur = 0;  // slots used by the current batch (<= slots)
@@ -2118,7 +2214,7 @@ struct Workspace {
     SlotState *st = nullptr;
     uint4 *heavy = nullptr;
     unsigned long long *prof = nullptr, *arena_used = nullptr, *out_used = nullptr;
-    uint2 *newatt = nullptr, *ovf = nullptr, *ovf2 = nullptr;
+    uint2 *newatt = nullptr, *ovf = nullptr, *ovf2 = nullptr, *tie = nullptr;
     OutHdr *hdr = nullptr;
     uint32_t *h_ctr = nullptr;  // pinned
     uint64_t bytes = 0;
@@ -2171,7 +2267,7 @@ struct Workspace {
         d.arena = arena; d.arena_used = arena_used; d.arena_cap = arena_cap;
         d.newatt = newatt; d.ovf = ovf; d.ovf2 = ovf2; d.ovf_cap = ovf_cap;
         d.big = big; d.big_words = big_words; d.mtab = mtab;
-        d.hdr = hdr; d.resid = resid; d.out = out; d.out_used = out_used; d.out_cap = out_cap;
+        d.hdr = hdr; d.tie = tie; d.resid = resid; d.out = out; d.out_used = out_used; d.out_cap = out_cap;
         return d;
     }
 };
@@ -2253,6 +2349,7 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     ws->big = ws->alloc<uint32_t>(ws->big_words * ws->big_ctas);
     ws->hdr = ws->alloc<OutHdr>(S * c.kmax);
     ws->resid = ws->alloc<uint32_t>(S * c.kmax);
+    ws->tie = ws->alloc<uint2>(S * c.capc);
     ws->out = ws->alloc<uint32_t>(c.out);
     ws->out_used = ws->alloc<unsigned long long>(1);
     CUDA_TRY(cudaMallocHost(&ws->h_ctr, 64 * sizeof(uint32_t)));
@@ -2268,6 +2365,8 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
 #undef SET_EX_ATTR
         CUDA_TRY(cudaFuncSetAttribute(k_decide_m, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
         CUDA_TRY(cudaFuncSetAttribute(k_final_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
+        CUDA_TRY(cudaFuncSetAttribute(k_tie_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
+        CUDA_TRY(cudaFuncSetAttribute(k_tie_weights, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
         CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
         CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
         CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
@@ -2489,6 +2588,12 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     // ---- top-k and packing
     k_final_select<<<wd.nslots, 256, 1024 * 16, s>>>(wd);
     L.check();
+    if (ws->tie_break) {  // R29 weight-sum tie-break
+        k_tie_weights<<<dim3(64, wd.nslots), 256, SORT_SMEM * 4, s>>>(gd, wd);
+        L.check();
+        k_tie_select<<<wd.nslots, 256, 1024 * 16, s>>>(wd);
+        L.check();
+    }
     k_final_lists<RowC><<<dim3(ws->kmax, wd.nslots), 256, SORT_SMEM * 4, s>>>(gd, wd);
     L.check();
     if (L.g->profiling) CUDA_TRY(cudaStreamSynchronize(s));
@@ -2563,6 +2668,7 @@ SlotState make_template(uint32_t k, uint32_t depth, const riki_params &p) {
     t.w = p.beam_w ? p.beam_w : k;
     t.depth = depth;
     t.beam_mode = p.beam_mode;
+    t.tie_break = p.tie_break;
     t.ptc_mode = p.ptc_mode;
     t.early_term = p.early_term;
     t.gamma = p.gamma;
@@ -2579,7 +2685,7 @@ uint32_t auto_slots(riki_graph *g, uint32_t nq, uint32_t rb0, uint32_t rb1) {
     if (g->ws && g->ws->slots >= want && g->ws->hcap[0] >= rb0 && g->ws->hcap[1] >= rb1) return want;
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
-    uint64_t per = (uint64_t)g->V * (rb0 + rb1 + 8) + 16384ull * (8 + sizeof(Cand) + 16 + 8) +
+    uint64_t per = (uint64_t)g->V * (rb0 + rb1 + 8) + 16384ull * (8 + sizeof(Cand) + 16 + 8 + 8) +
                    16ull * 8192 * 16 + 64 * 1024;
     uint64_t budget = fr > (4ull << 30) ? (fr - (4ull << 30)) / 2 : fr / 4;
     uint32_t fit = (uint32_t)std::max<uint64_t>(1, budget / std::max<uint64_t>(per, 1));
@@ -2729,7 +2835,11 @@ static void check_common(riki_graph *g, uint32_t k, uint32_t depth, const riki_p
     if (depth > RIKI_MAX_DEPTH) RIKI_THROW(RIKI_EDEPTH, "depth must be <= 254");
     if (!(p.gamma >= 0.0 && p.gamma <= 1.0)) RIKI_THROW(RIKI_EINVAL, "gamma must be in [0,1]");
     if (p.beam_mode < 0 || p.beam_mode > 1) RIKI_THROW(RIKI_EINVAL, "beam_mode must be 0 or 1");
-    if (p.tie_break != 0) RIKI_THROW(RIKI_ENOSYS, "tie_break != 0 not implemented");
+    if (p.tie_break != 0 && p.tie_break != 1) RIKI_THROW(RIKI_EINVAL, "tie_break must be 0 or 1");
+    if (p.tie_break == 1 && !g->d_wfix)
+        RIKI_THROW(RIKI_ENOWEIGHTS, "tie_break 1 needs the fine edge weights (set_edge/node/label_weights)");
+    if (p.tie_break == 1 && p.beam_mode == 1)
+        RIKI_THROW(RIKI_ENOSYS, "tie_break 1 with beam_mode 1 (beam truncated by W(CG)) is not implemented on the GPU");
     if (p.ptc_mode < 0 || p.ptc_mode > 3) RIKI_THROW(RIKI_EINVAL, "ptc_mode must be 0..3");
     if (p.early_term < 0 || p.early_term > 2) RIKI_THROW(RIKI_EINVAL, "early_term must be 0..2");
     if (p.beam_w && p.beam_w < k) RIKI_THROW(RIKI_EINVAL, "beam width must be >= k (P:309)");
@@ -2786,6 +2896,7 @@ void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, ui
                 Workspace *ws = g->ws;
                 ws->last_rb[0] = row_bytes(maxc);
                 ws->last_rb[1] = row_bytes(maxm);
+                ws->tie_break = tmpl.tie_break;
                 ws->cur = n;
                 set_layout(g, ws, n);
                 std::vector<SlotState> h(n, tmpl);
@@ -2850,6 +2961,7 @@ void engine_search_device(riki_graph *g, uint32_t nq, const uint64_t *d_cptr, co
         Workspace *ws = g->ws;
         ws->last_rb[0] = row_bytes(maxc);
         ws->last_rb[1] = row_bytes(maxm);
+        ws->tie_break = tmpl.tie_break;
         ws->cur = nq;
         set_layout(g, ws, nq);
         k_slots_from_device<<<(nq + 127) / 128, 128, 0, L.s>>>(ws->st, nq, 0, nq, d_cptr, d_cterms,

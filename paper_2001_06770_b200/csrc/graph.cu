@@ -59,6 +59,16 @@ __global__ void k_coarsen_nodes(const double *w, const uint32_t *dst, const uint
     }
 }
 
+// R29 (tie-break): the fine weight of every caller edge as the exact integer
+// round(w * 2^32) (w * 2^32 is exact in fp64), so weight sums are order independent.
+__global__ void k_wfix(const double *w, const uint32_t *dst, const uint32_t *iperm, uint64_t n,
+                       unsigned long long *out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        double x = dst ? w[iperm[dst[i]]] : w[i];  // node variant: w of the edge's target
+        out[i] = (unsigned long long)floor(__dadd_rn(__dmul_rn(x, 4294967296.0), 0.5));
+    }
+}
+
 __global__ void k_make_keys(const uint32_t *node, const uint32_t *cls, uint64_t n, uint64_t *key, uint32_t *val) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         key[i] = (uint64_t)node[i] << 32 | cls[i];
@@ -369,7 +379,7 @@ void graph_load(riki_graph *g, uint32_t V, uint64_t E, const uint32_t *src, cons
 
 void graph_free(riki_graph *g) {
     void *ps[] = {g->d_src, g->d_dst, g->d_cls, g->d_act_e, g->d_row, g->d_col, g->d_act, g->d_desc,
-                  g->d_irow, g->d_isrc, g->d_ieid, g->d_iact, g->d_tptr, g->d_post, g->d_perm, g->d_iperm, g->d_aoff, g->d_idesc, g->d_iaoff};
+                  g->d_irow, g->d_isrc, g->d_ieid, g->d_iact, g->d_tptr, g->d_post, g->d_perm, g->d_iperm, g->d_aoff, g->d_idesc, g->d_iaoff, g->d_wfix};
     for (void *p : ps) if (p) cudaFree(p);
     if (g->stream) cudaStreamDestroy(g->stream);
 }
@@ -383,6 +393,12 @@ static void finish_act(riki_graph *g, uint32_t *d_bad) {
     build_csr(g);
 }
 
+// Keeps the fine weights (fixed point, by caller edge id) for the tie-break (R29).
+static void keep_wfix(riki_graph *g, const double *dw, const uint32_t *dst) {
+    if (!g->d_wfix && g->E) g->d_wfix = dmalloc<unsigned long long>(g->E);
+    if (g->E) k_wfix<<<grid_for(g->E), 256, 0, g->stream>>>(dw, dst, g->d_iperm, g->E, g->d_wfix);
+}
+
 void graph_set_edge_weights(riki_graph *g, const double *w01, double alpha, double avg) {
     check_params(alpha, avg);
     if (g->E && !w01) RIKI_THROW(RIKI_EINVAL, "null weights");
@@ -391,6 +407,7 @@ void graph_set_edge_weights(riki_graph *g, const double *w01, double alpha, doub
     CUDA_TRY(cudaMemsetAsync(bad, 0, 4, g->stream));
     if (g->E) CUDA_TRY(cudaMemcpyAsync(dw, w01, g->E * 8, cudaMemcpyHostToDevice, g->stream));
     k_coarsen_edges<<<grid_for(g->E), 256, 0, g->stream>>>(dw, g->E, alpha, avg, g->d_act_e, bad);
+    keep_wfix(g, dw, nullptr);
     sync_check(g->stream);
     cudaFree(dw);
     finish_act(g, bad);
@@ -404,6 +421,7 @@ void graph_set_node_weights(riki_graph *g, const double *w01, double alpha, doub
     CUDA_TRY(cudaMemsetAsync(bad, 0, 4, g->stream));
     CUDA_TRY(cudaMemcpyAsync(dw, w01, (size_t)g->V * 8, cudaMemcpyHostToDevice, g->stream));
     k_coarsen_nodes<<<grid_for(g->E), 256, 0, g->stream>>>(dw, g->d_dst, g->d_iperm, g->E, alpha, avg, g->d_act_e, bad);
+    keep_wfix(g, dw, g->d_dst);
     sync_check(g->stream);
     cudaFree(dw);
     finish_act(g, bad);
@@ -443,6 +461,7 @@ void graph_set_label_weights(riki_graph *g, double alpha, double avg) {
     uint32_t *bad = dmalloc<uint32_t>(1);
     CUDA_TRY(cudaMemsetAsync(bad, 0, 4, s));
     k_coarsen_edges<<<grid_for(E), 256, 0, s>>>(w, E, alpha, avg, g->d_act_e, bad);
+    keep_wfix(g, w, nullptr);
     sync_check(s);
     cudaFree(t); cudaFree(raw); cudaFree(w); cudaFree(mm); cudaFree(co); cudaFree(ci);
     finish_act(g, bad);
@@ -454,6 +473,10 @@ void graph_set_act(riki_graph *g, const uint8_t *a) {
         if (a[e] == 0xFF) RIKI_THROW(RIKI_EINVAL, "activation 255 is reserved");
     if (g->E) CUDA_TRY(cudaMemcpyAsync(g->d_act_e, a, g->E, cudaMemcpyHostToDevice, g->stream));
     sync_check(g->stream);
+    if (g->d_wfix) {  // activation levels without fine weights: no weight-sum tie-break (R29)
+        cudaFree(g->d_wfix);
+        g->d_wfix = nullptr;
+    }
     build_csr(g);
 }
 

@@ -55,6 +55,7 @@ struct GraphDev {
     const uint64_t *tptr;       // inverted index (internal ids)
     const uint32_t *post;
     const uint32_t *perm, *iperm;  // caller id -> internal id (degree-descending), and back
+    const unsigned long long *wfix;  // fine weight of each caller edge id as round(w * 2^32) (tie-break R29), or null
     uint32_t Vh;                   // internal ids [0, Vh) have in-degree > 32 (pull: warp per node)
 };
 
@@ -80,6 +81,7 @@ struct riki_graph {
     uint64_t *d_tptr = nullptr;
     uint32_t *d_post = nullptr;
     uint32_t *d_perm = nullptr, *d_iperm = nullptr;
+    unsigned long long *d_wfix = nullptr;  // set with the fine weights (set_edge/node/label_weights)
     uint32_t Vh = 0;
     std::vector<uint64_t> h_tptr;
     uint64_t graph_bytes = 0;
@@ -96,6 +98,7 @@ struct riki_graph {
         g.row = d_row; g.col = d_col; g.act = d_act; g.desc = d_desc; g.aoff = d_aoff; g.idesc = d_idesc; g.iaoff = d_iaoff;
         g.irow = d_irow; g.isrc = d_isrc; g.ieid = d_ieid; g.iact = d_iact;
         g.src = d_src; g.dst = d_dst; g.tptr = d_tptr; g.post = d_post; g.perm = d_perm; g.iperm = d_iperm; g.Vh = Vh;
+        g.wfix = d_wfix;
         return g;
     }
 };
