@@ -92,8 +92,8 @@ riki_status riki_get_activation_levels(const riki_graph *g, uint8_t *a);
  *              1 = truncate the candidate CGs to the first w by (S^c, v)
  *   tie_break  0 = (S^r, S^c, v) ascending (R23) [0]; 1 = (S^r, S^c, W, v), W = sum of the
  *              fine weights of the result's distinct edges as round(w * 2^32) (P:293 re-ranking,
- *              R29; needs set_edge/node/label_weights, else RIKI_ENOWEIGHTS; with beam_mode 1
- *              RIKI_ENOSYS)
+ *              R29; needs set_edge/node/label_weights, else RIKI_ENOWEIGHTS); with beam_mode 1
+ *              the beam keeps the w smallest (S^c, W(CG), v)
  *   ptc_mode   0 = filter PTC failures, RPG-wide endpoint-inclusive (R19') [0];
  *              1 = keep failures, flagged ptc = 0; 2 = filter, PTC evaluated on G^m only;
  *              3 = filter, SPEC's exclusive form (V_C-resident marginal nodes never qualify)
@@ -141,7 +141,10 @@ riki_status riki_rpq_search_batch(riki_graph *g, uint32_t n_queries,
 /* Device-resident batch (benchmark / pipeline path): identical computation, but the query
  * arrays are DEVICE pointers and results stay on the device (no D2H); results are
  * retrievable afterwards with riki_batch_fetch (which performs the D2H).  Returns after
- * the work has been enqueued and completed on the library stream. */
+ * the work has been enqueued and completed on the library stream.  A batch larger than the
+ * slots that fit in flight (frontier items of a level must be 32-bit indexable: slots x
+ * queue capacity < 2^32; the recovery arena must stay below 2^32 words) runs in chunks,
+ * and then each chunk's results are copied to the host before the next chunk runs. */
 riki_status riki_rpq_search_batch_device(riki_graph *g, uint32_t n_queries,
                                          const uint64_t *d_c_ptr, const uint32_t *d_c_terms,
                                          const uint64_t *d_m_ptr, const uint32_t *d_m_terms,
@@ -237,6 +240,11 @@ riki_status riki_set_direction(riki_graph *g, int mode);
 riki_status riki_set_joint(riki_graph *g, int on);
 /* Batch slots (queries in flight per launch); 0 = automatic from free device memory. */
 riki_status riki_set_batch_slots(riki_graph *g, uint32_t slots);
+/* Recovery-arena limit in 32-bit words (0 = default: the 2^32 addressable by its offsets).
+ * A batch whose recovered subgraphs and memoised predecessor lists (Alg. 2) need more runs
+ * in chunks of fewer queries; a device batch that ran in chunks has its results collected
+ * to the host per chunk (riki_batch_fetch returns them as usual).  Tests use small limits. */
+riki_status riki_set_arena_limit(riki_graph *g, uint64_t words);
 /* device memory footprint of the resident graph and of the search workspace (bytes) */
 riki_status riki_memory_footprint(const riki_graph *g, uint64_t *graph_bytes, uint64_t *workspace_bytes);
 

@@ -307,6 +307,14 @@ riki_status riki_set_joint(riki_graph *g, int on) {
     });
 }
 
+riki_status riki_set_arena_limit(riki_graph *g, uint64_t words) {
+    return guard([&] {
+        need(g, "null graph");
+        need(words == 0 || words >= 4096, "arena limit must be 0 or >= 4096 words");
+        g->arena_limit = words;
+    });
+}
+
 riki_status riki_dist_unique_id(void *out128) {
     return guard([&] {
         need(out128 != nullptr, "null output");

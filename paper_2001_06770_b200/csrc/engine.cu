@@ -47,7 +47,12 @@ enum Ctr { C_NHEAVY = 0, C_NNEWATT, C_NOVF, C_ACTIVE, C_TOTAL, C_NCAND_TOTAL, C_
 enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_PULLNODES, P_PULLEDGES,
             // recovery diagnostics (compiled in with -DREC_STATS=1)
             P_R_BUILDS = 8, P_R_BEDGES, P_R_BCYC, P_R_WAITS, P_R_WCYC, P_R_CANDS, P_R_CANDCYC, P_R_CANDMAX, P_R_BMAX,
-            P_R_ITEMS, P_R_WARPMAX, P_R_H0, P_NPROF = 32 };  // P_R_H0..+5: candidate-time histogram
+            P_R_ITEMS, P_R_WARPMAX, P_R_H0,  // P_R_H0..+5: candidate-time histogram
+            // expansion item diagnostics (compiled in with -DEXP_STATS=1)
+            P_X_DUP = 24, P_X_BLOCKED, P_X_IDLE, P_X_WORK, P_NPROF = 32 };
+#ifndef EXP_STATS
+#define EXP_STATS 0
+#endif
 #ifndef REC_STATS
 #define REC_STATS 0
 #endif
@@ -107,7 +112,8 @@ struct WsDev {
     uint64_t *ck;
     Cand *cd;
     u128 *rk;
-    uint32_t *offs, *coffs, *pslots;
+    uint32_t *offs;  // frontier-item prefix over the slots (< 2^32: slots x qcap is bounded, max_slots_for)
+    uint32_t *coffs, *pslots;
     uint32_t track_reached;  // direction-optimising mode: count new nodes per slot
     uint4 *heavy;
     uint32_t heavy_cap;
@@ -159,7 +165,7 @@ __device__ __forceinline__ u128 rkey(double sr, uint32_t sc, uint32_t v) {
     return (u128)(unsigned long long)__double_as_longlong(sr) << 64 | (u128)sc << 32 | v;
 }
 
-__device__ __forceinline__ uint32_t find_slot(const uint32_t *offs, uint32_t n, uint32_t item) {
+template <class T> __device__ __forceinline__ uint32_t find_slot(const T *offs, uint32_t n, T item) {
     // largest s with offs[s] <= item (offs non-decreasing, offs[n] = total)
     uint32_t lo = 0, hi = n;
     while (hi - lo > 1) {
@@ -171,7 +177,7 @@ __device__ __forceinline__ uint32_t find_slot(const uint32_t *offs, uint32_t n, 
 
 // Warp-uniform form: largest s < n with offs[s] <= item for the same `item` in every lane
 // (n <= 32 * 32): a 32-way ballot over every stride-th boundary, then one over the stride.
-__device__ __forceinline__ uint32_t find_slot_warp(const uint32_t *offs, uint32_t n, uint32_t item) {
+template <class T> __device__ __forceinline__ uint32_t find_slot_warp(const T *offs, uint32_t n, T item) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t stride = (n + 31) >> 5;
     const uint32_t j = lane * stride;
@@ -572,7 +578,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
     uint32_t p_edges = 0, p_cells = 0;  // items and queue entries are counted by k_plan
 
     for (uint32_t base = gw * 32; base < total; base += nw * 32) {
-        uint32_t item = base + lane;
+        const uint32_t item = base + lane;
         bool valid = item < total;
         // slots of this warp's 32 items: two warp-uniform searches, then (rarely) a short
         // per-lane search between them
@@ -591,6 +597,10 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
             RowT used = used_mask<RowT>(info >> 8);
             bool dup = (ent & RETAINED) && (R::eq(Rf, L) & used);
             bool blocked = (info & 1) && R::le(Rf, L) == (RowT)~(RowT)0;  // CF: row complete, max <= l
+#if EXP_STATS
+            if (dup) atomicAdd(&w.prof[P_X_DUP], 1ull);
+            else if (blocked) atomicAdd(&w.prof[P_X_BLOCKED], 1ull);
+#endif
             if (!dup && !blocked) {
                 newc = R::eq(Rf, L) & used;   // reached at level l (or seeds at l = 0)
                 oldc = R::lt(Rf, L) & used;   // reached earlier: only edges with a == l are due now
@@ -603,6 +613,9 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
                     eq0 = eqlo;
                     len = hi - lo;
                     relaxn = (hi - rb) * R::ones(newc) + (hi - eqlo) * R::ones(oldc);
+#if EXP_STATS
+                    atomicAdd(&w.prof[len ? P_X_WORK : P_X_IDLE], 1ull);
+#endif
                     if (info & 4) len = 0;  // pull slot: relaxed bottom-up by k_pull
                     p_edges += len;
                     if (len > HEAVY) {
@@ -1197,8 +1210,10 @@ __global__ void k_cand_sort(GraphDev g, WsDev w) {
     }
     uint32_t n = min(st.ncand, w.capc);
     cta_sort_u64(w.CK(s), n, sm64, 4096);
-    uint32_t kept = st.beam_mode == 1 ? min(n, st.w) : n;
-    uint32_t nex = st.T[1] == 0 ? min(kept, st.k) : kept;
+    // beam_mode 1 with the tie-break (R29) truncates by (S^c, W(CG), v) after recovery
+    const bool beam_tie = st.beam_mode == 1 && st.tie_break;
+    uint32_t kept = st.beam_mode == 1 && !beam_tie ? min(n, st.w) : n;
+    uint32_t nex = st.T[1] == 0 && !st.tie_break ? min(kept, st.k) : kept;
     for (uint32_t i = threadIdx.x; i < nex; i += blockDim.x) {
         uint64_t key = w.CK(s)[i];
         Cand c;
@@ -2048,17 +2063,19 @@ __device__ __forceinline__ uint32_t cand_of_key(const WsDev &w, const SlotState 
 }
 
 // Tie-break (R29): W = sum of round(w * 2^32) over the DISTINCT edges of each result
-// in [0, ntie) (its edge list may repeat an edge shared by the CG and G^m).  Block per
-// result: the list is sorted in shared memory (arena for long lists), then reduced.
-__global__ void __launch_bounds__(256) k_tie_weights(GraphDev g, WsDev w) {
+// in [0, ntie) (its edge list may repeat an edge shared by the CG and G^m) -- or, with
+// cgs = true, of every recovered candidate CG of a beam_mode-1 slot.  Block per item: the
+// list is sorted in shared memory (arena for long lists), then reduced.
+__global__ void __launch_bounds__(256) k_tie_weights(GraphDev g, WsDev w, bool cgs) {
     extern __shared__ __align__(16) uint32_t sm32[];
     __shared__ unsigned long long acc;
     __shared__ uint32_t s_buf;
     const uint32_t s = blockIdx.y;
     const SlotState &st = w.st[s];
-    if (!st.active || st.err || !st.tie_break) return;
-    for (uint32_t i = blockIdx.x; i < st.ntie; i += gridDim.x) {
-        const uint32_t c = cand_of_key(w, st, s, w.RK(s)[i]);
+    if (!st.active || st.err || !st.tie_break || (cgs && st.beam_mode != 1)) return;
+    const uint32_t nitems = cgs ? st.n_extract : st.ntie;
+    for (uint32_t i = blockIdx.x; i < nitems; i += gridDim.x) {
+        const uint32_t c = cgs ? i : cand_of_key(w, st, s, w.RK(s)[i]);
         Cand &cd = w.CD(s)[c];
         const uint32_t n = cd.n_edges;
         uint32_t *buf = sm32;
@@ -2079,6 +2096,43 @@ __global__ void __launch_bounds__(256) k_tie_weights(GraphDev g, WsDev w) {
         __syncthreads();
         if (threadIdx.x == 0) cd.wsum = acc;
         __syncthreads();
+    }
+}
+
+// Beam of width w with the tie-break (R29): keep the w smallest (S^c, W(CG), v) of the
+// recovered tie-kept candidates, compacted in (S^c, v) order (candidate index order).
+// RK is free before run 2 and serves as sort space.
+__global__ void k_beam_tie(WsDev w) {
+    extern __shared__ __align__(16) u128 sm128[];
+    const uint32_t s = blockIdx.x;
+    SlotState &st = w.st[s];
+    if (!st.active || st.err || !st.tie_break || st.beam_mode != 1) return;
+    const uint32_t n = st.n_extract, keep = min(n, st.w);
+    if (n > keep) {
+        u128 *K = w.RK(s);
+        Cand *CD = w.CD(s);
+        uint64_t *CK = w.CK(s);
+        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+            K[i] = (u128)CD[i].sc << 96 | (u128)CD[i].wsum << 32 | i;
+        __syncthreads();
+        cta_sort_u128(K, n, sm128, 1024);
+        for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) K[i] = (uint32_t)K[i];
+        __syncthreads();
+        cta_sort_u128(K, keep, sm128, 1024);  // kept indices ascending = (S^c, v) order
+        // compaction in place: source index K[j] >= j; chunk reads happen before chunk writes
+        for (uint32_t j0 = 0; j0 < keep; j0 += blockDim.x) {
+            const uint32_t j = j0 + threadIdx.x;
+            Cand cd;
+            uint64_t ck = 0;
+            if (j < keep) { cd = CD[(uint32_t)K[j]]; ck = CK[(uint32_t)K[j]]; }
+            __syncthreads();
+            if (j < keep) { CD[j] = cd; CK[j] = ck; }
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) {
+        st.n_extract = keep;
+        st.ncand_kept = keep;
     }
 }
 
@@ -2198,6 +2252,7 @@ __global__ void k_pack_H(GraphDev g, WsDev w, uint32_t T, uint8_t *Hout, uint8_t
 struct Workspace {
     uint32_t track_reached = 0;
     uint32_t tie_break = 0;  // current batch uses the weight-sum tie-break (R29)
+    uint32_t beam_tie = 0;   // ... with beam_mode 1 (beam truncated by W(CG))
     uint32_t hnode = 0, SP = 0;  // H layout of the current batch
     uint32_t hcap[2] = {0, 0};   // bytes per H row allocated per run
     uint32_t cur = 0;  // slots used by the current batch (<= slots)
@@ -2299,6 +2354,14 @@ struct Caps {
     uint32_t rb[2];  // bytes per H row needed by each run
 };
 
+constexpr uint64_t ARENA_MAX_WORDS = 0xFFFFFF00ull;  // largest arena addressable by u32 offsets
+
+// Slots in flight such that the frontier items of one level (<= slots x qcap queue entries)
+// are indexable with 32 bits (k_plan's prefix, k_expand's item index).
+uint32_t max_slots_for(uint32_t qcap) {
+    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(MAX_SLOTS, 0xFFFFFFFFull / std::max(qcap, 1u)));
+}
+
 void ensure_workspace(riki_graph *g, const Caps &c) {
     Workspace *ws = g->ws;
     if (ws && ws->slots >= c.slots && ws->V == g->V && ws->capc >= c.capc && ws->kmax >= c.kmax &&
@@ -2308,6 +2371,9 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     uint32_t hb0 = std::max<uint32_t>(c.rb[0], ws ? ws->hcap[0] : 0), hb1 = std::max<uint32_t>(c.rb[1], ws ? ws->hcap[1] : 0);
     if (ws) { ws->release(); delete ws; g->ws = nullptr; }
     g->stats.reallocs++;
+    if (getenv("RIKI_TRACE"))
+        fprintf(stderr, "[riki] workspace: slots %u capc %u kmax %u qcap %u arena %llu words out %llu rb %u/%u\n", c.slots,
+                c.capc, c.kmax, c.qcap, (unsigned long long)c.arena, (unsigned long long)c.out, c.rb[0], c.rb[1]);
     ws = new Workspace();
     g->ws = ws;
     const uint32_t V = g->V;
@@ -2366,6 +2432,7 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
         CUDA_TRY(cudaFuncSetAttribute(k_decide_m, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
         CUDA_TRY(cudaFuncSetAttribute(k_final_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
         CUDA_TRY(cudaFuncSetAttribute(k_tie_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
+        CUDA_TRY(cudaFuncSetAttribute(k_beam_tie, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
         CUDA_TRY(cudaFuncSetAttribute(k_tie_weights, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
         CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
         CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
@@ -2394,9 +2461,12 @@ struct Launch {
         sec_ms[sec] += std::chrono::duration<double, std::milli>(t - t0).count();
         t0 = t;
     }
-    void check() {
+    void check(int line) {
         cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) RIKI_THROW(RIKI_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+        static const bool sync_each = getenv("RIKI_SYNC") != nullptr;  // diagnostics: fault -> launch site
+        if (e == cudaSuccess && sync_each) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess)
+            RIKI_THROW(RIKI_ECUDA, std::string("kernel launch (engine.cu:") + std::to_string(line) + "): " + cudaGetErrorString(e));
         launches++;
     }
 };
@@ -2433,13 +2503,13 @@ void vp_level(Launch &L, const GraphDev &gd, const WsDev &wd, int ph, uint32_t l
         const uint32_t ll = std::max(lo, gd.Vh);
         const uint32_t nbl = hi > ll ? std::min<uint32_t>((hi - ll + 255) / 256, 148 * 8) : 0;
         k_pull<RowT><<<dim3(nbh + nbl, npull), 256, 0, s>>>(gd, wd, ph, l, nbh, lo, hi, x + chunk * r, d->wc);
-        L.check();
+        L.check(__LINE__);
     }
     dist_allgather(L.g, x, chunk, s);
     const uint64_t total = (uint64_t)d->nranks * d->wc * 32;
     k_vp_apply<RowT><<<dim3((uint32_t)std::min<uint64_t>((total + 255) / 256, 148 * 8), npull), 256, 0, s>>>(
         gd, wd, ph, l, x, d->wc, d->nranks, d->d_bounds, npull);
-    L.check();
+    L.check(__LINE__);
 }
 
 // Runs one exploration loop over all slots (lock-step).  For run 2 the per-level attach /
@@ -2453,43 +2523,43 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
     ws->track_reached = L.g->pull_on ? 1 : 0;
     WsDev wd = ws->dev();
     k_phase_begin<<<(wd.nslots + 127) / 128, 128, 0, s>>>(wd, ph, hitting_mode);
-    L.check();
+    L.check(__LINE__);
     bool joint = false;
     if constexpr (sizeof(RowT) <= 4) joint = wd.hnode != 0;
     if (joint) {
         if constexpr (sizeof(RowT) <= 4) {
             k_fill_H_nodemajor<RowT><<<148 * 16, 256, 0, s>>>(wd, ph);
-            L.check();
+            L.check(__LINE__);
         }
         CUDA_TRY(cudaMemsetAsync(ws->ctr + C_JQN0, 0, 8, s));
     } else {
         k_fill_H<RowT><<<dim3(grid_of(ws->V, 256, 64), wd.nslots), 256, 0, s>>>(wd, ph);
-        L.check();
+        L.check(__LINE__);
     }
     k_seed<RowT><<<dim3(16, wd.nslots), 256, 0, s>>>(gd, wd, ph);
-    L.check();
+    L.check(__LINE__);
     // The host checks for termination only every LEVEL_BATCH levels: all per-level kernels
     // use fixed grids and read their work counts on the device, so levels past a slot's end
     // are device-side no-ops and the number of host synchronisations per run drops ~4x.
     for (uint32_t l = 0; l <= max_levels; l++) {
         if (ph == 1) {
             k_reset_level_ctrs<<<1, 1, 0, s>>>(wd);
-            L.check();
+            L.check(__LINE__);
             if (total_cands) {
                 k_attach<RowT><<<grid_of(total_cands * 32, 256), 256, 0, s>>>(wd);
-                L.check();
+                L.check(__LINE__);
                 k_extract_rpg<RowT, 0><<<148 * tier0_blocks_per_sm(k_extract_rpg<RowT, 0>), tier_threads<0>(), smem_ex<0>(), s>>>(gd, wd);
-                L.check();
+                L.check(__LINE__);
                 k_extract_rpg<RowT, 1><<<148 * 3, 256, smem_ex<1>(), s>>>(gd, wd);
-                L.check();
+                L.check(__LINE__);
                 k_extract_rpg_big<RowT><<<ws->big_ctas, 256, 0, s>>>(gd, wd);
-                L.check();
+                L.check(__LINE__);
             }
             k_decide_m<<<wd.nslots, 256, 1024 * 16, s>>>(wd, l);
-            L.check();
+            L.check(__LINE__);
         }
         k_plan<<<1, MAX_SLOTS, 0, s>>>(wd, ph, l, vp ? 0u : !L.g->pull_on ? 0xFFFFFFFFu : std::max<uint32_t>(ws->V / PULL_MIN_DIV, 1));
-        L.check();
+        L.check(__LINE__);
         if (l % LEVEL_BATCH == LEVEL_BATCH - 1 || l == max_levels || pull) {
             CUDA_TRY(cudaMemcpyAsync(ws->h_ctr, ws->ctr, C_NCTR * 4, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
@@ -2500,15 +2570,15 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
         if (joint) {
             if constexpr (sizeof(RowT) <= 4) {
                 k_jexpand<RowT, false><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
-                L.check();
+                L.check(__LINE__);
                 k_jexpand<RowT, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
-                L.check();
+                L.check(__LINE__);
             }
         } else {
             k_expand<RowT><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
-            L.check();
+            L.check(__LINE__);
             k_expand_heavy<RowT><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
-            L.check();
+            L.check(__LINE__);
         }
         if (vp) {
             if (uint32_t npull = ws->h_ctr[C_NPULL]) vp_level<RowT>(L, gd, wd, ph, l, npull);
@@ -2518,7 +2588,7 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
                 uint32_t nbl = std::min<uint32_t>((ws->V - gd.Vh + 255) / 256, 148 * 8);
                 k_pull<RowT><<<dim3(nbh + std::max<uint32_t>(nbl, 1), npull), 256, 0, s>>>(gd, wd, ph, l, nbh, 0u, ws->V,
                                                                                            nullptr, 0u);
-                L.check();
+                L.check(__LINE__);
             }
         }
         if (L.g->profiling) {  // events are read after the batch: no extra sync per level
@@ -2534,15 +2604,18 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             CUDA_TRY(cudaMemcpyAsync(pr, ws->prof, sizeof(pr), cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
             if (l == 0) memcpy(last, pr, sizeof(pr));
-            fprintf(stderr, "[riki-level] ph=%d l=%u active=%u items=%u heavy_chunks=%u edges=%llu cells=%llu\n", ph, l,
-                    c[C_ACTIVE], c[C_TOTAL], c[C_NHEAVY], pr[P_EDGES] - last[P_EDGES], pr[P_NEWCELLS] - last[P_NEWCELLS]);
+            fprintf(stderr, "[riki-level] ph=%d l=%u active=%u items=%u heavy_chunks=%u edges=%llu cells=%llu"
+                            " dup=%llu blocked=%llu idle=%llu work=%llu\n", ph, l,
+                    c[C_ACTIVE], c[C_TOTAL], c[C_NHEAVY], pr[P_EDGES] - last[P_EDGES], pr[P_NEWCELLS] - last[P_NEWCELLS],
+                    pr[P_X_DUP] - last[P_X_DUP], pr[P_X_BLOCKED] - last[P_X_BLOCKED], pr[P_X_IDLE] - last[P_X_IDLE],
+                    pr[P_X_WORK] - last[P_X_WORK]);
             memcpy(last, pr, sizeof(pr));
         }
     }
     if (joint) {
         k_jclear<<<64, 256, 0, s>>>(wd, 0);
         k_jclear<<<64, 256, 0, s>>>(wd, 1);
-        L.check();
+        L.check(__LINE__);
     }
 }
 
@@ -2565,20 +2638,28 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     L.mark(0);
     // ---- candidate CGs + recovery
     k_cand_sort<<<wd.nslots, 1024, 4096 * 8, s>>>(gd, wd);
-    L.check();
+    L.check(__LINE__);
     k_scan_cands<<<1, MAX_SLOTS, 0, s>>>(wd);
-    L.check();
+    L.check(__LINE__);
     CUDA_TRY(cudaMemcpyAsync(ws->h_ctr, ws->ctr, C_NCTR * 4, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     uint64_t total_cands = ws->h_ctr[C_NCAND_TOTAL];
     if (total_cands) {
         k_extract_cg<RowC, 0><<<grid_of(total_cands, Tier<0>::GROUPS, 148 * tier0_blocks_per_sm(k_extract_cg<RowC, 0>)), tier_threads<0>(),
                                  smem_ex<0>(), s>>>(gd, wd);
-        L.check();
+        L.check(__LINE__);
         k_extract_cg<RowC, 1><<<148 * 3, 256, smem_ex<1>(), s>>>(gd, wd);
-        L.check();
+        L.check(__LINE__);
         k_extract_cg_big<RowC><<<ws->big_ctas, 256, 0, s>>>(gd, wd);
-        L.check();
+        L.check(__LINE__);
+    }
+    if (ws->beam_tie) {  // beam_mode 1 + tie-break (R29): truncate the recovered beam by W(CG)
+        k_tie_weights<<<dim3(64, wd.nslots), 256, SORT_SMEM * 4, s>>>(gd, wd, true);
+        L.check(__LINE__);
+        k_beam_tie<<<wd.nslots, 256, 1024 * 16, s>>>(wd);
+        L.check(__LINE__);
+        k_scan_cands<<<1, MAX_SLOTS, 0, s>>>(wd);
+        L.check(__LINE__);
     }
     if (L.g->profiling) CUDA_TRY(cudaStreamSynchronize(s));
     L.mark(1);
@@ -2587,15 +2668,15 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     L.mark(2);
     // ---- top-k and packing
     k_final_select<<<wd.nslots, 256, 1024 * 16, s>>>(wd);
-    L.check();
+    L.check(__LINE__);
     if (ws->tie_break) {  // R29 weight-sum tie-break
-        k_tie_weights<<<dim3(64, wd.nslots), 256, SORT_SMEM * 4, s>>>(gd, wd);
-        L.check();
+        k_tie_weights<<<dim3(64, wd.nslots), 256, SORT_SMEM * 4, s>>>(gd, wd, false);
+        L.check(__LINE__);
         k_tie_select<<<wd.nslots, 256, 1024 * 16, s>>>(wd);
-        L.check();
+        L.check(__LINE__);
     }
     k_final_lists<RowC><<<dim3(ws->kmax, wd.nslots), 256, SORT_SMEM * 4, s>>>(gd, wd);
-    L.check();
+    L.check(__LINE__);
     if (L.g->profiling) CUDA_TRY(cudaStreamSynchronize(s));
     L.mark(3);
 }
@@ -2756,7 +2837,9 @@ std::string err_text(uint32_t e) {
 
 // Run [q0, q0+n) of a batch whose slot states are already on the device (any source).
 // Grows capacities and re-runs when a workspace overflow is reported.
-void run_with_retry(riki_graph *g, Launch &L, uint32_t depth, Caps &caps, uint32_t n_active,
+// Returns false when the batch needs more recovery arena than 32-bit offsets address: the
+// caller re-runs it in smaller chunks (caps.slots halved).
+bool run_with_retry(riki_graph *g, Launch &L, uint32_t depth, Caps &caps, uint32_t n_active,
                     const std::function<void()> &upload, std::vector<SlotState> *st_out) {
     for (int attempt = 0;; attempt++) {
         ensure_workspace(g, caps);
@@ -2770,14 +2853,29 @@ void run_with_retry(riki_graph *g, Launch &L, uint32_t depth, Caps &caps, uint32
         uint32_t err = 0;
         for (uint32_t i = 0; i < n_active; i++) err |= (*st_out)[i].err;
         if (err & E_UNRESOLVED) RIKI_THROW(RIKI_EUNRESOLVED, "a query term is unresolved (empty posting) or out of range");
-        if (!err) return;
+        if (!err) return true;
         g->stats.retries++;
         if (getenv("RIKI_TRACE")) fprintf(stderr, "[riki] retry after overflow:%s\n", err_text(err).c_str());
         if (attempt >= 6) RIKI_THROW(RIKI_ENOMEM, "workspace overflow:" + err_text(err));
         if (err & E_CAND) caps.capc = std::min<uint32_t>(caps.capc * 4, next_pow2(g->V + 1));
-        if (err & (E_ARENA | E_EXTRACT)) caps.arena *= 4;
+        if (err & (E_ARENA | E_EXTRACT)) {
+            // arena offsets are 32-bit words (EMPTY = 0xFFFFFFFF is the failure sentinel)
+            const uint64_t amax = g->arena_limit ? std::min<uint64_t>(g->arena_limit, ARENA_MAX_WORDS) : ARENA_MAX_WORDS;
+            if (caps.arena >= amax) {
+                if (n_active <= 1) RIKI_THROW(RIKI_ENOMEM, "recovery arena exceeds 2^32 words for one query");
+                caps.slots = std::max(1u, n_active / 2);
+                return false;
+            }
+            caps.arena = std::min<uint64_t>(caps.arena * 4, amax);
+        }
         if (err & E_OUT) caps.out *= 4;
-        if (err & E_QUEUE) caps.qcap = 2 * g->V;  // exact bound: one retained + one new entry per node
+        if (err & E_QUEUE) {
+            caps.qcap = 2 * g->V;  // exact bound: one retained + one new entry per node
+            if (n_active > max_slots_for(caps.qcap)) {
+                caps.slots = max_slots_for(caps.qcap);
+                return false;
+            }
+        }
         if (err & E_HEAVY) RIKI_THROW(RIKI_ENOMEM, "heavy work queue overflow");
     }
 }
@@ -2838,8 +2936,6 @@ static void check_common(riki_graph *g, uint32_t k, uint32_t depth, const riki_p
     if (p.tie_break != 0 && p.tie_break != 1) RIKI_THROW(RIKI_EINVAL, "tie_break must be 0 or 1");
     if (p.tie_break == 1 && !g->d_wfix)
         RIKI_THROW(RIKI_ENOWEIGHTS, "tie_break 1 needs the fine edge weights (set_edge/node/label_weights)");
-    if (p.tie_break == 1 && p.beam_mode == 1)
-        RIKI_THROW(RIKI_ENOSYS, "tie_break 1 with beam_mode 1 (beam truncated by W(CG)) is not implemented on the GPU");
     if (p.ptc_mode < 0 || p.ptc_mode > 3) RIKI_THROW(RIKI_EINVAL, "ptc_mode must be 0..3");
     if (p.early_term < 0 || p.early_term > 2) RIKI_THROW(RIKI_EINVAL, "early_term must be 0..2");
     if (p.beam_w && p.beam_w < k) RIKI_THROW(RIKI_EINVAL, "beam width must be >= k (P:309)");
@@ -2853,9 +2949,11 @@ static Caps initial_caps(riki_graph *g, uint32_t nq, uint32_t k, uint32_t rb0, u
     c.capc = std::min<uint32_t>(16384, next_pow2(g->V + 1));
     c.kmax = std::max<uint32_t>(k, g->ws ? g->ws->kmax : 1);
     c.arena = std::max<uint64_t>(64ull << 20, g->ws ? g->ws->arena_cap : 0);
+    if (g->arena_limit) c.arena = std::min<uint64_t>(c.arena, g->arena_limit);
     c.out = std::max<uint64_t>(16ull << 20, g->ws ? g->ws->out_cap : 0);
     if (g->ws) c.capc = std::max(c.capc, g->ws->capc);
     c.qcap = std::max<uint32_t>(g->V, g->ws ? g->ws->qcap : 0);
+    c.slots = std::min(c.slots, max_slots_for(c.qcap));
     return c;
 }
 
@@ -2897,6 +2995,7 @@ void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, ui
                 ws->last_rb[0] = row_bytes(maxc);
                 ws->last_rb[1] = row_bytes(maxm);
                 ws->tie_break = tmpl.tie_break;
+                ws->beam_tie = tmpl.tie_break && tmpl.beam_mode == 1;
                 ws->cur = n;
                 set_layout(g, ws, n);
                 std::vector<SlotState> h(n, tmpl);
@@ -2916,7 +3015,7 @@ void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, ui
                 CUDA_TRY(cudaMemsetAsync(ws->prof, 0, P_NPROF * 8, L.s));
             };
             tr("before run");
-            run_with_retry(g, L, depth, caps, n, upload, &stv);
+            if (!run_with_retry(g, L, depth, caps, n, upload, &stv)) continue;  // smaller chunk
             tr("run_with_retry");
             collect_results(g, g->ws, n, qidx, &res);
             tr("collect_results");
@@ -2950,35 +3049,57 @@ void engine_search_device(riki_graph *g, uint32_t nq, const uint64_t *d_cptr, co
     tr("ptr D2H");
     Caps caps = initial_caps(g, nq, k, row_bytes(std::max(maxc, 1u)), row_bytes(std::max(maxm, 1u)));
     tr("initial_caps");
-    caps.slots = std::max(caps.slots, std::min<uint32_t>(nq, MAX_SLOTS));
+    caps.slots = std::min(std::max(caps.slots, std::min<uint32_t>(nq, MAX_SLOTS)), max_slots_for(caps.qcap));
     ensure_workspace(g, caps);
-    if (nq > g->ws->slots) RIKI_THROW(RIKI_EINVAL, "device batch larger than the workspace slots");
     Launch L{g, g->stream};
     SlotState tmpl = make_template(k, depth, p);
     if (maxc == 0) RIKI_THROW(RIKI_EEMPTY_CENTRAL, "C must be non-empty (Def. RPQ, P:105)");
     std::vector<SlotState> stv;
-    auto upload = [&]() {
-        Workspace *ws = g->ws;
-        ws->last_rb[0] = row_bytes(maxc);
-        ws->last_rb[1] = row_bytes(maxm);
-        ws->tie_break = tmpl.tie_break;
-        ws->cur = nq;
-        set_layout(g, ws, nq);
-        k_slots_from_device<<<(nq + 127) / 128, 128, 0, L.s>>>(ws->st, nq, 0, nq, d_cptr, d_cterms,
-                                                                      d_mptr, d_mterms, tmpl, g->d_tptr, g->n_terms);
-        L.check();
-        CUDA_TRY(cudaMemsetAsync(ws->prof, 0, P_NPROF * 8, L.s));
-    };
-    tr("ensure+setup");
-    run_with_retry(g, L, depth, caps, nq, upload, &stv);
-    tr("run_with_retry");
+    for (riki_results *r : g->dev_stash) delete r;
+    g->dev_stash.clear();
+    bool chunked = false;
+    for (uint32_t q0 = 0; q0 < nq;) {
+        const uint32_t n = std::min<uint32_t>(std::min(caps.slots, g->ws->slots), nq - q0);
+        auto upload = [&]() {
+            Workspace *ws = g->ws;
+            ws->last_rb[0] = row_bytes(maxc);
+            ws->last_rb[1] = row_bytes(maxm);
+            ws->tie_break = tmpl.tie_break;
+            ws->beam_tie = tmpl.tie_break && tmpl.beam_mode == 1;
+            ws->cur = n;
+            set_layout(g, ws, n);
+            k_slots_from_device<<<(n + 127) / 128, 128, 0, L.s>>>(ws->st, n, q0, nq, d_cptr, d_cterms, d_mptr, d_mterms,
+                                                                  tmpl, g->d_tptr, g->n_terms);
+            L.check(__LINE__);
+            CUDA_TRY(cudaMemsetAsync(ws->prof, 0, P_NPROF * 8, L.s));
+        };
+        tr("ensure+setup");
+        if (!run_with_retry(g, L, depth, caps, n, upload, &stv)) {  // arena limit: smaller chunks
+            chunked = true;
+            continue;
+        }
+        tr("run_with_retry");
+        if (chunked || n < nq) {  // results of a chunk leave HBM before the next chunk runs
+            chunked = true;
+            g->dev_stash.resize(nq, nullptr);
+            std::vector<uint32_t> qidx(n);
+            for (uint32_t i = 0; i < n; i++) qidx[i] = q0 + i;
+            collect_results(g, g->ws, n, qidx, &g->dev_stash);
+        }
+        add_stats(g, g->ws, L, n);
+        q0 += n;
+    }
     g->ws->last_n = nq;
-    add_stats(g, g->ws, L, nq);
     tr("add_stats");
 }
 
 void engine_fetch(riki_graph *g, uint32_t nq, std::vector<riki_results *> *out) {
     if (!g->ws || g->ws->last_n != nq) RIKI_THROW(RIKI_EINVAL, "no device batch of that size to fetch");
+    if (!g->dev_stash.empty()) {  // the batch ran in chunks: results were collected per chunk
+        *out = std::move(g->dev_stash);
+        g->dev_stash.clear();
+        return;
+    }
     out->assign(nq, nullptr);
     std::vector<uint32_t> qidx(nq);
     for (uint32_t i = 0; i < nq; i++) qidx[i] = i;
@@ -3031,7 +3152,7 @@ void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uin
             run_phase<uint64_t, uint64_t>(L, gd, ws, 0, block_mode, depth + 1, 0);
             k_pack_H<uint64_t><<<grid_of(g->V, 256), 256, 0, L.s>>>(gd, wd, T, dH, dB, blocking);
         }
-        L.check();
+        L.check(__LINE__);
         CUDA_TRY(cudaMemcpyAsync(H_out, dH, (size_t)g->V * T, cudaMemcpyDeviceToHost, L.s));
         CUDA_TRY(cudaMemcpyAsync(block_out, dB, g->V, cudaMemcpyDeviceToHost, L.s));
         SlotState s0;
@@ -3060,6 +3181,8 @@ void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uin
 }
 
 void engine_free(riki_graph *g) {
+    for (riki_results *r : g->dev_stash) delete r;
+    g->dev_stash.clear();
     if (g->ws) {
         g->ws->release();
         delete g->ws;

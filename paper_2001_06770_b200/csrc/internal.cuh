@@ -90,6 +90,8 @@ struct riki_graph {
     uint32_t batch_slots = 0;
     riki_stats stats{};
     DistState *dist = nullptr;  // set by riki_dist_init
+    std::vector<riki_results *> dev_stash;
+    uint64_t arena_limit = 0;  // riki_set_arena_limit (tests): 0 = the 32-bit offset limit  // device batch run in chunks: results collected per chunk
     bool vp() const { return dist && dist->mode == 1; }
 
     GraphDev dev() const {

@@ -113,6 +113,7 @@ def load():
         "riki_set_joint": (i32, [P, i32]),
         "riki_set_batch_slots": (i32, [P, u32]),
         "riki_memory_footprint": (i32, [P, P, P]),
+        "riki_set_arena_limit": (i32, [P, u64]),
         "riki_dist_unique_id": (i32, [P]),
         "riki_dist_init": (i32, [P, i32, i32, P, i32]),
         "riki_dist_partition": (i32, [P, u32, u32, P]),
@@ -393,6 +394,9 @@ class Graph:
     def set_joint(self, on=True):
         """Joint multi-query traversal for large batches (identical results)."""
         _check(self.lib.riki_set_joint(self.h, int(on)))
+
+    def set_arena_limit(self, words):
+        _check(self.lib.riki_set_arena_limit(self.h, int(words)))
 
     def set_batch_slots(self, n):
         _check(self.lib.riki_set_batch_slots(self.h, n))

@@ -47,11 +47,6 @@ def test_tie_break_golden_fixture(P):
     for case in d["cases"]:
         M = [2] if case["marginal"] else []
         kw = dict(tie_break=case["tie_break"], beam_w=case.get("beam_w", 0), beam_mode=case.get("beam_mode", 0))
-        if case["tie_break"] == 1 and kw["beam_mode"] == 1:
-            with pytest.raises(P.RikiError) as ei:
-                g.search([0, 1], M, case["k"], d["depth"], **kw)
-            assert ei.value.code == -9  # RIKI_ENOSYS
-            continue
         r = g.search([0, 1], M, case["k"], d["depth"], **kw)
         assert [x.central_node for x in r.rpgs] == case["expect"], case
         for x, ed in zip(r.rpgs, case.get("edges", [])):
@@ -74,7 +69,8 @@ def test_tie_break_random(P, seed):
         C, M = tt[:nc], tt[nc:]
         k = int(rng.choice([1, 2, 3, 5, 8]))
         D = int(rng.choice([4, 20]))
-        kw = dict(ptc_mode=int(rng.integers(0, 4)), early_term=int(rng.choice([0, 2])))
+        kw = dict(ptc_mode=int(rng.integers(0, 4)), early_term=int(rng.choice([0, 2])),
+                  beam_mode=int(rng.integers(0, 2)), beam_w=int(rng.choice([0, k, k + 1, 2 * k])))
         r = g.search(C, M, k, D, tie_break=1, **kw)
         ro = O.search(og, [post[t] for t in C], [post[t] for t in M], k, D, tie_break=1, wfine=wf, **kw)
         _same(r, ro)
