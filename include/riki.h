@@ -58,6 +58,14 @@ riki_status riki_load_graph(int device, uint32_t n_nodes, uint64_t n_edges,
                             const uint32_t *src, const uint32_t *dst, const uint32_t *label_class,
                             uint32_t n_terms, const uint64_t *term_ptr, const uint32_t *postings,
                             riki_graph **out);
+/* Same, with every array a DEVICE pointer on `device` (e.g. torch tensors): the inputs are
+ * validated on the device and copied device-to-device (the CSR build reorders them anyway),
+ * so the caller may free them after the call.  term_ptr is also read back to the host
+ * (n_terms + 1 words).  Errors as riki_load_graph (without the offending index). */
+riki_status riki_load_graph_device(int device, uint32_t n_nodes, uint64_t n_edges,
+                                   const uint32_t *src, const uint32_t *dst, const uint32_t *label_class,
+                                   uint32_t n_terms, const uint64_t *term_ptr, const uint32_t *postings,
+                                   riki_graph **out);
 void riki_free_graph(riki_graph *g);
 
 /* ---------------------------------------------------------------------------------------
@@ -141,10 +149,9 @@ riki_status riki_rpq_search_batch(riki_graph *g, uint32_t n_queries,
 /* Device-resident batch (benchmark / pipeline path): identical computation, but the query
  * arrays are DEVICE pointers and results stay on the device (no D2H); results are
  * retrievable afterwards with riki_batch_fetch (which performs the D2H).  Returns after
- * the work has been enqueued and completed on the library stream.  A batch larger than the
- * slots that fit in flight (frontier items of a level must be 32-bit indexable: slots x
- * queue capacity < 2^32; the recovery arena must stay below 2^32 words) runs in chunks,
- * and then each chunk's results are copied to the host before the next chunk runs. */
+ * the work has been enqueued and completed on the library stream.  A batch whose recovery
+ * arena (32-bit word offsets) would exceed 2^32 words runs in chunks of fewer queries, and
+ * then each chunk's results are copied to the host before the next chunk runs. */
 riki_status riki_rpq_search_batch_device(riki_graph *g, uint32_t n_queries,
                                          const uint64_t *d_c_ptr, const uint32_t *d_c_terms,
                                          const uint64_t *d_m_ptr, const uint32_t *d_m_terms,

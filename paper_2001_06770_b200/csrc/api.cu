@@ -78,9 +78,9 @@ void riki_params_default(riki_params *p) {
     p->early_term = 0;
 }
 
-riki_status riki_load_graph(int device, uint32_t n_nodes, uint64_t n_edges, const uint32_t *src, const uint32_t *dst,
-                            const uint32_t *label_class, uint32_t n_terms, const uint64_t *term_ptr,
-                            const uint32_t *postings, riki_graph **out) {
+static riki_status load_graph(int device, uint32_t n_nodes, uint64_t n_edges, const uint32_t *src, const uint32_t *dst,
+                              const uint32_t *label_class, uint32_t n_terms, const uint64_t *term_ptr,
+                              const uint32_t *postings, riki_graph **out, bool device_inputs) {
     return guard([&] {
         need(out != nullptr, "null out");
         *out = nullptr;
@@ -88,7 +88,7 @@ riki_status riki_load_graph(int device, uint32_t n_nodes, uint64_t n_edges, cons
         riki_graph *g = new riki_graph();
         g->device = device;
         try {
-            graph_load(g, n_nodes, n_edges, src, dst, label_class, n_terms, term_ptr, postings);
+            graph_load(g, n_nodes, n_edges, src, dst, label_class, n_terms, term_ptr, postings, device_inputs);
         } catch (...) {
             graph_free(g);
             delete g;
@@ -96,6 +96,18 @@ riki_status riki_load_graph(int device, uint32_t n_nodes, uint64_t n_edges, cons
         }
         *out = g;
     });
+}
+
+riki_status riki_load_graph(int device, uint32_t n_nodes, uint64_t n_edges, const uint32_t *src, const uint32_t *dst,
+                            const uint32_t *label_class, uint32_t n_terms, const uint64_t *term_ptr,
+                            const uint32_t *postings, riki_graph **out) {
+    return load_graph(device, n_nodes, n_edges, src, dst, label_class, n_terms, term_ptr, postings, out, false);
+}
+
+riki_status riki_load_graph_device(int device, uint32_t n_nodes, uint64_t n_edges, const uint32_t *src,
+                                   const uint32_t *dst, const uint32_t *label_class, uint32_t n_terms,
+                                   const uint64_t *term_ptr, const uint32_t *postings, riki_graph **out) {
+    return load_graph(device, n_nodes, n_edges, src, dst, label_class, n_terms, term_ptr, postings, out, true);
 }
 
 void riki_free_graph(riki_graph *g) {

@@ -22,6 +22,7 @@
 #include <chrono>
 #include <functional>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "internal.cuh"
@@ -112,7 +113,7 @@ struct WsDev {
     uint64_t *ck;
     Cand *cd;
     u128 *rk;
-    uint32_t *offs;  // frontier-item prefix over the slots (< 2^32: slots x qcap is bounded, max_slots_for)
+    unsigned long long *offs;  // frontier-item prefix over the slots (k_expand<.., WIDE> beyond 2^32)
     uint32_t *coffs, *pslots;
     uint32_t track_reached;  // direction-optimising mode: count new nodes per slot
     uint4 *heavy;
@@ -296,7 +297,7 @@ template <class RowT> __global__ void k_seed(GraphDev g, WsDev w, int ph) {
 #endif
 // pull_min: minimum frontier for bottom-up (0xFFFFFFFF disables it)
 __global__ void k_plan(WsDev w, int ph, uint32_t l, uint32_t pull_min) {
-    __shared__ uint32_t sc[MAX_SLOTS];
+    __shared__ unsigned long long sc[MAX_SLOTS];
     __shared__ uint32_t nact, npull;
     __shared__ unsigned long long nenq;
     uint32_t s = threadIdx.x;
@@ -336,7 +337,7 @@ __global__ void k_plan(WsDev w, int ph, uint32_t l, uint32_t pull_min) {
     sc[s] = items;
     __syncthreads();
     for (uint32_t o = 1; o < MAX_SLOTS; o <<= 1) {
-        uint32_t v = s >= o ? sc[s - o] : 0;
+        unsigned long long v = s >= o ? sc[s - o] : 0;
         __syncthreads();
         sc[s] += v;
         __syncthreads();
@@ -345,7 +346,7 @@ __global__ void k_plan(WsDev w, int ph, uint32_t l, uint32_t pull_min) {
     if (s == 0) {
         w.offs[w.nslots] = sc[MAX_SLOTS - 1];
         w.ctr[C_ACTIVE] = nact;
-        w.ctr[C_TOTAL] = sc[MAX_SLOTS - 1];
+        w.ctr[C_TOTAL] = (uint32_t)min(sc[MAX_SLOTS - 1], 0xFFFFFFFFull);  // diagnostics
         w.ctr[C_NHEAVY] = 0;
         w.ctr[C_NPULL] = npull;
         if (!w.hnode) {  // profiling counters of the per-slot expansion (k_expand counts edges/cells)
@@ -553,20 +554,24 @@ template <class RowT> struct alignas(16) OwnF {
     RowT nw, od;
 };
 
-template <class RowT>
+// WIDE: 64-bit frontier-item indices, for batches whose level can exceed 2^32 items
+// (slots x queue capacity >= 2^32, e.g. 200 queries on a 30M-node graph); the common
+// case keeps the 32-bit loop.
+template <class RowT, bool WIDE>
 __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, int ph, uint32_t l) {
     typedef Row<RowT> R;
-    __shared__ uint32_t s_offs[MAX_SLOTS + 1];
+    typedef typename std::conditional<WIDE, unsigned long long, uint32_t>::type IdxT;
+    __shared__ IdxT s_offs[MAX_SLOTS + 1];
     __shared__ uint32_t s_info[MAX_SLOTS];
     __shared__ OwnF<RowT> s_own[8][32];
     const uint32_t ns = w.nslots;
-    for (uint32_t i = threadIdx.x; i <= ns; i += blockDim.x) s_offs[i] = w.offs[i];
+    for (uint32_t i = threadIdx.x; i <= ns; i += blockDim.x) s_offs[i] = (IdxT)w.offs[i];
     for (uint32_t i = threadIdx.x; i < ns; i += blockDim.x) {
         const SlotState &st = w.st[i];
         s_info[i] = st.blocking | st.collect << 1 | st.pull << 2 | st.T[ph] << 8;
     }
     __syncthreads();
-    const uint32_t total = s_offs[ns];
+    const IdxT total = s_offs[ns];
     const uint32_t lane = lane_id();
     const uint32_t cur = l & 1, nxt = cur ^ 1;
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -577,8 +582,8 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
     OwnF<RowT> *const own = s_own[threadIdx.x >> 5];
     uint32_t p_edges = 0, p_cells = 0;  // items and queue entries are counted by k_plan
 
-    for (uint32_t base = gw * 32; base < total; base += nw * 32) {
-        const uint32_t item = base + lane;
+    for (IdxT base = (IdxT)gw * 32; base < total; base += (IdxT)nw * 32) {
+        const IdxT item = base + lane;
         bool valid = item < total;
         // slots of this warp's 32 items: two warp-uniform searches, then (rarely) a short
         // per-lane search between them
@@ -590,7 +595,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
         if (valid) {
             if (sB != sA) s = find_slot(s_offs + sA, sB - sA + 1, item) + sA;
             uint32_t info = s_info[s];
-            uint32_t ent = w.Q(s, cur)[item - s_offs[s]];
+            uint32_t ent = w.Q(s, cur)[(uint32_t)(item - s_offs[s])];
             f = ent & ~RETAINED;
             RowT Rf = R::load(Hb + (size_t)s * V + f);
             const uint4 d = __ldg(g.desc + f);  // issued with the row load (dropped if dup / blocked)
@@ -2260,7 +2265,8 @@ struct Workspace {
     uint64_t arena_cap = 0, out_cap = 0, big_words = 0;
     uint8_t *H[2] = {nullptr, nullptr};
     uint32_t qcap = 0;  // entries per level queue
-    uint32_t *q = nullptr, *bm = nullptr, *jq = nullptr, *jbm = nullptr, *offs = nullptr, *coffs = nullptr, *pslots = nullptr, *ctr = nullptr, *arena = nullptr,
+    unsigned long long *offs = nullptr;
+    uint32_t *q = nullptr, *bm = nullptr, *jq = nullptr, *jbm = nullptr, *coffs = nullptr, *pslots = nullptr, *ctr = nullptr, *arena = nullptr,
              *big = nullptr, *resid = nullptr, *out = nullptr;
     uint4 *mtab = nullptr;
     uint64_t *ck = nullptr;
@@ -2356,11 +2362,6 @@ struct Caps {
 
 constexpr uint64_t ARENA_MAX_WORDS = 0xFFFFFF00ull;  // largest arena addressable by u32 offsets
 
-// Slots in flight such that the frontier items of one level (<= slots x qcap queue entries)
-// are indexable with 32 bits (k_plan's prefix, k_expand's item index).
-uint32_t max_slots_for(uint32_t qcap) {
-    return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(MAX_SLOTS, 0xFFFFFFFFull / std::max(qcap, 1u)));
-}
 
 void ensure_workspace(riki_graph *g, const Caps &c) {
     Workspace *ws = g->ws;
@@ -2394,7 +2395,7 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     ws->cd = ws->alloc<Cand>(S * c.capc);
     ws->rk = ws->alloc<u128>(S * c.capc);
     ws->st = ws->alloc<SlotState>(S);
-    ws->offs = ws->alloc<uint32_t>(S + 1);
+    ws->offs = ws->alloc<unsigned long long>(S + 1);
     ws->coffs = ws->alloc<uint32_t>(S + 1);
     ws->pslots = ws->alloc<uint32_t>(S + 1);
     uint64_t hc = (uint64_t)S * (g->E / CHUNK + g->E / HEAVY + 64);
@@ -2519,6 +2520,7 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
                uint64_t total_cands) {
     cudaStream_t s = L.s;
     const bool vp = L.g->vp();  // vertex-partitioned: every level is a partitioned pull + all-gather
+    const bool wide_forced = getenv("RIKI_FORCE_WIDE") != nullptr;  // tests: 64-bit item loop at any size
     const bool pull = L.g->pull_on || vp;
     ws->track_reached = L.g->pull_on ? 1 : 0;
     WsDev wd = ws->dev();
@@ -2575,7 +2577,10 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
                 L.check(__LINE__);
             }
         } else {
-            k_expand<RowT><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
+            if ((uint64_t)wd.nslots * ws->qcap >= (1ull << 32) || wide_forced)
+                k_expand<RowT, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
+            else
+                k_expand<RowT, false><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
             L.check(__LINE__);
             k_expand_heavy<RowT><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
             L.check(__LINE__);
@@ -2869,13 +2874,7 @@ bool run_with_retry(riki_graph *g, Launch &L, uint32_t depth, Caps &caps, uint32
             caps.arena = std::min<uint64_t>(caps.arena * 4, amax);
         }
         if (err & E_OUT) caps.out *= 4;
-        if (err & E_QUEUE) {
-            caps.qcap = 2 * g->V;  // exact bound: one retained + one new entry per node
-            if (n_active > max_slots_for(caps.qcap)) {
-                caps.slots = max_slots_for(caps.qcap);
-                return false;
-            }
-        }
+        if (err & E_QUEUE) caps.qcap = 2 * g->V;  // exact bound: one retained + one new entry per node
         if (err & E_HEAVY) RIKI_THROW(RIKI_ENOMEM, "heavy work queue overflow");
     }
 }
@@ -2953,7 +2952,6 @@ static Caps initial_caps(riki_graph *g, uint32_t nq, uint32_t k, uint32_t rb0, u
     c.out = std::max<uint64_t>(16ull << 20, g->ws ? g->ws->out_cap : 0);
     if (g->ws) c.capc = std::max(c.capc, g->ws->capc);
     c.qcap = std::max<uint32_t>(g->V, g->ws ? g->ws->qcap : 0);
-    c.slots = std::min(c.slots, max_slots_for(c.qcap));
     return c;
 }
 
@@ -3049,7 +3047,7 @@ void engine_search_device(riki_graph *g, uint32_t nq, const uint64_t *d_cptr, co
     tr("ptr D2H");
     Caps caps = initial_caps(g, nq, k, row_bytes(std::max(maxc, 1u)), row_bytes(std::max(maxm, 1u)));
     tr("initial_caps");
-    caps.slots = std::min(std::max(caps.slots, std::min<uint32_t>(nq, MAX_SLOTS)), max_slots_for(caps.qcap));
+    caps.slots = std::max(caps.slots, std::min<uint32_t>(nq, MAX_SLOTS));
     ensure_workspace(g, caps);
     Launch L{g, g->stream};
     SlotState tmpl = make_template(k, depth, p);

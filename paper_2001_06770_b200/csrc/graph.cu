@@ -276,26 +276,62 @@ void check_params(double alpha, double avg) {
 
 }  // namespace
 
+// riki_load_graph_device: the caller's arrays are validated where they live.  bad: bit 0 =
+// endpoint out of range, bit 1 = posting out of range, bit 2 = postings not sorted unique.
+__global__ void k_validate_edges(const uint32_t *src, const uint32_t *dst, uint64_t E, uint32_t V, uint32_t *bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < E; i += (uint64_t)gridDim.x * blockDim.x)
+        if (src[i] >= V || dst[i] >= V) atomicOr(bad, 1u);
+}
+__global__ void k_validate_postings(const uint64_t *tptr, uint32_t n_terms, const uint32_t *post, uint32_t V,
+                                    uint32_t *bad) {
+    for (uint32_t t = blockIdx.x; t < n_terms; t += gridDim.x)
+        for (uint64_t i = tptr[t] + threadIdx.x; i < tptr[t + 1]; i += blockDim.x) {
+            if (post[i] >= V) atomicOr(bad, 2u);
+            if (i > tptr[t] && post[i] <= post[i - 1]) atomicOr(bad, 4u);
+        }
+}
+
 void graph_load(riki_graph *g, uint32_t V, uint64_t E, const uint32_t *src, const uint32_t *dst, const uint32_t *cls,
-                uint32_t n_terms, const uint64_t *tptr, const uint32_t *post) {
+                uint32_t n_terms, const uint64_t *tptr_in, const uint32_t *post, bool device_inputs) {
     if (V == 0) RIKI_THROW(RIKI_EINVAL, "n_nodes must be > 0");
     if (E >= (1ull << 32)) RIKI_THROW(RIKI_EINVAL, "n_edges must be < 2^32");
     if (E && (!src || !dst)) RIKI_THROW(RIKI_EINVAL, "null edge arrays");
-    if (n_terms && (!tptr)) RIKI_THROW(RIKI_EINVAL, "null term_ptr");
-    for (uint64_t e = 0; e < E; e++)
-        if (src[e] >= V || dst[e] >= V) RIKI_THROW(RIKI_EINVAL, "edge " + std::to_string(e) + " endpoint out of range");
+    if (n_terms && (!tptr_in)) RIKI_THROW(RIKI_EINVAL, "null term_ptr");
+    CUDA_TRY(cudaSetDevice(g->device));
+    std::vector<uint64_t> tptr_h;
+    const uint64_t *tptr = tptr_in;
+    if (device_inputs && n_terms) {  // the (small) term pointer is needed on the host anyway (h_tptr)
+        tptr_h.resize(n_terms + 1);
+        CUDA_TRY(cudaMemcpy(tptr_h.data(), tptr_in, (n_terms + 1) * 8, cudaMemcpyDeviceToHost));
+        tptr = tptr_h.data();
+    }
+    if (!device_inputs)
+        for (uint64_t e = 0; e < E; e++)
+            if (src[e] >= V || dst[e] >= V) RIKI_THROW(RIKI_EINVAL, "edge " + std::to_string(e) + " endpoint out of range");
     uint64_t P = n_terms ? tptr[n_terms] : 0;
     if (n_terms && tptr[0] != 0) RIKI_THROW(RIKI_EINVAL, "term_ptr[0] must be 0");
     if (P && !post) RIKI_THROW(RIKI_EINVAL, "null postings");
     for (uint32_t t = 0; t < n_terms; t++) {
         if (tptr[t + 1] < tptr[t]) RIKI_THROW(RIKI_EINVAL, "term_ptr not monotone");
+        if (device_inputs) continue;
         for (uint64_t i = tptr[t]; i < tptr[t + 1]; i++) {
             if (post[i] >= V) RIKI_THROW(RIKI_EINVAL, "posting node out of range (term " + std::to_string(t) + ")");
             if (i > tptr[t] && post[i] <= post[i - 1])
                 RIKI_THROW(RIKI_EINVAL, "postings of term " + std::to_string(t) + " not sorted unique");
         }
     }
-    CUDA_TRY(cudaSetDevice(g->device));
+    if (device_inputs) {
+        uint32_t *bad = dmalloc<uint32_t>(1), hbad = 0;
+        CUDA_TRY(cudaMemset(bad, 0, 4));
+        if (E) k_validate_edges<<<grid_for(E), 256>>>(src, dst, E, V, bad);
+        if (P) k_validate_postings<<<std::min<uint32_t>(n_terms, 148 * 16), 256>>>(tptr_in, n_terms, post, V, bad);
+        CUDA_TRY(cudaMemcpy(&hbad, bad, 4, cudaMemcpyDeviceToHost));
+        cudaFree(bad);
+        if (hbad & 1) RIKI_THROW(RIKI_EINVAL, "edge endpoint out of range");
+        if (hbad & 2) RIKI_THROW(RIKI_EINVAL, "posting node out of range");
+        if (hbad & 4) RIKI_THROW(RIKI_EINVAL, "postings not sorted unique");
+    }
+    const cudaMemcpyKind kind = device_inputs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     CUDA_TRY(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
     g->V = V;
     g->E = E;
@@ -317,16 +353,16 @@ void graph_load(riki_graph *g, uint32_t V, uint64_t E, const uint32_t *src, cons
     g->d_post = dmalloc<uint32_t>(P, acc);
     cudaStream_t s = g->stream;
     if (E) {
-        CUDA_TRY(cudaMemcpyAsync(g->d_src, src, E * 4, cudaMemcpyHostToDevice, s));
-        CUDA_TRY(cudaMemcpyAsync(g->d_dst, dst, E * 4, cudaMemcpyHostToDevice, s));
-        if (cls) CUDA_TRY(cudaMemcpyAsync(g->d_cls, cls, E * 4, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(g->d_src, src, E * 4, kind, s));
+        CUDA_TRY(cudaMemcpyAsync(g->d_dst, dst, E * 4, kind, s));
+        if (cls) CUDA_TRY(cudaMemcpyAsync(g->d_cls, cls, E * 4, kind, s));
         else CUDA_TRY(cudaMemsetAsync(g->d_cls, 0, E * 4, s));
     }
     g->h_tptr.assign(n_terms + 1, 0);
     if (n_terms) {
         std::copy(tptr, tptr + n_terms + 1, g->h_tptr.begin());
         CUDA_TRY(cudaMemcpyAsync(g->d_tptr, tptr, (n_terms + 1) * 8, cudaMemcpyHostToDevice, s));
-        if (P) CUDA_TRY(cudaMemcpyAsync(g->d_post, post, P * 4, cudaMemcpyHostToDevice, s));
+        if (P) CUDA_TRY(cudaMemcpyAsync(g->d_post, post, P * 4, kind, s));
     }
     // ---- degree-descending relabeling (internal ids); translated back at the boundary
     g->d_perm = dmalloc<uint32_t>(V, acc);

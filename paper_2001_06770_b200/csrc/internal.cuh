@@ -107,7 +107,7 @@ struct riki_graph {
 
 // graph.cu
 void graph_load(riki_graph *g, uint32_t n_nodes, uint64_t n_edges, const uint32_t *src, const uint32_t *dst,
-                const uint32_t *cls, uint32_t n_terms, const uint64_t *tptr, const uint32_t *post);
+                const uint32_t *cls, uint32_t n_terms, const uint64_t *tptr, const uint32_t *post, bool device_inputs);
 void graph_free(riki_graph *g);
 void graph_set_edge_weights(riki_graph *g, const double *w01, double alpha, double avg);
 void graph_set_node_weights(riki_graph *g, const double *w01, double alpha, double avg);

@@ -85,6 +85,7 @@ def load():
     P, u32, u64, i32, dbl = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int, C.c_double
     sig = {
         "riki_load_graph": (i32, [i32, u32, u64, P, P, P, u32, P, P, P]),
+        "riki_load_graph_device": (i32, [i32, u32, u64, P, P, P, u32, P, P, P]),
         "riki_free_graph": (None, [P]),
         "riki_set_edge_weights": (i32, [P, P, dbl, dbl]),
         "riki_set_node_weights": (i32, [P, P, dbl, dbl]),
@@ -292,6 +293,23 @@ class Graph:
         self._debug = False
         self.V = int(n_nodes)
         self.E = len(src)
+
+    @classmethod
+    def from_device(cls, n_nodes, n_edges, src_ptr, dst_ptr, cls_ptr, n_terms, tptr_ptr, post_ptr, device=0):
+        """riki_load_graph_device: every array a device pointer (int, e.g. tensor.data_ptr());
+        u32 src/dst/label_class[n_edges], u64 term_ptr[n_terms + 1], u32 postings."""
+        self = cls.__new__(cls)
+        self.lib = load()
+        self.h = None
+        h = C.c_void_p()
+        _check(self.lib.riki_load_graph_device(device, int(n_nodes), int(n_edges), C.c_void_p(src_ptr),
+                                               C.c_void_p(dst_ptr), C.c_void_p(cls_ptr) if cls_ptr else None,
+                                               int(n_terms), C.c_void_p(tptr_ptr), C.c_void_p(post_ptr), C.byref(h)))
+        self.h = h
+        self._debug = False
+        self.V = int(n_nodes)
+        self.E = int(n_edges)
+        return self
 
     def close(self):
         if self.h:

@@ -53,3 +53,42 @@ def test_arena_limit_chunks_host_and_device_batches(P):
         g2.search_batch_device(n, *(x.data_ptr() for x in d), qs.k, qs.depth)
         assert _key(g2.fetch(n, [len(c) for c in qs.central], [len(m) for m in qs.marginal])) == base
     assert chunked >= 1
+
+
+def test_wide_item_indexing_matches(P, monkeypatch):
+    # k_expand's 64-bit item loop (batches with > 2^32 frontier items per level) forced on a
+    # small batch gives the 32-bit loop's results
+    kg = synth.make_kg(1)
+    qs = synth.config_queries(kg, 1)
+    g = _graph(P, kg)
+    base = _key(g.search_batch(qs.central, qs.marginal, qs.k, qs.depth))
+    monkeypatch.setenv("RIKI_FORCE_WIDE", "1")
+    assert _key(g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)) == base
+
+
+def test_load_graph_device_matches_host_load(P):
+    import torch
+    kg = synth.make_kg(1)
+    qs = synth.config_queries(kg, 1)
+    host = _graph(P, kg)
+    base = _key(host.search_batch(qs.central, qs.marginal, qs.k, qs.depth))
+    t = [torch.from_numpy(np.ascontiguousarray(x).view(np.int32)).cuda() for x in (kg.src, kg.dst, kg.label_class)]
+    tp = torch.from_numpy(np.ascontiguousarray(kg.term_ptr, np.uint64).view(np.int64)).cuda()
+    po = torch.from_numpy(np.ascontiguousarray(kg.postings, np.uint32).view(np.int32)).cuda()
+    g = P.Graph.from_device(kg.n_nodes, len(kg.src), t[0].data_ptr(), t[1].data_ptr(), t[2].data_ptr(),
+                            len(kg.term_ptr) - 1, tp.data_ptr(), po.data_ptr())
+    del t, tp, po  # copied: the caller may free its arrays
+    torch.cuda.synchronize()
+    g.set_label_weights(0.5, kg.avg_hops)
+    assert (g.activation_levels() == host.activation_levels()).all()
+    assert _key(g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)) == base
+    # device-side validation
+    bad = torch.from_numpy(np.ascontiguousarray(kg.dst).view(np.int32)).cuda()
+    bad[3] = kg.n_nodes
+    good = torch.from_numpy(np.ascontiguousarray(kg.src).view(np.int32)).cuda()
+    tp = torch.from_numpy(np.ascontiguousarray(kg.term_ptr, np.uint64).view(np.int64)).cuda()
+    po = torch.from_numpy(np.ascontiguousarray(kg.postings, np.uint32).view(np.int32)).cuda()
+    with pytest.raises(P.RikiError) as ei:
+        P.Graph.from_device(kg.n_nodes, len(kg.src), good.data_ptr(), bad.data_ptr(), 0, len(kg.term_ptr) - 1,
+                            tp.data_ptr(), po.data_ptr())
+    assert ei.value.code == -1

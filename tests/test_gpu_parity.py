@@ -471,7 +471,7 @@ def test_search_c4_wikidata_scale_depth_sweep(P):
     import time
     t0 = time.time()
     kg = synth.make_kg(4)
-    qs = synth.config_queries(kg, 4, 64)
+    qs = synth.config_queries(kg, 4, 200)  # the bench's batch: 200 x 30M > 2^32 -> 64-bit item loop
     g = P.Graph(kg.n_nodes, kg.src, kg.dst, kg.label_class, kg.term_ptr, kg.postings)
     g.set_label_weights(0.5, kg.avg_hops)
     a = O.coarsen_all(O.fine_weights(kg.n_nodes, kg.src, kg.dst, kg.label_class), 0.5, kg.avg_hops)
@@ -480,7 +480,7 @@ def test_search_c4_wikidata_scale_depth_sweep(P):
     print(f"c4 setup {time.time() - t0:.0f}s")
     for depth in (4, 8, 20):
         res = g.search_batch(qs.central, qs.marginal, qs.k, depth)
-        for i in (0, 1):
+        for i in (0, 1, 177):
             t = time.time()
             ro = _oracle_run(og, kg.posting, qs.central[i], qs.marginal[i], qs.k, depth, want_matrices=False)
             _cmp_results(res[i], ro)

@@ -9,6 +9,7 @@ from scipy.sparse.csgraph import shortest_path
 
 import brute
 import oracle as O
+import synth
 from fixtures import load_golden, random_instance, undirected_to_directed
 
 INF = 0xFF
@@ -382,3 +383,22 @@ def test_tie_break_beam_truncation(seed):
     keys = sorted((c.sc, brute.weight_sum(c.cg_edges, wf), c.v) for c in full.candidates)[:bw]
     r = O.search(g, C, M, 1, 20, beam_w=bw, beam_mode=1, tie_break=1, wfine=wf, early_term=2)
     assert [(c.sc, c.v) for c in r.candidates] == sorted((sc, v) for sc, _, v in keys)
+
+
+def test_oracle_is_reentrant_across_threads():
+    # bench.py's cpu_baseline runs one oracle query per host thread: results must not depend on it
+    from concurrent.futures import ThreadPoolExecutor
+    kg = synth.make_kg(1)
+    qs = synth.config_queries(kg, 1)
+    og = O.Graph(kg.n_nodes, kg.src, kg.dst, O.coarsen_all(O.fine_weights(kg.n_nodes, kg.src, kg.dst,
+                                                                          kg.label_class), 0.5, kg.avg_hops))
+
+    def one(i):
+        r = O.search(og, [kg.posting(t) for t in qs.central[i]], [kg.posting(t) for t in qs.marginal[i]], qs.k,
+                     qs.depth, want_matrices=False, want_candidates=False)
+        return [(x.central_node, x.score, x.edge_ids.tolist()) for x in r.rpgs]
+
+    seq = [one(i) for i in range(len(qs.central))]
+    with ThreadPoolExecutor(8) as ex:
+        par = list(ex.map(one, range(len(qs.central))))
+    assert par == seq
