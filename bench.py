@@ -32,6 +32,10 @@ UNIT = "queries/s"
 
 
 def _workload_name(cfg, spec):
+    if cfg == 5:
+        return (f"C5 {spec.name}: config 4's synthetic KG ({spec.n_nodes} nodes / {spec.n_edges} directed edges), "
+                f"batch of {spec.n_queries} queries: half 2 central + 4 marginal, half the Exp-1 mix "
+                f"{{1,2,4}} x {{2,4,6}}, k={spec.k}, depth {spec.depth}")
     return (f"C{cfg} {spec.name}: synthetic power-law KG {spec.n_nodes} nodes / {spec.n_edges} directed edges, "
             f"{spec.n_central} central + {spec.n_marginal} marginal keywords, k={spec.k}, depth {spec.depth}")
 
@@ -217,6 +221,8 @@ def main():
     nq = args.queries or spec.n_queries
     if world == 1 or args.vp:
         qs = synth.config_queries(kg, args.config, nq)
+    elif args.config == 5:  # weak scaling: each rank its own batch of the same mix
+        qs = synth.c5_queries(kg, nq, 2005 + 7919 * rank)
     else:  # weak scaling: each rank its own query batch of the same shape
         qs = synth.make_queries(kg, nq, spec.n_central, spec.n_marginal, spec.k, spec.depth,
                                 2000 + args.config + 7919 * rank)
@@ -340,7 +346,7 @@ def main():
         "config": {"workload": _workload_name(args.config, spec), "queries_per_step_per_gpu": nq,
                    "l2": "flushed between steps (256 MiB write)", "parallelism": f"vertex-partitioned x{world} (NCCL bit-plane all-gather per level)" if args.vp
                    else f"query-sharded replicas x{world}",
-                   "graph_seed": 1000 + args.config, "query_seed": 2000 + args.config},
+                   "graph_seed": 1000 + synth.GRAPH_OF.get(args.config, args.config), "query_seed": 2000 + args.config},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if peak else None, "traffic": traffic, "traffic_source": traffic_src,
                      "achieved_bytes_per_launch": st["expand_bytes"] / max(1, st["expand_launches"]),

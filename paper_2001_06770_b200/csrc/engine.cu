@@ -2762,8 +2762,8 @@ SlotState make_template(uint32_t k, uint32_t depth, const riki_params &p) {
     return t;
 }
 
-uint32_t auto_slots(riki_graph *g, uint32_t nq, uint32_t rb0, uint32_t rb1) {
-    uint32_t want = g->batch_slots ? g->batch_slots : 256;
+uint32_t auto_slots(riki_graph *g, uint32_t nq, uint32_t rb0, uint32_t rb1, uint32_t want_hint = 0) {
+    uint32_t want = want_hint ? want_hint : g->batch_slots ? g->batch_slots : 256;
     want = std::min<uint32_t>(want, MAX_SLOTS);
     want = std::min<uint32_t>(want, std::max<uint32_t>(nq, 1));
     // an existing workspace that already fits needs no memory query (cudaMemGetInfo can take
@@ -2940,11 +2940,11 @@ static void check_common(riki_graph *g, uint32_t k, uint32_t depth, const riki_p
     if (p.beam_w && p.beam_w < k) RIKI_THROW(RIKI_EINVAL, "beam width must be >= k (P:309)");
 }
 
-static Caps initial_caps(riki_graph *g, uint32_t nq, uint32_t k, uint32_t rb0, uint32_t rb1) {
+static Caps initial_caps(riki_graph *g, uint32_t nq, uint32_t k, uint32_t rb0, uint32_t rb1, uint32_t want_hint = 0) {
     Caps c;
     c.rb[0] = rb0;
     c.rb[1] = rb1;
-    c.slots = auto_slots(g, nq, rb0, rb1);
+    c.slots = auto_slots(g, nq, rb0, rb1, want_hint);
     c.capc = std::min<uint32_t>(16384, next_pow2(g->V + 1));
     c.kmax = std::max<uint32_t>(k, g->ws ? g->ws->kmax : 1);
     c.arena = std::max<uint64_t>(64ull << 20, g->ws ? g->ws->arena_cap : 0);
@@ -3045,9 +3045,10 @@ void engine_search_device(riki_graph *g, uint32_t nq, const uint64_t *d_cptr, co
     }
     if (maxc > RIKI_MAX_TERMS || maxm > RIKI_MAX_TERMS) RIKI_THROW(RIKI_EINVAL, "at most 8 terms per keyword class");
     tr("ptr D2H");
-    Caps caps = initial_caps(g, nq, k, row_bytes(std::max(maxc, 1u)), row_bytes(std::max(maxm, 1u)));
+    // the whole batch in flight when it fits the device memory (auto_slots), else chunks
+    Caps caps = initial_caps(g, nq, k, row_bytes(std::max(maxc, 1u)), row_bytes(std::max(maxm, 1u)),
+                             std::max(g->batch_slots, std::min<uint32_t>(nq, MAX_SLOTS)));
     tr("initial_caps");
-    caps.slots = std::max(caps.slots, std::min<uint32_t>(nq, MAX_SLOTS));
     ensure_workspace(g, caps);
     Launch L{g, g->stream};
     SlotState tmpl = make_template(k, depth, p);

@@ -83,7 +83,12 @@ CONFIGS = {
                   *_scaled(5, 6059, 5_000_000, 15.1e6), 8192, 3.87),
     4: ConfigSpec("wikidata-30M", 30_000_000, 150_000_000, 2000, 2, 4, 20, 20, 200,
                   *_scaled(51, 87102, 30_000_000, 30.6e6), 1024, 3.68, True),
+    # C5: config 4's graph (same seed) with a 10k-query throughput batch: half 2 + 4, half the
+    # Exp-1 mix cknum x mknum in {1,2,4} x {2,4,6} -- see c5_queries
+    5: ConfigSpec("wikidata-30M-throughput", 30_000_000, 150_000_000, 2000, 2, 4, 20, 20, 10_000,
+                  *_scaled(51, 87102, 30_000_000, 30.6e6), 1024, 3.68, True),
 }
+GRAPH_OF = {5: 4}  # configs that share another config's graph (and its seed)
 
 
 def _chung_lu_weights(rng, n, exponent):
@@ -188,6 +193,8 @@ def exact_avg_hops(n_nodes, src, dst):
 
 
 def make_kg(cfg: int | ConfigSpec, seed: int | None = None) -> KG:
+    if isinstance(cfg, int):
+        cfg = GRAPH_OF.get(cfg, cfg)
     spec = CONFIGS[cfg] if isinstance(cfg, int) else cfg
     num = cfg if isinstance(cfg, int) else 0
     seed = 1000 + num if seed is None else seed
@@ -212,7 +219,22 @@ def make_queries(kg: KG, n_queries: int, n_central: int, n_marginal: int, k: int
     return QuerySet(cs, ms, k, depth)
 
 
+def c5_queries(kg: KG, n_queries: int, seed: int = 2005) -> QuerySet:
+    """Config 5's batch: even queries 2 central + 4 marginal, odd queries drawn from the
+    Exp-1 mix cknum in {1, 2, 4} x mknum in {2, 4, 6}; k = 20, D = 20."""
+    rng = np.random.default_rng(seed)
+    cs, ms = [], []
+    for i in range(n_queries):
+        nc, nm = (2, 4) if i % 2 == 0 else (int(rng.choice([1, 2, 4])), int(rng.choice([2, 4, 6])))
+        t = rng.choice(kg.n_terms, size=nc + nm, replace=False)
+        cs.append([int(x) for x in t[:nc]])
+        ms.append([int(x) for x in t[nc:]])
+    return QuerySet(cs, ms, 20, 20)
+
+
 def config_queries(kg: KG, cfg: int, n_queries: int | None = None) -> QuerySet:
+    if cfg == 5:
+        return c5_queries(kg, n_queries or CONFIGS[5].n_queries)
     spec = CONFIGS[cfg]
     return make_queries(kg, n_queries or spec.n_queries, spec.n_central, spec.n_marginal, spec.k, spec.depth,
                         2000 + cfg)

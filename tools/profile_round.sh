@@ -34,3 +34,7 @@ echo "full capture: k_expand launch ordinal $SKIP"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_expand -s $SKIP -c 1 \
     -o gpurun_out/${R}_expand_full python bench.py --steps 1 --warmup 1 --quick > gpurun_out/${R}_full.log 2>&1
 echo profile_done
+# 4) DRAM bytes and duration of EVERY launch of one step: per-kernel achieved DRAM GB/s
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 3000 \
+    --csv --log-file gpurun_out/${R}_all_dram.csv python bench.py --steps 1 --warmup 1 --quick > gpurun_out/${R}_all_dram.log 2>&1
+echo dram_done
