@@ -2281,6 +2281,18 @@ struct Workspace {
     uint64_t bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     std::vector<cudaEvent_t> evpool;
+    // CUDA graphs of LEVEL_BATCH-level chunks of the level loop, keyed by everything their
+    // kernel nodes bake in (phase, first level, kernel variants, grids, device views)
+    struct GraphEntry {
+        std::vector<uint8_t> key;
+        cudaGraphExec_t exec;
+        uint32_t kernels;
+    };
+    std::vector<GraphEntry> gcache;
+    void clear_graphs() {
+        for (GraphEntry &e : gcache) cudaGraphExecDestroy(e.exec);
+        gcache.clear();
+    }
     cudaEvent_t event(uint32_t i) {
         while (evpool.size() <= i) {
             cudaEvent_t e;
@@ -2308,6 +2320,7 @@ struct Workspace {
         return p;
     }
     void release() {
+        clear_graphs();
         for (void *p : allocs) cudaFree(p);
         allocs.clear();
         if (h_ctr) cudaFreeHost(h_ctr);
@@ -2321,6 +2334,7 @@ struct Workspace {
     }
     WsDev dev() const {
         WsDev d;
+        memset(&d, 0, sizeof(d));  // padding too: the struct is part of CUDA-graph cache keys
         d.st = st; d.nslots = cur ? cur : slots; d.V = V; d.W = W; d.capc = capc; d.kmax = kmax;
         d.H[0] = H[0]; d.H[1] = H[1]; d.hnode = hnode; d.SP = SP; d.rb[0] = last_rb[0]; d.rb[1] = last_rb[1];
         d.q = q; d.qcap = qcap; d.bm = bm; d.jq = jq; d.jbm = jbm; d.ck = ck; d.cd = cd; d.rk = rk; d.offs = offs; d.coffs = coffs; d.pslots = pslots; d.track_reached = track_reached;
@@ -2543,12 +2557,23 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
     // The host checks for termination only every LEVEL_BATCH levels: all per-level kernels
     // use fixed grids and read their work counts on the device, so levels past a slot's end
     // are device-side no-ops and the number of host synchronisations per run drops ~4x.
-    for (uint32_t l = 0; l <= max_levels; l++) {
+    static const bool trace_levels = getenv("RIKI_LEVELS") != nullptr;
+    const bool no_graphs = getenv("RIKI_NO_GRAPHS") != nullptr || getenv("RIKI_SYNC") != nullptr;
+    const bool wide = (uint64_t)wd.nslots * ws->qcap >= (1ull << 32) || wide_forced;
+    // LEVEL_BATCH-level chunks replay as one CUDA graph (one launch instead of ~9 per level);
+    // the per-level profiling events, the pull / vertex-partitioned levels (host-sized grids,
+    // NCCL) and the level trace keep the plain launches
+    const bool use_graphs = !no_graphs && !L.g->profiling && !pull && !joint && !trace_levels;
+    // graph keys must not depend on the candidate count (a miss costs a capture and an
+    // instantiation, milliseconds): grid-stride attach with one fixed grid
+    const uint32_t attach_blocks = total_cands ? 148 * 16 : 0;
+    const uint32_t pull_min = vp ? 0u : !L.g->pull_on ? 0xFFFFFFFFu : std::max<uint32_t>(ws->V / PULL_MIN_DIV, 1);
+    auto level_pre = [&](uint32_t l) {  // run 2: attach / RPG recovery / decide; then the plan
         if (ph == 1) {
             k_reset_level_ctrs<<<1, 1, 0, s>>>(wd);
             L.check(__LINE__);
             if (total_cands) {
-                k_attach<RowT><<<grid_of(total_cands * 32, 256), 256, 0, s>>>(wd);
+                k_attach<RowT><<<attach_blocks, 256, 0, s>>>(wd);
                 L.check(__LINE__);
                 k_extract_rpg<RowT, 0><<<148 * tier0_blocks_per_sm(k_extract_rpg<RowT, 0>), tier_threads<0>(), smem_ex<0>(), s>>>(gd, wd);
                 L.check(__LINE__);
@@ -2560,15 +2585,10 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             k_decide_m<<<wd.nslots, 256, 1024 * 16, s>>>(wd, l);
             L.check(__LINE__);
         }
-        k_plan<<<1, MAX_SLOTS, 0, s>>>(wd, ph, l, vp ? 0u : !L.g->pull_on ? 0xFFFFFFFFu : std::max<uint32_t>(ws->V / PULL_MIN_DIV, 1));
+        k_plan<<<1, MAX_SLOTS, 0, s>>>(wd, ph, l, pull_min);
         L.check(__LINE__);
-        if (l % LEVEL_BATCH == LEVEL_BATCH - 1 || l == max_levels || pull) {
-            CUDA_TRY(cudaMemcpyAsync(ws->h_ctr, ws->ctr, C_NCTR * 4, cudaMemcpyDeviceToHost, s));
-            CUDA_TRY(cudaStreamSynchronize(s));
-            if (ws->h_ctr[C_ACTIVE] == 0) break;
-        }
-        L.levels++;
-        if (L.g->profiling) CUDA_TRY(cudaEventRecord(ws->event(L.nev++), s));
+    };
+    auto level_expand = [&](uint32_t l) {
         if (joint) {
             if constexpr (sizeof(RowT) <= 4) {
                 k_jexpand<RowT, false><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
@@ -2577,7 +2597,7 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
                 L.check(__LINE__);
             }
         } else {
-            if ((uint64_t)wd.nslots * ws->qcap >= (1ull << 32) || wide_forced)
+            if (wide)
                 k_expand<RowT, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
             else
                 k_expand<RowT, false><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
@@ -2585,6 +2605,67 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             k_expand_heavy<RowT><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
             L.check(__LINE__);
         }
+    };
+    for (uint32_t l = 0; l <= max_levels; l++) {
+        if (use_graphs) {  // levels [l, l + n) as one graph, then the host termination check
+            const uint32_t n = std::min<uint32_t>(LEVEL_BATCH - l % LEVEL_BATCH, max_levels + 1 - l);
+            struct Key {
+                int ph;
+                uint32_t l0, n, rbT, rbC, wide, attach_blocks, big_ctas, tier0;
+                WsDev wd;
+                GraphDev gd;
+            } key;
+            memset(&key, 0, sizeof(key));
+            key.ph = ph; key.l0 = l; key.n = n; key.rbT = sizeof(RowT); key.rbC = sizeof(RowC); key.wide = wide;
+            key.attach_blocks = attach_blocks; key.big_ctas = ws->big_ctas;
+            key.tier0 = tier0_blocks_per_sm(k_extract_rpg<RowT, 0>);
+            key.wd = wd; key.gd = gd;
+            const uint8_t *kb = (const uint8_t *)&key;
+            Workspace::GraphEntry *hit = nullptr;
+            for (Workspace::GraphEntry &e : ws->gcache)
+                if (e.key.size() == sizeof(key) && !memcmp(e.key.data(), kb, sizeof(key))) { hit = &e; break; }
+            if (!hit) {
+                if (ws->gcache.size() >= 512) ws->clear_graphs();
+                const uint64_t before = L.launches;
+                cudaGraph_t graph = nullptr;
+                CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+                try {
+                    for (uint32_t i = 0; i < n; i++) {
+                        level_pre(l + i);
+                        level_expand(l + i);
+                    }
+                } catch (...) {
+                    cudaStreamEndCapture(s, &graph);
+                    if (graph) cudaGraphDestroy(graph);
+                    throw;
+                }
+                CUDA_TRY(cudaStreamEndCapture(s, &graph));
+                cudaGraphExec_t exec = nullptr;
+                const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+                cudaGraphDestroy(graph);
+                if (e != cudaSuccess) RIKI_THROW(RIKI_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+                ws->gcache.push_back({std::vector<uint8_t>(kb, kb + sizeof(key)), exec, (uint32_t)(L.launches - before)});
+                L.launches = before;
+                hit = &ws->gcache.back();
+            }
+            CUDA_TRY(cudaGraphLaunch(hit->exec, s));
+            L.launches += hit->kernels;
+            CUDA_TRY(cudaMemcpyAsync(ws->h_ctr, ws->ctr, C_NCTR * 4, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            L.levels += n;
+            if (ws->h_ctr[C_ACTIVE] == 0) break;  // (the last level's expansion was a device no-op)
+            l += n - 1;
+            continue;
+        }
+        level_pre(l);
+        if (l % LEVEL_BATCH == LEVEL_BATCH - 1 || l == max_levels || pull) {
+            CUDA_TRY(cudaMemcpyAsync(ws->h_ctr, ws->ctr, C_NCTR * 4, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            if (ws->h_ctr[C_ACTIVE] == 0) break;
+        }
+        L.levels++;
+        if (L.g->profiling) CUDA_TRY(cudaEventRecord(ws->event(L.nev++), s));
+        level_expand(l);
         if (vp) {
             if (uint32_t npull = ws->h_ctr[C_NPULL]) vp_level<RowT>(L, gd, wd, ph, l, npull);
         } else if (L.g->pull_on) {
@@ -2600,7 +2681,6 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             CUDA_TRY(cudaEventRecord(ws->event(L.nev++), s));
             L.expand_launches += 2 + (ws->h_ctr[C_NPULL] ? 1 : 0);
         }
-        static const bool trace_levels = getenv("RIKI_LEVELS") != nullptr;
         if (trace_levels) {  // diagnostics: per-level frontier / edge / new-cell counts (syncs every level)
             static unsigned long long last[P_NPROF];
             unsigned long long pr[P_NPROF];

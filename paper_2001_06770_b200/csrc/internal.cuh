@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstring>
 #include <vector>
 
 #include "../../include/riki.h"
@@ -96,6 +97,7 @@ struct riki_graph {
 
     GraphDev dev() const {
         GraphDev g;
+        memset(&g, 0, sizeof(g));  // padding too: the struct is part of CUDA-graph cache keys
         g.V = V; g.E = E;
         g.row = d_row; g.col = d_col; g.act = d_act; g.desc = d_desc; g.aoff = d_aoff; g.idesc = d_idesc; g.iaoff = d_iaoff;
         g.irow = d_irow; g.isrc = d_isrc; g.ieid = d_ieid; g.iact = d_iact;

@@ -92,3 +92,21 @@ def test_load_graph_device_matches_host_load(P):
         P.Graph.from_device(kg.n_nodes, len(kg.src), good.data_ptr(), bad.data_ptr(), 0, len(kg.term_ptr) - 1,
                             tp.data_ptr(), po.data_ptr())
     assert ei.value.code == -1
+
+
+def test_level_graphs_match_plain_launches(P, monkeypatch):
+    # the level loop replayed as CUDA graphs (default) and as plain launches give the same
+    # results, over repeated calls (graph cache hits) and changing batch shapes
+    kg = synth.make_kg(1)
+    qs = synth.config_queries(kg, 1)
+    g = _graph(P, kg)
+    monkeypatch.setenv("RIKI_NO_GRAPHS", "1")
+    plain = _key(g.search_batch(qs.central, qs.marginal, qs.k, qs.depth))
+    single = [_key([g.search(qs.central[i], qs.marginal[i], qs.k, qs.depth)]) for i in range(8)]
+    H0 = g.hitting_levels(np.arange(3, dtype=np.uint32), 20, 1)
+    monkeypatch.delenv("RIKI_NO_GRAPHS")
+    for _ in range(2):
+        assert _key(g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)) == plain
+        assert [_key([g.search(qs.central[i], qs.marginal[i], qs.k, qs.depth)]) for i in range(8)] == single
+    H1 = g.hitting_levels(np.arange(3, dtype=np.uint32), 20, 1)
+    assert all((a == b).all() if hasattr(a, "all") else a == b for a, b in zip(H0, H1))
