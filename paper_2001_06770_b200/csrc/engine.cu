@@ -44,7 +44,10 @@ constexpr uint32_t EMPTY = 0xFFFFFFFFu;
 constexpr uint32_t SORT_SMEM = 8192;  // u32 keys sorted in shared memory
 
 enum Ctr { C_NHEAVY = 0, C_NNEWATT, C_NOVF, C_ACTIVE, C_TOTAL, C_NCAND_TOTAL, C_NOVF2, C_NPULL, C_JQN0, C_JQN1,
-           C_JQCUR, C_JHEAVY, C_NCTR = 16 };
+           C_JQCUR, C_JHEAVY, C_LEVEL, C_NCTR = 16 };
+// level argument of the per-level kernels: a value, or LV_DEVICE = read the device level
+// counter ctr[C_LEVEL] (the whole-run CUDA graph with a device-side while loop)
+constexpr uint32_t LV_DEVICE = 0xFFFFFFFFu;
 enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_PULLNODES, P_PULLEDGES,
             // recovery diagnostics (compiled in with -DREC_STATS=1)
             P_R_BUILDS = 8, P_R_BEDGES, P_R_BCYC, P_R_WAITS, P_R_WCYC, P_R_CANDS, P_R_CANDCYC, P_R_CANDMAX, P_R_BMAX,
@@ -296,7 +299,8 @@ template <class RowT> __global__ void k_seed(GraphDev g, WsDev w, int ph) {
 #define PULL_MIN_DIV 64
 #endif
 // pull_min: minimum frontier for bottom-up (0xFFFFFFFF disables it)
-__global__ void k_plan(WsDev w, int ph, uint32_t l, uint32_t pull_min) {
+__global__ void k_plan(WsDev w, int ph, uint32_t l_arg, uint32_t pull_min) {
+    const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
     __shared__ unsigned long long sc[MAX_SLOTS];
     __shared__ uint32_t nact, npull;
     __shared__ unsigned long long nenq;
@@ -558,8 +562,9 @@ template <class RowT> struct alignas(16) OwnF {
 // (slots x queue capacity >= 2^32, e.g. 200 queries on a 30M-node graph); the common
 // case keeps the 32-bit loop.
 template <class RowT, bool WIDE>
-__global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, int ph, uint32_t l) {
+__global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, int ph, uint32_t l_arg) {
     typedef Row<RowT> R;
+    const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
     typedef typename std::conditional<WIDE, unsigned long long, uint32_t>::type IdxT;
     __shared__ IdxT s_offs[MAX_SLOTS + 1];
     __shared__ uint32_t s_info[MAX_SLOTS];
@@ -738,7 +743,8 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
 }
 
 // Heavy ranges (hub rows): one warp per CHUNK-edge piece, two edges per lane in flight.
-template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l) {
+template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l_arg) {
+    const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
     typedef Row<RowT> R;
     const uint32_t lane = lane_id();
     const uint32_t nxt = (l & 1) ^ 1;
@@ -1961,7 +1967,8 @@ __device__ void cta_sort_u128(u128 *keys, uint32_t n, u128 *smem, uint32_t smem_
 // Termination of run 2 at level l (after attach): depth, empty frontier, all attached, or
 // the exact bound (R21): |R| >= k and the best key any unattached candidate can still
 // reach, (gamma*S^c + (1-gamma)*(l+1), S^c, v), is worse than the k-th key of R.
-__global__ void k_decide_m(WsDev w, uint32_t l) {
+__global__ void k_decide_m(WsDev w, uint32_t l_arg) {
+    const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
     extern __shared__ __align__(16) u128 sm128[];
     __shared__ uint32_t first;
     uint32_t s = blockIdx.x;
@@ -2498,6 +2505,16 @@ template <class K> uint32_t tier0_blocks_per_sm(K kernel) {
     return cached;
 }
 
+// Device-side loop control of the whole-run graph (after level l's plan and expansion):
+// continue while some slot is still in its run and l < max_levels (the host loop's rule),
+// and advance the level counter.
+__global__ void k_loop_cond(WsDev w, cudaGraphConditionalHandle h, uint32_t max_levels) {
+    const uint32_t l = w.ctr[C_LEVEL];
+    const bool go = w.ctr[C_ACTIVE] != 0 && l < max_levels;
+    w.ctr[C_LEVEL] = l + 1;
+    cudaGraphSetConditional(h, go ? 1u : 0u);
+}
+
 // One vertex-partitioned level: pull over this rank's node range into its
 // slice of the bit-plane buffer (every range, in simulated mode), one in-place all-gather
 // on the search stream, then every rank applies all slices.  Identical H, blocks, frontiers
@@ -2566,7 +2583,11 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
     const bool use_graphs = !no_graphs && !L.g->profiling && !pull && !joint && !trace_levels;
     // graph keys must not depend on the candidate count (a miss costs a capture and an
     // instantiation, milliseconds): grid-stride attach with one fixed grid
-    const uint32_t attach_blocks = total_cands ? 148 * 16 : 0;
+    // (sized by the slots in flight: a lone query's idle levels then cost a few blocks, not
+    // 2368 -- single-query latency; full grids from 32 slots up)
+    const uint32_t attach_blocks = total_cands ? std::min<uint32_t>(148 * 16, 64 * wd.nslots) : 0;
+    const uint32_t rpg0_blocks = std::min<uint32_t>(148 * tier0_blocks_per_sm(k_extract_rpg<RowT, 0>), 32 * wd.nslots);
+    const uint32_t rpg1_blocks = std::min<uint32_t>(148 * 3, 8 * wd.nslots);
     const uint32_t pull_min = vp ? 0u : !L.g->pull_on ? 0xFFFFFFFFu : std::max<uint32_t>(ws->V / PULL_MIN_DIV, 1);
     auto level_pre = [&](uint32_t l) {  // run 2: attach / RPG recovery / decide; then the plan
         if (ph == 1) {
@@ -2575,9 +2596,9 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             if (total_cands) {
                 k_attach<RowT><<<attach_blocks, 256, 0, s>>>(wd);
                 L.check(__LINE__);
-                k_extract_rpg<RowT, 0><<<148 * tier0_blocks_per_sm(k_extract_rpg<RowT, 0>), tier_threads<0>(), smem_ex<0>(), s>>>(gd, wd);
+                k_extract_rpg<RowT, 0><<<rpg0_blocks, tier_threads<0>(), smem_ex<0>(), s>>>(gd, wd);
                 L.check(__LINE__);
-                k_extract_rpg<RowT, 1><<<148 * 3, 256, smem_ex<1>(), s>>>(gd, wd);
+                k_extract_rpg<RowT, 1><<<rpg1_blocks, 256, smem_ex<1>(), s>>>(gd, wd);
                 L.check(__LINE__);
                 k_extract_rpg_big<RowT><<<ws->big_ctas, 256, 0, s>>>(gd, wd);
                 L.check(__LINE__);
@@ -2606,6 +2627,69 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             L.check(__LINE__);
         }
     };
+    if (use_graphs && !getenv("RIKI_CHUNK_GRAPHS")) {
+        // The whole run as ONE graph: a device-side while loop (conditional node) around one
+        // level's kernels, the level index in ctr[C_LEVEL], the continue decision taken by
+        // k_loop_cond from the plan's active-slot count -- no host round trip per level.
+        struct Key {
+            int ph;
+            uint32_t max_levels, rbT, rbC, wide, attach_blocks, big_ctas, tier0, whole;
+            WsDev wd;
+            GraphDev gd;
+        } key;
+        memset(&key, 0, sizeof(key));
+        key.ph = ph; key.max_levels = max_levels; key.rbT = sizeof(RowT); key.rbC = sizeof(RowC); key.wide = wide;
+        key.attach_blocks = attach_blocks; key.big_ctas = ws->big_ctas; key.whole = 1;
+        key.tier0 = tier0_blocks_per_sm(k_extract_rpg<RowT, 0>);
+        key.wd = wd; key.gd = gd;
+        const uint8_t *kb = (const uint8_t *)&key;
+        Workspace::GraphEntry *hit = nullptr;
+        for (Workspace::GraphEntry &e : ws->gcache)
+            if (e.key.size() == sizeof(key) && !memcmp(e.key.data(), kb, sizeof(key))) { hit = &e; break; }
+        if (!hit) {
+            if (ws->gcache.size() >= 512) ws->clear_graphs();
+            cudaGraph_t graph = nullptr;
+            CUDA_TRY(cudaGraphCreate(&graph, 0));
+            cudaGraphExec_t exec = nullptr;
+            uint64_t before = L.launches;
+            try {
+                cudaGraphConditionalHandle h;
+                CUDA_TRY(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+                cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+                cp.conditional.handle = h;
+                cp.conditional.type = cudaGraphCondTypeWhile;
+                cp.conditional.size = 1;
+                cudaGraphNode_t wn;
+                CUDA_TRY(cudaGraphAddNode(&wn, graph, nullptr, 0, &cp));
+                cudaGraph_t body = cp.conditional.phGraph_out[0];
+                CUDA_TRY(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+                try {
+                    level_pre(LV_DEVICE);
+                    level_expand(LV_DEVICE);
+                    k_loop_cond<<<1, 1, 0, s>>>(wd, h, max_levels);
+                    L.check(__LINE__);
+                } catch (...) {
+                    cudaGraph_t dummy = nullptr;
+                    cudaStreamEndCapture(s, &dummy);
+                    throw;
+                }
+                CUDA_TRY(cudaStreamEndCapture(s, &body));
+                const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+                if (e != cudaSuccess) RIKI_THROW(RIKI_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+            } catch (...) {
+                cudaGraphDestroy(graph);
+                throw;
+            }
+            cudaGraphDestroy(graph);
+            ws->gcache.push_back({std::vector<uint8_t>(kb, kb + sizeof(key)), exec, (uint32_t)(L.launches - before)});
+            L.launches = before;
+            hit = &ws->gcache.back();
+        }
+        CUDA_TRY(cudaMemsetAsync(ws->ctr + C_LEVEL, 0, 4, s));
+        CUDA_TRY(cudaGraphLaunch(hit->exec, s));
+        L.launches += hit->kernels;  // kernels per level (the level count is known on the device only)
+        L.levels += 1;
+    } else
     for (uint32_t l = 0; l <= max_levels; l++) {
         if (use_graphs) {  // levels [l, l + n) as one graph, then the host termination check
             const uint32_t n = std::min<uint32_t>(LEVEL_BATCH - l % LEVEL_BATCH, max_levels + 1 - l);

@@ -105,8 +105,37 @@ def test_level_graphs_match_plain_launches(P, monkeypatch):
     single = [_key([g.search(qs.central[i], qs.marginal[i], qs.k, qs.depth)]) for i in range(8)]
     H0 = g.hitting_levels(np.arange(3, dtype=np.uint32), 20, 1)
     monkeypatch.delenv("RIKI_NO_GRAPHS")
-    for _ in range(2):
-        assert _key(g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)) == plain
-        assert [_key([g.search(qs.central[i], qs.marginal[i], qs.k, qs.depth)]) for i in range(8)] == single
-    H1 = g.hitting_levels(np.arange(3, dtype=np.uint32), 20, 1)
-    assert all((a == b).all() if hasattr(a, "all") else a == b for a, b in zip(H0, H1))
+    for chunked in (False, True):  # whole-run graph (device while loop) / 4-level chunk graphs
+        if chunked:
+            monkeypatch.setenv("RIKI_CHUNK_GRAPHS", "1")
+        for _ in range(2):
+            assert _key(g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)) == plain
+            assert [_key([g.search(qs.central[i], qs.marginal[i], qs.k, qs.depth)]) for i in range(8)] == single
+        H1 = g.hitting_levels(np.arange(3, dtype=np.uint32), 20, 1)
+        assert all((a == b).all() if hasattr(a, "all") else a == b for a, b in zip(H0, H1))
+        for D in (0, 1, 3):  # depth bounds around the loop's exit rule
+            monkeypatch.setenv("RIKI_NO_GRAPHS", "1")
+            ref = _key(g.search_batch(qs.central, qs.marginal, qs.k, D))
+            monkeypatch.delenv("RIKI_NO_GRAPHS")
+            assert _key(g.search_batch(qs.central, qs.marginal, qs.k, D)) == ref
+
+
+@pytest.mark.timeout(600)
+def test_bench_two_ranks_replicated_gloo(P):
+    # bench.py's multi-rank path (torchrun, weak scaling, max over ranks) with two ranks sharing
+    # the pool's one GPU (gloo for the plumbing; the contract run uses NCCL, one GPU per rank)
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RIKI_BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2", "--master-addr",
+           "127.0.0.1", "--master-port", "29517", "bench.py", "--gpus", "2", "--config", "1", "--steps", "2",
+           "--warmup", "3", "--no-cpu", "--latency-queries", "2"]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=500)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["gpu_launches"] > 0
