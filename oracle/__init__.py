@@ -279,3 +279,41 @@ def search(g: Graph, central_nodes, marginal_nodes, k: int, depth: int, gamma: f
         return out
     finally:
         lib.orc_result_free(r)
+
+
+# ---------------------------------------------------------------- Abar by sampled pairs
+HOP_INF = 0xFFFFFFFF
+
+
+def sample_avg_hops(n_nodes: int, src, dst, ps, pt, max_hops: int = 255):
+    """P:611 "We sample ten thousand pairs of nodes for estimation of Abar" (Abar: "the average
+    shortest hops in the graph").  Reading R30: d(s, t) = fewest edges of a directed path
+    s -> t in the edge list (BFS; scipy's unweighted shortest_path is the BFS step), pairs with no
+    path within max_hops are left out; mean and sample standard deviation (n - 1) from exact
+    integer moments: mean = S1 / n, sd = sqrt((n*S2 - S1^2) / (n * (n - 1))).
+    Returns (mean, sd, n_reached, dist[] with HOP_INF for no path)."""
+    import math
+
+    import scipy.sparse as sp
+    import scipy.sparse.csgraph as cg
+    src = np.asarray(src, np.int64)
+    dst = np.asarray(dst, np.int64)
+    ps = np.asarray(ps, np.int64)
+    pt = np.asarray(pt, np.int64)
+    dist = np.full(len(ps), HOP_INF, np.uint32)
+    if len(ps):
+        A = sp.csr_matrix((np.ones(len(src)), (src, dst)), shape=(n_nodes, n_nodes))
+        uniq = np.unique(ps)
+        row = {int(x): i for i, x in enumerate(uniq)}
+        D = cg.shortest_path(A, directed=True, unweighted=True, indices=uniq)
+        for i, (s_, t_) in enumerate(zip(ps, pt)):
+            d = D[row[int(s_)], int(t_)]
+            if np.isfinite(d) and d <= max_hops:
+                dist[i] = int(d)
+    ok = [int(x) for x in dist if x != HOP_INF]
+    n = len(ok)
+    s1 = sum(ok)
+    s2 = sum(x * x for x in ok)
+    mean = float(s1) / float(n) if n else float("nan")
+    sd = math.sqrt(float(n * s2 - s1 * s1) / (float(n) * float(n - 1))) if n >= 2 else float("nan")
+    return mean, sd, n, dist

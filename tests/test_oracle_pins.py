@@ -402,3 +402,58 @@ def test_oracle_is_reentrant_across_threads():
     with ThreadPoolExecutor(8) as ex:
         par = list(ex.map(one, range(len(qs.central))))
     assert par == seq
+
+
+# ----------------------------------------------------------------- Abar by sampled pairs (R30)
+def _bfs_brute(V, src, dst, s):
+    from collections import deque
+    adj = [[] for _ in range(V)]
+    for a, b in zip(src, dst):
+        adj[int(a)].append(int(b))
+    d = [None] * V
+    d[s] = 0
+    q = deque([s])
+    while q:
+        u = q.popleft()
+        for w in adj[u]:
+            if d[w] is None:
+                d[w] = d[u] + 1
+                q.append(w)
+    return d
+
+
+def test_sample_avg_hops_hand_fixtures():
+    # path 0-1-2-3-4 (bidirected) plus a one-way edge 5 -> 0
+    und = [(0, 1), (1, 2), (2, 3), (3, 4)]
+    src = [a for a, b in und] + [b for a, b in und] + [5]
+    dst = [b for a, b in und] + [a for a, b in und] + [0]
+    m, sd, n, d = O.sample_avg_hops(6, src, dst, [0, 1, 2, 5, 0], [4, 3, 2, 4, 5])
+    assert d.tolist() == [4, 2, 0, 5, O.HOP_INF]  # 0 cannot reach 5 (one-way edge)
+    assert n == 4 and m == 11 / 4
+    assert abs(sd - np.std([4, 2, 0, 5], ddof=1)) < 1e-15
+    m, sd, n, d = O.sample_avg_hops(6, src, dst, [0, 1], [4, 3], max_hops=3)
+    assert d.tolist() == [O.HOP_INF, 2] and n == 1 and m == 2.0 and np.isnan(sd)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_sample_avg_hops_matches_brute_bfs(seed):
+    import statistics
+    rng = np.random.default_rng(8800 + seed)
+    V, src, dst, _, _ = random_instance(rng, 5, 60, deg=float(rng.choice([1.0, 2.0, 3.0])))
+    if seed % 3 == 0:  # some one-way edges
+        keep = rng.random(len(src)) < 0.8
+        src, dst = src[keep], dst[keep]
+    ps = rng.integers(0, V, 40)
+    pt = rng.integers(0, V, 40)
+    m, sd, n, d = O.sample_avg_hops(V, src, dst, ps, pt)
+    exp = []
+    for s_, t_ in zip(ps, pt):
+        x = _bfs_brute(V, src, dst, int(s_))[int(t_)]
+        exp.append(O.HOP_INF if x is None else x)
+    assert d.tolist() == exp
+    ok = [x for x in exp if x != O.HOP_INF]
+    assert n == len(ok)
+    if len(ok) >= 1:
+        assert abs(m - statistics.fmean(ok)) <= 1e-12 * max(1.0, m)
+    if len(ok) >= 2:
+        assert abs(sd - statistics.stdev(ok)) <= 1e-12 * max(1.0, sd)
