@@ -247,6 +247,18 @@ riki_status riki_set_direction(riki_graph *g, int mode);
 riki_status riki_set_joint(riki_graph *g, int on);
 /* Batch slots (queries in flight per launch); 0 = automatic from free device memory. */
 riki_status riki_set_batch_slots(riki_graph *g, uint32_t slots);
+/* Abar estimation: "We sample ten thousand pairs of nodes for
+ * estimation of Abar", the average shortest hops that Eq. 1-3 scale around.
+ * src/dst: n_pairs node ids (caller ids, host arrays); the caller draws the pairs.  d(s, t)
+ * = fewest edges of a directed path s -> t in the caller's edge list (bidirected: the
+ * undirected distance), found by batched level-synchronous BFS on the device, at most
+ * max_hops levels (>= 1).  Outputs (each may be NULL): mean and sample standard deviation
+ * (n - 1) over the n_reached pairs with a path (NaN when n_reached < 1 / < 2), computed from
+ * exact integer moments (R30); dist_out[n_pairs] the distances (0xFFFFFFFF = no path within
+ * max_hops).  Needs no activation levels.  Errors: RIKI_EINVAL (ids, max_hops), RIKI_ENOMEM. */
+riki_status riki_sample_avg_hops(riki_graph *g, uint32_t n_pairs, const uint32_t *src, const uint32_t *dst,
+                                 uint32_t max_hops, double *mean, double *stddev, uint64_t *n_reached,
+                                 uint32_t *dist_out);
 /* Recovery-arena limit in 32-bit words (0 = default: the 2^32 addressable by its offsets).
  * A batch whose recovered subgraphs and memoised predecessor lists (Alg. 2) need more runs
  * in chunks of fewer queries; a device batch that ran in chunks has its results collected

@@ -9,7 +9,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("RIKI_LIB_OUT", os.path.join(HERE, "libriki.so"))
-SOURCES = ["graph.cu", "engine.cu", "api.cu", "dist.cu"]
+SOURCES = ["graph.cu", "engine.cu", "api.cu", "dist.cu", "hops.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [*os.environ.get("RIKI_DEFS", "").split(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "--expt-relaxed-constexpr", "-Xptxas", "-v"]

@@ -1,6 +1,7 @@
 // api.cu -- the C-ABI entry points of libriki.so (include/riki.h): argument checks,
 // exception-to-status translation, thread-local error text and host result objects.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <new>
 #include <string>
@@ -316,6 +317,39 @@ riki_status riki_set_joint(riki_graph *g, int on) {
         need(g, "null graph");
         need(!(on && g->vp()), "joint traversal is not available in vertex-partitioned mode");
         g->joint_on = on != 0;
+    });
+}
+
+riki_status riki_sample_avg_hops(riki_graph *g, uint32_t n_pairs, const uint32_t *src, const uint32_t *dst,
+                                 uint32_t max_hops, double *mean, double *stddev, uint64_t *n_reached,
+                                 uint32_t *dist_out) {
+    return guard([&] {
+        need(g, "null graph");
+        need(n_pairs == 0 || (src && dst), "null pair arrays");
+        need(max_hops >= 1, "max_hops must be >= 1");
+        CUDA_TRY(cudaSetDevice(g->device));
+        std::vector<uint32_t> dist(n_pairs);
+        graph_sample_hops(g, n_pairs, src, dst, max_hops, dist.data());
+        // exact integer moments, then one division each (order independent; R30)
+        uint64_t n = 0, s1 = 0;
+        unsigned __int128 s2 = 0;
+        for (uint32_t i = 0; i < n_pairs; i++) {
+            if (dist[i] == 0xFFFFFFFFu) continue;
+            n++;
+            s1 += dist[i];
+            s2 += (unsigned __int128)dist[i] * dist[i];
+        }
+        if (mean) *mean = n ? (double)s1 / (double)n : NAN;
+        if (stddev) {
+            if (n >= 2) {
+                const unsigned __int128 num = (unsigned __int128)n * s2 - (unsigned __int128)s1 * s1;
+                *stddev = sqrt((double)num / ((double)n * (double)(n - 1)));
+            } else {
+                *stddev = NAN;
+            }
+        }
+        if (n_reached) *n_reached = n;
+        if (dist_out && n_pairs) memcpy(dist_out, dist.data(), (size_t)n_pairs * 4);
     });
 }
 

@@ -146,6 +146,10 @@ void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uin
                            uint8_t *H_out, uint8_t *block_out, uint64_t *relax_out, int32_t *L_out);
 void engine_free(riki_graph *g);
 
+// hops.cu
+void graph_sample_hops(riki_graph *g, uint32_t n_pairs, const uint32_t *src, const uint32_t *dst, uint32_t max_hops,
+                       uint32_t *dist_out);
+
 // dist.cu
 void dist_unique_id(void *out128);
 void dist_init(riki_graph *g, int nranks, int rank, const void *uid, int mode);

@@ -115,6 +115,7 @@ def load():
         "riki_set_batch_slots": (i32, [P, u32]),
         "riki_memory_footprint": (i32, [P, P, P]),
         "riki_set_arena_limit": (i32, [P, u64]),
+        "riki_sample_avg_hops": (i32, [P, u32, P, P, u32, P, P, P, P]),
         "riki_dist_unique_id": (i32, [P]),
         "riki_dist_init": (i32, [P, i32, i32, P, i32]),
         "riki_dist_partition": (i32, [P, u32, u32, P]),
@@ -412,6 +413,17 @@ class Graph:
     def set_joint(self, on=True):
         """Joint multi-query traversal for large batches (identical results)."""
         _check(self.lib.riki_set_joint(self.h, int(on)))
+
+    def sample_avg_hops(self, src, dst, max_hops=255):
+        """Abar from sampled pairs (riki_sample_avg_hops): (mean, sample std, n_reached, dist[])."""
+        s_ = np.ascontiguousarray(src, np.uint32)
+        t_ = np.ascontiguousarray(dst, np.uint32)
+        assert len(s_) == len(t_)
+        dist = np.zeros(len(s_), np.uint32)
+        m, sd, n = C.c_double(), C.c_double(), C.c_uint64()
+        _check(self.lib.riki_sample_avg_hops(self.h, len(s_), _p(s_), _p(t_), int(max_hops), C.byref(m), C.byref(sd),
+                                             C.byref(n), _p(dist)))
+        return m.value, sd.value, n.value, dist
 
     def set_arena_limit(self, words):
         _check(self.lib.riki_set_arena_limit(self.h, int(words)))
