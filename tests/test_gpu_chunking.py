@@ -139,3 +139,44 @@ def test_bench_two_ranks_replicated_gloo(P):
     assert len(lines) == 1
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0 and d["gpu_launches"] > 0
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_modes_combined_against_oracle(P, seed, monkeypatch):
+    # every search mode combined with every execution variant (plain launches / whole-run graph /
+    # 64-bit item loop / simulated vertex partitions) gives the oracle's results
+    import oracle as O
+    from fixtures import random_instance
+    rng = np.random.default_rng(13000 + seed)
+    V, src, dst, _, _ = random_instance(rng, 20, 150, deg=2.8)
+    wf = rng.integers(0, 9, len(src)) / 8.0
+    nterm = 8
+    post = [np.unique(rng.integers(0, V, int(rng.integers(1, 5)))).astype(np.uint32) for _ in range(nterm)]
+    tp = np.zeros(nterm + 1, np.uint64)
+    tp[1:] = np.cumsum([len(x) for x in post])
+    g = P.Graph(V, src, dst, None, tp, np.concatenate(post))
+    g.set_edge_weights(wf, 0.5, float(rng.choice([1.0, 2.0, 3.5])))
+    og = O.Graph(V, src, dst, g.activation_levels())
+    variant = seed % 4
+    if variant == 0:
+        monkeypatch.setenv("RIKI_NO_GRAPHS", "1")
+    elif variant == 2:
+        monkeypatch.setenv("RIKI_FORCE_WIDE", "1")
+    elif variant == 3:
+        g.dist_init(int(rng.choice([2, 3, 5])), 0, None, mode=1)
+    cs, ms, kws, refs = [], [], [], []
+    k = int(rng.choice([1, 3, 5]))
+    D = int(rng.choice([3, 8, 20]))
+    kw = dict(ptc_mode=int(rng.integers(0, 4)), early_term=int(rng.integers(0, 3)), beam_mode=int(rng.integers(0, 2)),
+              tie_break=int(rng.integers(0, 2)))
+    for _ in range(6):
+        nc = int(rng.integers(1, 4))
+        nm = int(rng.integers(0, 4))
+        tt = rng.choice(nterm, nc + nm, replace=False)
+        cs.append([int(x) for x in tt[:nc]])
+        ms.append([int(x) for x in tt[nc:]])
+        refs.append(O.search(og, [post[t] for t in cs[-1]], [post[t] for t in ms[-1]], k, D, wfine=wf, **kw))
+    res = g.search_batch(cs, ms, k, D, **kw)
+    for r, ro in zip(res, refs):
+        assert [(x.central_node, x.sc, x.sm, x.score, x.ptc, x.edge_ids.tolist()) for x in r.rpgs] == \
+               [(x.central_node, x.sc, x.sm, x.score, x.ptc, x.edge_ids.tolist()) for x in ro.rpgs]
