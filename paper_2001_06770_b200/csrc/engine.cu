@@ -42,6 +42,7 @@ constexpr uint32_t HEAVY = EXP_HEAVY;  // longer active ranges are split into CH
 constexpr uint32_t CHUNK = EXP_HEAVY;
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
 constexpr uint32_t SORT_SMEM = 8192;  // u32 keys sorted in shared memory
+constexpr uint32_t U128_SORT_KEYS = 4096;  // u128 result keys sorted in shared memory (64 KB; larger sets in global)
 
 enum Ctr { C_NHEAVY = 0, C_NNEWATT, C_NOVF, C_ACTIVE, C_TOTAL, C_NCAND_TOTAL, C_NOVF2, C_NPULL, C_JQN0, C_JQN1,
            C_JQCUR, C_JHEAVY, C_LEVEL, C_NCTR = 16 };
@@ -1977,7 +1978,7 @@ __global__ void k_decide_m(WsDev w, uint32_t l_arg) {
     if (threadIdx.x == 0) first = EMPTY;
     __syncthreads();
     uint32_t nR = min(st.nR, w.capc);
-    if (nR != st.nR_sorted) cta_sort_u128(w.RK(s), nR, sm128, 1024);  // only when new RPGs arrived
+    if (nR != st.nR_sorted) cta_sort_u128(w.RK(s), nR, sm128, U128_SORT_KEYS);  // only when new RPGs arrived
     // attachment is monotone, so the first unattached candidate only moves forward
     const uint32_t c_begin = st.first_unatt, c_end = st.n_extract;
     for (uint32_t c0 = c_begin; c0 < c_end; c0 += blockDim.x) {
@@ -2040,7 +2041,7 @@ __global__ void k_final_select(WsDev w) {
         return;
     }
     uint32_t nR = min(st.nR, w.capc);
-    cta_sort_u128(w.RK(s), nR, sm128, 1024);
+    cta_sort_u128(w.RK(s), nR, sm128, U128_SORT_KEYS);
     uint32_t n = min(st.k, nR);
     if (st.tie_break) {  // R29: the order of [0, end of the k-th key's (S^r, S^c) group) needs W
         if (threadIdx.x == 0) {
@@ -2127,10 +2128,10 @@ __global__ void k_beam_tie(WsDev w) {
         for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
             K[i] = (u128)CD[i].sc << 96 | (u128)CD[i].wsum << 32 | i;
         __syncthreads();
-        cta_sort_u128(K, n, sm128, 1024);
+        cta_sort_u128(K, n, sm128, U128_SORT_KEYS);
         for (uint32_t i = threadIdx.x; i < keep; i += blockDim.x) K[i] = (uint32_t)K[i];
         __syncthreads();
-        cta_sort_u128(K, keep, sm128, 1024);  // kept indices ascending = (S^c, v) order
+        cta_sort_u128(K, keep, sm128, U128_SORT_KEYS);  // kept indices ascending = (S^c, v) order
         // compaction in place: source index K[j] >= j; chunk reads happen before chunk writes
         for (uint32_t j0 = 0; j0 < keep; j0 += blockDim.x) {
             const uint32_t j = j0 + threadIdx.x;
@@ -2171,7 +2172,7 @@ __global__ void k_tie_select(WsDev w) {
         K[i] = (u128)t.y << 96 | (u128)w.CD(s)[t.x].wsum << 32 | t.x;
     }
     __syncthreads();
-    cta_sort_u128(K, nt, sm128, 1024);
+    cta_sort_u128(K, nt, sm128, U128_SORT_KEYS);
     for (uint32_t i = threadIdx.x; i < st.nres; i += blockDim.x) w.resid[(size_t)s * w.kmax + i] = (uint32_t)K[i];
 }
 
@@ -2451,10 +2452,10 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
         SET_EX_ATTR(k_extract_cg)
         SET_EX_ATTR(k_extract_rpg)
 #undef SET_EX_ATTR
-        CUDA_TRY(cudaFuncSetAttribute(k_decide_m, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
-        CUDA_TRY(cudaFuncSetAttribute(k_final_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
-        CUDA_TRY(cudaFuncSetAttribute(k_tie_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
-        CUDA_TRY(cudaFuncSetAttribute(k_beam_tie, cudaFuncAttributeMaxDynamicSharedMemorySize, 1024 * 16));
+        CUDA_TRY(cudaFuncSetAttribute(k_decide_m, cudaFuncAttributeMaxDynamicSharedMemorySize, U128_SORT_KEYS * 16));
+        CUDA_TRY(cudaFuncSetAttribute(k_final_select, cudaFuncAttributeMaxDynamicSharedMemorySize, U128_SORT_KEYS * 16));
+        CUDA_TRY(cudaFuncSetAttribute(k_tie_select, cudaFuncAttributeMaxDynamicSharedMemorySize, U128_SORT_KEYS * 16));
+        CUDA_TRY(cudaFuncSetAttribute(k_beam_tie, cudaFuncAttributeMaxDynamicSharedMemorySize, U128_SORT_KEYS * 16));
         CUDA_TRY(cudaFuncSetAttribute(k_tie_weights, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
         CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
         CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
@@ -2603,7 +2604,7 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
                 k_extract_rpg_big<RowT><<<ws->big_ctas, 256, 0, s>>>(gd, wd);
                 L.check(__LINE__);
             }
-            k_decide_m<<<wd.nslots, 256, 1024 * 16, s>>>(wd, l);
+            k_decide_m<<<wd.nslots, 256, U128_SORT_KEYS * 16, s>>>(wd, l);
             L.check(__LINE__);
         }
         k_plan<<<1, MAX_SLOTS, 0, s>>>(wd, ph, l, pull_min);
@@ -2825,7 +2826,7 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     if (ws->beam_tie) {  // beam_mode 1 + tie-break (R29): truncate the recovered beam by W(CG)
         k_tie_weights<<<dim3(64, wd.nslots), 256, SORT_SMEM * 4, s>>>(gd, wd, true);
         L.check(__LINE__);
-        k_beam_tie<<<wd.nslots, 256, 1024 * 16, s>>>(wd);
+        k_beam_tie<<<wd.nslots, 256, U128_SORT_KEYS * 16, s>>>(wd);
         L.check(__LINE__);
         k_scan_cands<<<1, MAX_SLOTS, 0, s>>>(wd);
         L.check(__LINE__);
@@ -2836,12 +2837,12 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     run_phase<RowM, RowC>(L, gd, ws, 1, -1, depth + 1, total_cands);
     L.mark(2);
     // ---- top-k and packing
-    k_final_select<<<wd.nslots, 256, 1024 * 16, s>>>(wd);
+    k_final_select<<<wd.nslots, 256, U128_SORT_KEYS * 16, s>>>(wd);
     L.check(__LINE__);
     if (ws->tie_break) {  // R29 weight-sum tie-break
         k_tie_weights<<<dim3(64, wd.nslots), 256, SORT_SMEM * 4, s>>>(gd, wd, false);
         L.check(__LINE__);
-        k_tie_select<<<wd.nslots, 256, 1024 * 16, s>>>(wd);
+        k_tie_select<<<wd.nslots, 256, U128_SORT_KEYS * 16, s>>>(wd);
         L.check(__LINE__);
     }
     k_final_lists<RowC><<<dim3(ws->kmax, wd.nslots), 256, SORT_SMEM * 4, s>>>(gd, wd);
