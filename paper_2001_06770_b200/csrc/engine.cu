@@ -58,6 +58,16 @@ enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_PULLNODES, P_PUL
 #ifndef EXP_STATS
 #define EXP_STATS 0
 #endif
+// cache policy of the expansion's streamed reads (CSR columns, queue entries): 0 = __ldg
+// (default), 1 = __ldcs (evict-first: keep L2 for the random H-row accesses)
+#ifndef EXP_STREAM_LD
+#define EXP_STREAM_LD 0
+#endif
+#if EXP_STREAM_LD
+#define STREAM_LD(p) __ldcs(p)
+#else
+#define STREAM_LD(p) __ldg(p)
+#endif
 #ifndef REC_STATS
 #define REC_STATS 0
 #endif
@@ -601,7 +611,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
         if (valid) {
             if (sB != sA) s = find_slot(s_offs + sA, sB - sA + 1, item) + sA;
             uint32_t info = s_info[s];
-            uint32_t ent = w.Q(s, cur)[(uint32_t)(item - s_offs[s])];
+            uint32_t ent = STREAM_LD(w.Q(s, cur) + (uint32_t)(item - s_offs[s]));
             f = ent & ~RETAINED;
             RowT Rf = R::load(Hb + (size_t)s * V + f);
             const uint4 d = __ldg(g.desc + f);  // issued with the row load (dropped if dup / blocked)
@@ -699,7 +709,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
                 ev[u] = idx < tot;
                 const OwnF<RowT> o = own[ev[u] ? ow : 0];
                 o_s[u] = o.s;
-                n[u] = ev[u] ? __ldg(g.col + (uint32_t)(o.delta + idx)) : 0;  // delta wraps: add in 32 bits
+                n[u] = ev[u] ? STREAM_LD(g.col + (uint32_t)(o.delta + idx)) : 0;  // delta wraps: add in 32 bits
                 mask[u] = o.nw | (idx >= o.thr ? o.od : (RowT)0);  // [eqlo, hi) are the edges with a == l
             }
 #pragma unroll
@@ -771,7 +781,7 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
 #pragma unroll
             for (int u = 0; u < 2; u++) {
                 uint32_t e = e0 + 32 * u + lane;
-                n[u] = e < h.w ? __ldg(g.col + e) : 0;
+                n[u] = e < h.w ? STREAM_LD(g.col + e) : 0;
                 a[u] = e < h.w ? __ldg(g.act + e) : 0xFF;
             }
 #pragma unroll
