@@ -212,7 +212,7 @@ def main():
 
     import paper_2001_06770_b200 as P
     import synth
-    from paper_2001_06770_b200.dist import max_over_ranks
+    from paper_2001_06770_b200.dist import gather_results, max_over_ranks
 
     rank, world, dist = _dist()
     dev = torch.cuda.current_device()
@@ -298,6 +298,8 @@ def main():
         torch.cuda.synchronize()
         e2e_ev[i][0].record()
         rr = g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)
+        if dist and not args.vp:  # replicated mode: every shard's results gathered to rank 0
+            gather_results(rr, device=rdev)
         e2e_ev[i][1].record()
         d2h = sum(4 * (len(x.nodes) + len(x.vc)) + 4 * len(x.edge_ids) + 64 for r in rr for x in r.rpgs)
     torch.cuda.synchronize()
@@ -353,7 +355,8 @@ def main():
                      "kernel": "k_expand + k_expand_heavy (Alg. 1 expansion), CUDA events on the library stream",
                      "sections_ms_per_step": [x / args.steps for x in st["section_ms"]], "levels_per_step": st["levels"] / args.steps,
                      "peak_source": peak_src, "expand_share_of_step": st["expand_ms"] / tot_ms if tot_ms else None},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "results_gathered_to_rank0": bool(dist) and not args.vp},
         "gpu_launches": int(st["kernel_launches"]),
         "latency_ms": {"p50": lat[len(lat) // 2] if lat else None,
                        "p99": lat[min(len(lat) - 1, int(0.99 * len(lat)))] if lat else None, "n": len(lat)},

@@ -7,6 +7,7 @@ sets, plus the max-over-ranks timing reduction of the benchmark.  No collective 
 data path.  Everything here is host logic, covered by world_size-2 gloo tests on CPU."""
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -29,6 +30,59 @@ def search_sharded(search_fn, centrals, marginals, k, depth, group=None, **kw):
     parts = [None] * world
     dist.all_gather_object(parts, local, group=group)
     return [r for p in parts for r in p]
+
+
+_FIELDS = ("cnt", "hdr", "score", "nodes", "edges", "vc", "cd", "md", "stats")
+
+
+def pack_batch(br) -> np.ndarray:
+    """A BatchResult's columnar arrays as one byte buffer: a u64 header (n, then per field the
+    byte length) followed by the raw arrays (query term counts travel in the stats)."""
+    arrs = [np.ascontiguousarray(getattr(br, f)) for f in _FIELDS]
+    hdr = np.array([br.n, len(br.ncs)] + list(br.ncs) + list(br.nms) + [a.nbytes for a in arrs], np.uint64)
+    return np.concatenate([hdr.view(np.uint8)] + [a.reshape(-1).view(np.uint8) for a in arrs])
+
+
+def unpack_batch(buf: np.ndarray, like):
+    """Inverse of pack_batch; `like` supplies dtypes / trailing shapes (any BatchResult)."""
+    from .riki import BatchResult
+    buf = np.ascontiguousarray(buf, np.uint8)
+    n, m = (int(x) for x in buf[:16].view(np.uint64))
+    ncs = [int(x) for x in buf[16:16 + 8 * m].view(np.uint64)]
+    nms = [int(x) for x in buf[16 + 8 * m:16 + 16 * m].view(np.uint64)]
+    o = 16 + 16 * m
+    lens = [int(x) for x in buf[o:o + 8 * len(_FIELDS)].view(np.uint64)]
+    o += 8 * len(_FIELDS)
+    out = {}
+    for f, ln in zip(_FIELDS, lens):
+        ref = getattr(like, f)
+        a = buf[o:o + ln].view(ref.dtype)
+        out[f] = a.reshape((-1,) + ref.shape[1:]) if ref.ndim > 1 else a
+        o += ln
+    return BatchResult(n, ncs, nms, out["cnt"], out["hdr"], out["score"], out["nodes"], out["edges"], out["vc"],
+                       out["cd"], out["md"], out["stats"][:n])
+
+
+def gather_results(br, group=None, device=None):
+    """Gather every rank's BatchResult to rank 0 over the process group (the one
+    exchange of the replicated mode).  The packed buffers are padded to the largest and
+    all-gathered as one tensor on `device` (NCCL over NVLink on GPUs; gloo on CPU).  Returns
+    the list of per-rank BatchResults on rank 0 (rank order = query-shard order), None elsewhere."""
+    import torch
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    buf = pack_batch(br)
+    n = torch.tensor([buf.size], dtype=torch.int64, device=device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n, group=group)
+    mx = int(max(int(x.item()) for x in sizes))
+    t = torch.zeros(mx, dtype=torch.uint8, device=device)
+    t[:buf.size] = torch.from_numpy(buf).to(t.device)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t, group=group)
+    if rank != 0:
+        return None
+    return [unpack_batch(p[:int(sz.item())].cpu().numpy(), br) for p, sz in zip(parts, sizes)]
 
 
 def init_vertex_partitioned(graph, group=None, unique_id_fn=None):
