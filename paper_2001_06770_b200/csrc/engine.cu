@@ -753,7 +753,10 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
     }
 }
 
-// Heavy ranges (hub rows): one warp per CHUNK-edge piece, two edges per lane in flight.
+// Heavy ranges (hub rows): one warp per CHUNK-edge piece, HEAVY_UNROLL edges per lane in flight.
+#ifndef HEAVY_UNROLL
+#define HEAVY_UNROLL 2
+#endif
 template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l_arg) {
     const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
     typedef Row<RowT> R;
@@ -775,21 +778,23 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
         RowT Rf = R::load(Hs + h.y);  // values <= l are final; concurrent l+1 writes don't change the masks
         RowT newc = R::eq(Rf, L) & used, oldc = R::lt(Rf, L) & used;
         bool collect = st.collect;
-        for (uint32_t e0 = h.z; e0 < h.w; e0 += 64) {
-            uint32_t n[2], a[2];
-            RowT hn[2];
+        for (uint32_t e0 = h.z; e0 < h.w; e0 += 32 * HEAVY_UNROLL) {
+            uint32_t n[HEAVY_UNROLL], a[HEAVY_UNROLL];
+            RowT hn[HEAVY_UNROLL];
 #pragma unroll
-            for (int u = 0; u < 2; u++) {
+            for (int u = 0; u < HEAVY_UNROLL; u++) {
                 uint32_t e = e0 + 32 * u + lane;
                 n[u] = e < h.w ? STREAM_LD(g.col + e) : 0;
                 a[u] = e < h.w ? __ldg(g.act + e) : 0xFF;
             }
 #pragma unroll
-            for (int u = 0; u < 2; u++) hn[u] = (e0 + 32 * u + lane < h.w) ? R::load(Hs + n[u]) : (RowT)0;
-            bool enq[2], idn[2];
-            const uint32_t ss[2] = {s, s};
+            for (int u = 0; u < HEAVY_UNROLL; u++) hn[u] = (e0 + 32 * u + lane < h.w) ? R::load(Hs + n[u]) : (RowT)0;
+            bool enq[HEAVY_UNROLL], idn[HEAVY_UNROLL];
+            uint32_t ss[HEAVY_UNROLL];
 #pragma unroll
-            for (int u = 0; u < 2; u++) {
+            for (int u = 0; u < HEAVY_UNROLL; u++) ss[u] = s;
+#pragma unroll
+            for (int u = 0; u < HEAVY_UNROLL; u++) {
                 Relax<RowT> r{false, false, 0};
                 if (e0 + 32 * u + lane < h.w) {
                     RowT mask = newc | (a[u] == l ? oldc : (RowT)0);
@@ -799,9 +804,9 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
                 enq[u] = r.enq;
                 idn[u] = r.ident;
             }
-            frontier_push_n<2>(w, enq, ss, n, nxt);
+            frontier_push_n<HEAVY_UNROLL>(w, enq, ss, n, nxt);
 #pragma unroll
-            for (int u = 0; u < 2; u++) cand_push(g, w, idn[u] && collect, s, n[u], l + 1);
+            for (int u = 0; u < HEAVY_UNROLL; u++) cand_push(g, w, idn[u] && collect, s, n[u], l + 1);
         }
     }
     p_cells = warp_sum(p_cells);
