@@ -45,7 +45,7 @@ constexpr uint32_t SORT_SMEM = 8192;  // u32 keys sorted in shared memory
 constexpr uint32_t U128_SORT_KEYS = 4096;  // u128 result keys sorted in shared memory (64 KB; larger sets in global)
 
 enum Ctr { C_NHEAVY = 0, C_NNEWATT, C_NOVF, C_ACTIVE, C_TOTAL, C_NCAND_TOTAL, C_NOVF2, C_NPULL, C_JQN0, C_JQN1,
-           C_JQCUR, C_JHEAVY, C_LEVEL, C_NCTR = 16 };
+           C_JQCUR, C_JHEAVY, C_LEVEL, C_RECQ, C_NCTR = 16 };
 // level argument of the per-level kernels: a value, or LV_DEVICE = read the device level
 // counter ctr[C_LEVEL] (the whole-run CUDA graph with a device-side while loop)
 constexpr uint32_t LV_DEVICE = 0xFFFFFFFFu;
@@ -1274,6 +1274,7 @@ __global__ void k_scan_cands(WsDev w) {
     if (s == 0) {
         w.coffs[w.nslots] = sc[MAX_SLOTS - 1];
         w.ctr[C_NCAND_TOTAL] = sc[MAX_SLOTS - 1];
+        w.ctr[C_RECQ] = 0;
         w.ctr[C_NOVF] = 0;
         w.ctr[C_NOVF2] = 0;
     }
@@ -1506,6 +1507,23 @@ __device__ void bfs_column(const G &G_, const GraphDev &g, const WsDev &w, uint3
     }
 }
 
+// Tier-0 recovery work distribution: every warp starts on item `first` (< stride); with
+// REC_DYNAMIC the next items come from a shared counter (ctr[C_RECQ], zeroed before the
+// launch) in index order, so a warp stuck on a long predecessor-list build does not hold
+// back a fixed share of the items; otherwise the static cyclic stride.
+#ifndef REC_DYNAMIC
+#define REC_DYNAMIC 0
+#endif
+__device__ __forceinline__ uint32_t rec_next(const WsDev &w, uint32_t item, uint32_t stride) {
+#if REC_DYNAMIC
+    uint32_t nx = 0;
+    if (lane_id() == 0) nx = stride + atomicAdd(&w.ctr[C_RECQ], 1u);
+    return __shfl_sync(FULLMASK, nx, 0);
+#else
+    return item + stride;
+#endif
+}
+
 __device__ __forceinline__ uint32_t arena_alloc(const WsDev &w, uint32_t words, uint32_t s) {
     unsigned long long p = atomicAdd(w.arena_used, (unsigned long long)words);
     if (p + words > w.arena_cap) {
@@ -1671,7 +1689,7 @@ template <class RowC, int TIER> __global__ void __launch_bounds__(tier_threads<T
 #endif
         // cyclic distribution: concurrent warps share queries (their H arrays and memo lists stay
         // hot in L2), which measured faster than spreading warps over queries
-        for (uint32_t item = first; item < total; item += stride) {
+        for (uint32_t item = first; item < total; item = rec_next(w, item, stride)) {
             uint32_t s = find_slot(w.coffs, w.nslots, item), c = item - w.coffs[s];
             bool ovf = false;
 #if REC_STATS
@@ -1921,7 +1939,7 @@ template <class RowM, int TIER> __global__ void __launch_bounds__(tier_threads<T
         GroupWarp G_;
         if (first >= n) return;
         ex_init(G_, b, sh);
-        for (uint32_t i = first; i < n; i += stride) {
+        for (uint32_t i = first; i < n; i = rec_next(w, i, stride)) {
             uint2 sc = w.newatt[i];
             bool ovf = false;
             extract_rpg<GroupWarp, RowM>(G_, g, w, sc.x, sc.y, b, sh, &ovf);
@@ -1962,6 +1980,7 @@ template <class RowM> __global__ void __launch_bounds__(256) k_extract_rpg_big(G
 }
 
 __global__ void k_reset_level_ctrs(WsDev w) {
+    w.ctr[C_RECQ] = 0;
     w.ctr[C_NNEWATT] = 0;
     w.ctr[C_NOVF] = 0;
     w.ctr[C_NOVF2] = 0;
