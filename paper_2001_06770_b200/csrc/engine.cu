@@ -32,6 +32,14 @@ typedef unsigned __int128 u128;
 namespace {
 
 constexpr uint32_t MAX_SLOTS = 1024;
+// H layout of the per-slot ("slot-major") mode: slots are grouped by HGRP, and inside a group
+// the rows of one node are contiguous, so row (s, n) lives at
+//   H + ((s / HGRP) * V + n) * HGRP + s % HGRP        (in rows);
+// HGRP = 1 is plain slot-major.  Queries of a group that touch the same (hub) node share its
+// sector.
+#ifndef HGRP
+#define HGRP 1
+#endif
 #ifndef LEVEL_BATCH
 #define LEVEL_BATCH 4  // levels enqueued between host termination checks
 #endif
@@ -153,7 +161,7 @@ struct WsDev {
     uint32_t hnode, SP;  // H layout: 0 slot-major, 1 node-major with SP (padded) slots per node
     template <class RowT> __device__ __forceinline__ HV<RowT> Hs(int ph, uint32_t s) const {
         return hnode ? HV<RowT>{(RowT *)(H[ph] + (size_t)s * rb[ph]), SP}
-                     : HV<RowT>{(RowT *)(H[ph] + (size_t)s * V * rb[ph]), 1u};
+                     : HV<RowT>{(RowT *)(H[ph] + ((size_t)(s / HGRP) * V * HGRP + s % HGRP) * rb[ph]), (uint32_t)HGRP};
     }
     __device__ __forceinline__ uint64_t *CK(uint32_t s) const { return ck + (size_t)s * capc; }
     __device__ __forceinline__ Cand *CD(uint32_t s) const { return cd + (size_t)s * capc; }
@@ -593,7 +601,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const RowT L = R::splat(l);
-    RowT *const Hb = (RowT *)w.H[ph];  // slot-major: row (s, n) at Hb + s*V + n (never joint here)
+    RowT *const Hb = (RowT *)w.H[ph];  // per-slot layout (HGRP groups; never joint here)
     const size_t V = w.V;
     OwnF<RowT> *const own = s_own[threadIdx.x >> 5];
     uint32_t p_edges = 0, p_cells = 0;  // items and queue entries are counted by k_plan
@@ -613,7 +621,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
             uint32_t info = s_info[s];
             uint32_t ent = STREAM_LD(w.Q(s, cur) + (uint32_t)(item - s_offs[s]));
             f = ent & ~RETAINED;
-            RowT Rf = R::load(Hb + (size_t)s * V + f);
+            RowT Rf = R::load(Hb + ((size_t)(s / HGRP) * V + f) * HGRP + s % HGRP);
             const uint4 d = __ldg(g.desc + f);  // issued with the row load (dropped if dup / blocked)
             RowT used = used_mask<RowT>(info >> 8);
             bool dup = (ent & RETAINED) && (R::eq(Rf, L) & used);
@@ -713,13 +721,15 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
                 mask[u] = o.nw | (idx >= o.thr ? o.od : (RowT)0);  // [eqlo, hi) are the edges with a == l
             }
 #pragma unroll
-            for (int u = 0; u < EXP_UNROLL; u++) hn[u] = ev[u] ? R::load(Hb + (size_t)o_s[u] * V + n[u]) : (RowT)0;
+            for (int u = 0; u < EXP_UNROLL; u++)
+                hn[u] = ev[u] ? R::load(Hb + ((size_t)(o_s[u] / HGRP) * V + n[u]) * HGRP + o_s[u] % HGRP) : (RowT)0;
             bool enq[EXP_UNROLL], idn[EXP_UNROLL];
 #pragma unroll
             for (int u = 0; u < EXP_UNROLL; u++) {
                 Relax<RowT> r{false, false, 0};
                 if (ev[u]) {
-                    r = relax<RowT>(HV<RowT>{Hb + (size_t)o_s[u] * V, 1u}, n[u], hn[u], mask[u], l);
+                    r = relax<RowT>(HV<RowT>{Hb + (size_t)(o_s[u] / HGRP) * V * HGRP + o_s[u] % HGRP, (uint32_t)HGRP},
+                                    n[u], hn[u], mask[u], l);
                     p_cells += r.cells;
                 }
                 enq[u] = r.enq;
@@ -774,7 +784,7 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
         if (s >= w.nslots || h.y >= w.V || h.z > h.w || h.w > g.E) continue;
         const SlotState &st = w.st[s];
         RowT used = used_mask<RowT>(st.T[ph]);
-        RowT *const Hs = (RowT *)w.H[ph] + (size_t)s * w.V;  // slot-major (never joint here)
+        const HV<RowT> Hs = w.Hs<RowT>(ph, s);  // per-slot layout (never joint here)
         RowT Rf = R::load(Hs + h.y);  // values <= l are final; concurrent l+1 writes don't change the masks
         RowT newc = R::eq(Rf, L) & used, oldc = R::lt(Rf, L) & used;
         bool collect = st.collect;
@@ -798,7 +808,7 @@ template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_
                 Relax<RowT> r{false, false, 0};
                 if (e0 + 32 * u + lane < h.w) {
                     RowT mask = newc | (a[u] == l ? oldc : (RowT)0);
-                    r = relax<RowT>(HV<RowT>{Hs, 1u}, n[u], hn[u], mask, l);
+                    r = relax<RowT>(Hs, n[u], hn[u], mask, l);
                     p_cells += r.cells;
                 }
                 enq[u] = r.enq;
@@ -2439,7 +2449,8 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     const size_t S = c.slots;
     ws->hcap[0] = hb0;
     ws->hcap[1] = hb1;
-    const size_t S8 = (S + 7) & ~(size_t)7;  // node-major layout pads slots to a multiple of 8
+    const size_t SG = std::max<size_t>(8, HGRP);  // node-major / grouped layouts pad the slots
+    const size_t S8 = (S + SG - 1) / SG * SG;
     ws->H[0] = ws->alloc<uint8_t>(S8 * V * hb0);
     ws->H[1] = ws->alloc<uint8_t>(S8 * V * hb1);
     ws->qcap = c.qcap;
