@@ -358,6 +358,7 @@ riki_status riki_set_arena_limit(riki_graph *g, uint64_t words) {
         need(g, "null graph");
         need(words == 0 || words >= 4096, "arena limit must be 0 or >= 4096 words");
         g->arena_limit = words;
+        g->slots_cap = 0;
     });
 }
 
@@ -403,6 +404,7 @@ riki_status riki_set_batch_slots(riki_graph *g, uint32_t slots) {
         need(g, "null graph");
         need(slots <= 1024, "at most 1024 slots");
         g->batch_slots = slots;
+        g->slots_cap = 0;
     });
 }
 riki_status riki_memory_footprint(const riki_graph *g, uint64_t *gb, uint64_t *wb) {

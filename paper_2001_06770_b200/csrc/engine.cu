@@ -3079,6 +3079,7 @@ bool run_with_retry(riki_graph *g, Launch &L, uint32_t depth, Caps &caps, uint32
             if (caps.arena >= amax) {
                 if (n_active <= 1) RIKI_THROW(RIKI_ENOMEM, "recovery arena exceeds 2^32 words for one query");
                 caps.slots = std::max(1u, n_active / 2);
+                g->slots_cap = caps.slots;  // remembered: later batches start at this chunk size
                 return false;
             }
             caps.arena = std::min<uint64_t>(caps.arena * 4, amax);
@@ -3155,6 +3156,7 @@ static Caps initial_caps(riki_graph *g, uint32_t nq, uint32_t k, uint32_t rb0, u
     c.rb[0] = rb0;
     c.rb[1] = rb1;
     c.slots = auto_slots(g, nq, rb0, rb1, want_hint);
+    if (g->slots_cap) c.slots = std::min(c.slots, g->slots_cap);  // a batch this wide overflowed the arena
     c.capc = std::min<uint32_t>(16384, next_pow2(g->V + 1));
     c.kmax = std::max<uint32_t>(k, g->ws ? g->ws->kmax : 1);
     c.arena = std::max<uint64_t>(64ull << 20, g->ws ? g->ws->arena_cap : 0);

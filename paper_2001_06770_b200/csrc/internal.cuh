@@ -92,7 +92,8 @@ struct riki_graph {
     riki_stats stats{};
     DistState *dist = nullptr;  // set by riki_dist_init
     std::vector<riki_results *> dev_stash;
-    uint64_t arena_limit = 0;  // riki_set_arena_limit (tests): 0 = the 32-bit offset limit  // device batch run in chunks: results collected per chunk
+    uint64_t arena_limit = 0;  // riki_set_arena_limit (tests): 0 = the 32-bit offset limit
+    uint32_t slots_cap = 0;    // chunk size learnt from an arena-limited batch (0 = none)  // device batch run in chunks: results collected per chunk
     bool vp() const { return dist && dist->mode == 1; }
 
     GraphDev dev() const {
