@@ -89,11 +89,12 @@ def brute_levels(V, src, dst, act, sources, max_edges=12):
     return np.array(best, np.int64)
 
 
-def o2_levels(V, src, dst, act, terms, depth, blocking):
+def o2_levels(V, src, dst, act, terms, depth, blocking, events=None):
     """Event-driven evaluator.  At level L every settled (f, j) with key
     max(h_fj, a_e) == L relaxes e unless f is blocked at L; f is blocked at L iff
     blocking and its row is complete with max <= L (R10 closed form).
-    Returns H (V x T, INF = 255) and L_stop (first level with no live work)."""
+    Returns H (V x T, INF = 255).  ``events`` (a list of >= depth zeros), when given,
+    receives the number of relaxation events processed in each bucket L."""
     T = len(terms)
     H = np.full((V, T), INF, np.int64)
     for j, t in enumerate(terms):
@@ -117,12 +118,59 @@ def o2_levels(V, src, dst, act, terms, depth, blocking):
                 for e in out[f]:
                     if max(h, act[e]) != L:
                         continue
+                    if events is not None:
+                        events[L] += 1
                     n = int(dst[e])
                     if H[n, j] == INF:
                         updates.append((n, j))
         for n, j in updates:
             H[n, j] = L + 1
     return H
+
+
+def o2_phase(V, src, dst, act, terms, depth, blocking):
+    """O2 extended with the two quantities the oracle's phase also reports, each derived from
+    the paper's definitions by its own route (no frontier array, no re-scans):
+
+    * L_end -- the first level l with an empty frontier, or ``depth``.  Alg. 1 keeps F_f = 1
+      while f is unblocked and some out-edge has a_fn > l (lines 9-11), and sets
+      F_n = 1 when n is first reached (line 17), so by induction f is in the frontier Phi_l
+      (l >= 1) iff some column of f was reached at exactly l, or (f was reached before l,
+      max_e a_e >= l and f was not blocked at l - 1).  Seeds form Phi_0.
+    * R -- SURVEY §8(d)'s relaxation count, as the number of events the bucket queue
+      processes in buckets L < L_end: (f, j, e) with key max(h_fj, a_e) = L and f not blocked
+      at L (R10 closed form, tested while H holds only the final values <= L), counted whether
+      or not the event reaches a new cell.
+
+    Returns (H, L_end, R)."""
+    events = [0] * max(depth, 1)
+    H = o2_levels(V, src, dst, act, terms, depth, blocking, events)
+    T = len(terms)
+    out, _ = _adj(V, np.asarray(src), np.asarray(dst))
+    act = np.asarray(act, np.int64)
+    fin = H != INF
+    comp = fin.all(axis=1)
+    blk = np.where(comp, H.max(axis=1), INF) if blocking and T > 0 else np.full(V, INF)
+    h0 = np.where(fin.any(axis=1), np.where(fin, H, INF).min(axis=1), INF)
+    amax = np.array([max((int(act[e]) for e in out[f]), default=-1) for f in range(V)])
+
+    def frontier_nonempty(l):
+        if l == 0:
+            return bool((h0 == 0).any())
+        for f in range(V):
+            if (H[f] == l).any():
+                return True
+            if h0[f] != INF and h0[f] <= l - 1 and amax[f] >= l and blk[f] > l - 1:
+                return True
+        return False
+
+    L_end = depth
+    for l in range(depth + 1):
+        if not frontier_nonempty(l):
+            L_end = l
+            break
+    R = sum(events[:L_end])
+    return H, L_end, R
 
 
 def enumerate_min_paths(V, src, dst, act, H, j, blockarr, targets, max_edges=14):

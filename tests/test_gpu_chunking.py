@@ -155,8 +155,9 @@ def test_modes_combined_against_oracle(P, seed, monkeypatch):
     tp = np.zeros(nterm + 1, np.uint64)
     tp[1:] = np.cumsum([len(x) for x in post])
     g = P.Graph(V, src, dst, None, tp, np.concatenate(post))
-    g.set_edge_weights(wf, 0.5, float(rng.choice([1.0, 2.0, 3.5])))
-    og = O.Graph(V, src, dst, g.activation_levels())
+    A = float(rng.choice([1.0, 2.0, 3.5]))
+    g.set_edge_weights(wf, 0.5, A)
+    og = O.Graph(V, src, dst, O.coarsen_all(wf, 0.5, A))  # oracle-computed activations (Eq. 1-3)
     variant = seed % 4
     if variant == 0:
         monkeypatch.setenv("RIKI_NO_GRAPHS", "1")

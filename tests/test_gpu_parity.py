@@ -156,7 +156,7 @@ def test_hitting_levels_c1_all_terms(P):
     kg = synth.make_kg(1)
     g = P.Graph(kg.n_nodes, kg.src, kg.dst, kg.label_class, kg.term_ptr, kg.postings)
     g.set_label_weights(0.5, kg.avg_hops)
-    og = O.Graph(kg.n_nodes, kg.src, kg.dst, g.activation_levels())
+    og = O.Graph(kg.n_nodes, kg.src, kg.dst, _oracle_act(kg))
     for t0 in range(0, kg.n_terms - 4, 4):
         terms = np.arange(t0, t0 + 4, dtype=np.uint32)
         for mode in (0, 1, 2):
@@ -183,6 +183,36 @@ def test_golden_fixtures(P, name):
         assert sorted((int(s[e]), int(t[e])) for e in got.edge_ids) == sorted(tuple(x) for x in exp["directed_edges"])
     if "expect_ptc_fail" in d:
         assert r.stats["n_ptc_fail"] == d["expect_ptc_fail"]
+
+
+@pytest.mark.parametrize("name", ["ptc_gm_only_r20i.json", "ptc_single_marginal_node.json",
+                                  "early_term_literal_gamma1.json"])
+def test_golden_mode_fixtures(P, name):
+    # the hand-derived option fixtures (ptc_mode 2, R19', early_term 1 at gamma = 1) through the C-ABI
+    d = load_golden(name)
+    s, t, a = undirected_to_directed(d["undirected_edges"])
+    terms = d["central"] + d["marginal"]
+    g = _dev_graph(P, d["nodes"], s, t, a, terms)
+    nc = len(d["central"])
+    for run in d["runs"]:
+        r = g.search(np.arange(nc), np.arange(nc, len(terms)), d["k"], d["depth"], gamma=d["gamma"], **run["params"])
+        assert len(r.rpgs) == len(run["expect"]), run["params"]
+        for got, exp in zip(r.rpgs, run["expect"]):
+            assert (got.central_node, got.sc, got.sm, got.score, int(got.ptc)) == \
+                   (exp["central_node"], exp["sc"], exp["sm"], exp["score"], exp["ptc"])
+            assert got.nodes.tolist() == exp["nodes"]
+            assert sorted((int(s[e]), int(t[e])) for e in got.edge_ids) == \
+                   sorted(tuple(x) for x in exp["directed_edges"])
+        if "expect_ptc_fail" in run:
+            assert r.stats["n_ptc_fail"] == run["expect_ptc_fail"]
+        if "expect_L_marginal" in run:
+            assert r.stats["L_marginal"] == run["expect_L_marginal"]
+
+
+def _oracle_act(kg, alpha=0.5):
+    """Activation levels computed by the ORACLE from the label-class fine weights:
+    the oracle never takes an input produced by the CUDA path."""
+    return O.coarsen_all(O.fine_weights(kg.n_nodes, kg.src, kg.dst, kg.label_class), alpha, kg.avg_hops)
 
 
 def _oracle_run(og, kg_post, C, M, k, D, **kw):
@@ -222,7 +252,7 @@ def test_search_batch_c1_all_queries(P):
     g = P.Graph(kg.n_nodes, kg.src, kg.dst, kg.label_class, kg.term_ptr, kg.postings)
     g.set_label_weights(0.5, kg.avg_hops)
     g.set_debug(True)
-    og = O.Graph(kg.n_nodes, kg.src, kg.dst, g.activation_levels())
+    og = O.Graph(kg.n_nodes, kg.src, kg.dst, _oracle_act(kg))
     res = g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)
     n_nonempty = 0
     for i, r in enumerate(res):
@@ -414,7 +444,7 @@ def test_joint_traversal_c1_batch(P):
     qs = synth.config_queries(kg, 1)
     g = P.Graph(kg.n_nodes, kg.src, kg.dst, kg.label_class, kg.term_ptr, kg.postings)
     g.set_label_weights(0.5, kg.avg_hops)
-    og = O.Graph(kg.n_nodes, kg.src, kg.dst, g.activation_levels())
+    og = O.Graph(kg.n_nodes, kg.src, kg.dst, _oracle_act(kg))
     g.set_joint(True)
     res = g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)
     for i, r in enumerate(res):
@@ -468,7 +498,7 @@ def test_joint_traversal_c2_sampled(P):
     for i in range(len(res)):
         _cmp_results(res[i], ref[i])
         assert res[i].stats == ref[i].stats
-    og = O.Graph(kg.n_nodes, kg.src, kg.dst, g.activation_levels())
+    og = O.Graph(kg.n_nodes, kg.src, kg.dst, _oracle_act(kg))
     for i in (0, 99, 199):
         _cmp_results(res[i], _oracle_run(og, kg.posting, qs.central[i], qs.marginal[i], qs.k, qs.depth,
                                          want_matrices=False))

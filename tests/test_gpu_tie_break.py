@@ -60,8 +60,9 @@ def test_tie_break_random(P, seed):
     wf = rng.integers(0, 9, len(src)) / 8.0  # coarse grid: ties on W happen too
     nterm = 8
     post = [np.unique(rng.integers(0, V, int(rng.integers(1, 5)))).astype(np.uint32) for _ in range(nterm)]
-    g = _graph(P, V, src, dst, post, wf, 0.5, float(rng.choice([0.6, 1.5, 3.0])))
-    og = O.Graph(V, src, dst, g.activation_levels())
+    A = float(rng.choice([0.6, 1.5, 3.0]))
+    g = _graph(P, V, src, dst, post, wf, 0.5, A)
+    og = O.Graph(V, src, dst, O.coarsen_all(wf, 0.5, A))  # oracle-computed activations (Eq. 1-3)
     for _ in range(4):
         nc = int(rng.integers(1, 4))
         nm = int(rng.integers(0, 4))
@@ -82,7 +83,7 @@ def test_tie_break_batch_and_node_weights(P):
     g = P.Graph(kg.n_nodes, kg.src, kg.dst, kg.label_class, kg.term_ptr, kg.postings)
     g.set_label_weights(0.5, kg.avg_hops)
     wf = O.fine_weights(kg.n_nodes, kg.src, kg.dst, kg.label_class)
-    og = O.Graph(kg.n_nodes, kg.src, kg.dst, g.activation_levels())
+    og = O.Graph(kg.n_nodes, kg.src, kg.dst, O.coarsen_all(wf, 0.5, kg.avg_hops))
     res = g.search_batch(qs.central, qs.marginal, qs.k, qs.depth, tie_break=1)
     for i, r in enumerate(res):
         ro = O.search(og, [kg.posting(t) for t in qs.central[i]], [kg.posting(t) for t in qs.marginal[i]], qs.k,
@@ -92,7 +93,7 @@ def test_tie_break_batch_and_node_weights(P):
     rng = np.random.default_rng(5)
     wn = rng.integers(0, 5, kg.n_nodes) / 4.0
     g.set_node_weights(wn, 0.5, kg.avg_hops)
-    og = O.Graph(kg.n_nodes, kg.src, kg.dst, g.activation_levels())
+    og = O.Graph(kg.n_nodes, kg.src, kg.dst, O.coarsen_all(wn[kg.dst], 0.5, kg.avg_hops))
     we = wn[kg.dst]
     for i in range(0, len(qs.central), 7):
         r = g.search(qs.central[i], qs.marginal[i], qs.k, qs.depth, tie_break=1)

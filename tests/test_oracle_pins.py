@@ -185,6 +185,51 @@ def test_levels_match_event_driven_with_blocking(seed):
         assert (blk.astype(np.int64) == ref.astype(np.int64)).all()
 
 
+@pytest.mark.parametrize("seed", range(60))
+def test_phase_relaxations_and_end_level_match_event_counts(seed):
+    # SURVEY §8(d) relaxation count R (the GTEPS numerator) and the terminating level of a raw
+    # run, pinned by O2's event count per bucket and an independent frontier-emptiness rule
+    # (tests/brute.py::o2_phase); a mistake such as counting L <= L_end, ignoring blocking or
+    # stopping one level late fails here
+    rng = np.random.default_rng(900 + seed)
+    V, src, dst, act, terms = random_instance(rng, 5, 40, T_hi=4)
+    D = int(rng.choice([3, 5, 8, 20]))
+    g = O.Graph(V, src, dst, act)
+    for mode in (0, 1, 2):
+        H, blk, L, rel = O.phase(g, terms, D, mode)
+        blocking = mode == 1 or (mode == 2 and len(terms) >= 2)
+        H2, L2, R2 = brute.o2_phase(V, src, dst, act, terms, D, blocking)
+        assert (H.astype(np.int64) == H2).all()
+        assert L == L2, (mode, L, L2)
+        assert rel == R2, (mode, rel, R2)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_search_relaxations_match_event_counts(seed):
+    # the search's per-run relaxation counts (bench GTEPS numerator) against O2's events below
+    # each run's terminating level; the central terminating level itself against its definition
+    # ("at least w CGs", R8 depth, empty frontier)
+    rng = np.random.default_rng(2000 + seed)
+    V, src, dst, act, _ = random_instance(rng, 6, 18, deg=2.2, amax=4)
+    nc, nm = int(rng.integers(1, 4)), int(rng.integers(1, 4))
+    terms = [np.unique(rng.integers(0, V, int(rng.integers(1, 4)))).astype(np.uint32) for _ in range(nc + nm)]
+    C, M = terms[:nc], terms[nc:]
+    k = int(rng.choice([1, 3, 5]))
+    D = int(rng.choice([3, 6, 20]))
+    r = O.search(O.Graph(V, src, dst, act), C, M, k, D)
+    ev = [0] * D
+    Hc = brute.o2_levels(V, src, dst, act, C, D, True, ev)
+    _, Lend, _ = brute.o2_phase(V, src, dst, act, C, D, True)
+    mx = np.where((Hc != INF).all(axis=1), Hc.max(axis=1), INF)
+    Lw = next((L for L in range(D + 1) if (mx <= L).sum() >= k), D)
+    assert r.Lc == min(Lw, Lend)
+    assert r.relax_c == sum(ev[:r.Lc])
+    if r.Lm >= 0:
+        evm = [0] * D
+        brute.o2_levels(V, src, dst, act, M, D, nm >= 2, evm)
+        assert r.relax_m == sum(evm[:r.Lm])
+
+
 @pytest.mark.parametrize("seed", range(20))
 def test_levels_depth_truncation_and_permutation(seed):
     rng = np.random.default_rng(1300 + seed)
@@ -238,6 +283,54 @@ def test_golden_end_to_end(name):
         assert de == sorted(tuple(x) for x in exp["directed_edges"])
     if "expect_ptc_fail" in d:
         assert r.n_ptc_fail == d["expect_ptc_fail"]
+
+
+def _check_rpgs(rpgs, expect, s, t):
+    assert len(rpgs) == len(expect), (len(rpgs), len(expect))
+    for got, exp in zip(rpgs, expect):
+        assert (got.central_node, got.sc, got.sm, got.score) == (exp["central_node"], exp["sc"], exp["sm"],
+                                                                 exp["score"])
+        assert int(got.ptc) == exp["ptc"]
+        assert got.nodes.tolist() == exp["nodes"]
+        assert sorted((int(s[e]), int(t[e])) for e in got.edge_ids) == sorted(tuple(x) for x in exp["directed_edges"])
+
+
+@pytest.mark.parametrize("name", ["ptc_gm_only_r20i.json", "ptc_single_marginal_node.json",
+                                  "early_term_literal_gamma1.json"])
+def test_golden_mode_fixtures(name):
+    # hand-derived fixtures for the option paths: ptc_mode 2 (G^m-only PTC, R20 case (i)),
+    # R19' ("at least two different marginal keyword nodes") and the paper-literal early
+    # termination (early_term 1) where it differs from the exact bound R21
+    d = load_golden(name)
+    s, t, a = undirected_to_directed(d["undirected_edges"])
+    g = O.Graph(d["nodes"], s, t, a)
+    C = [np.array(x, np.uint32) for x in d["central"]]
+    M = [np.array(x, np.uint32) for x in d["marginal"]]
+    for run in d["runs"]:
+        r = O.search(g, C, M, d["k"], d["depth"], gamma=d["gamma"], **run["params"])
+        _check_rpgs(r.rpgs, run["expect"], s, t)
+        if "expect_ptc_fail" in run:
+            assert r.n_ptc_fail == run["expect_ptc_fail"], run["params"]
+        if "expect_L_marginal" in run:
+            assert r.Lm == run["expect_L_marginal"], run["params"]
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_literal_early_termination_exact_below_gamma_one(seed):
+    # early_term 1 (P:375-381 literal) for 0 <= gamma < 1: S^r(kth) <= g*min S^c + (1-g)*S^m(kth)
+    # reduces to S^c(kth) <= min S^c(unattached), and every unattached CG has S^m >= l+1 > S^m(kth),
+    # so it never changes the answer: it must equal the plain-definition (exhaustive) form
+    rng = np.random.default_rng(7700 + seed)
+    V, src, dst, act, _ = random_instance(rng, 8, 20, deg=2.5, amax=3)
+    nc, nm = int(rng.integers(1, 3)), int(rng.integers(1, 4))
+    terms = [np.unique(rng.integers(0, V, int(rng.integers(1, 3)))).astype(np.uint32) for _ in range(nc + nm)]
+    C, M = terms[:nc], terms[nc:]
+    k = int(rng.choice([1, 3, 5]))
+    gamma = float(rng.choice([0.0, 0.25, 0.5, 0.9]))
+    r = O.search(O.Graph(V, src, dst, act), C, M, k, 20, gamma=gamma, early_term=1)
+    ref, _ = brute.search_plain(V, src, dst, act, C, M, k, 20, gamma=gamma)
+    assert [(x.score, x.sc, x.central_node, x.sm, x.nodes.tolist(), sorted(int(e) for e in x.edge_ids))
+            for x in r.rpgs] == [(x[0], x[1], x[2], x[3], x[4], x[5]) for x in ref]
 
 
 def test_ptc_modes_on_vc_marginal():

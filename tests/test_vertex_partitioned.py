@@ -209,7 +209,7 @@ def test_vp_c1_batch_simulated_and_nccl_one_rank(P):
     qs = synth.config_queries(kg, 1)
     g = P.Graph(kg.n_nodes, kg.src, kg.dst, kg.label_class, kg.term_ptr, kg.postings)
     g.set_label_weights(0.5, kg.avg_hops)
-    og = O.Graph(kg.n_nodes, kg.src, kg.dst, g.activation_levels())
+    og = O.Graph(kg.n_nodes, kg.src, kg.dst, O.coarsen_all(O.fine_weights(kg.n_nodes, kg.src, kg.dst, kg.label_class), 0.5, kg.avg_hops))
     base = g.search_batch(qs.central, qs.marginal, qs.k, qs.depth)
     for i in range(0, len(base), 9):
         ro = O.search(og, [kg.posting(t) for t in qs.central[i]], [kg.posting(t) for t in qs.marginal[i]], qs.k,
@@ -247,7 +247,7 @@ def test_vp_c2_sampled_queries(P):
         _cmp(a, b)
         assert a.stats["relax_central"] == b.stats["relax_central"]
         assert a.stats["relax_marginal"] == b.stats["relax_marginal"]
-    og = O.Graph(kg.n_nodes, kg.src, kg.dst, g.activation_levels())
+    og = O.Graph(kg.n_nodes, kg.src, kg.dst, O.coarsen_all(O.fine_weights(kg.n_nodes, kg.src, kg.dst, kg.label_class), 0.5, kg.avg_hops))
     for i in (0, 13):
         ro = O.search(og, [kg.posting(t) for t in qs.central[i]], [kg.posting(t) for t in qs.marginal[i]], qs.k,
                       qs.depth, want_matrices=False)
