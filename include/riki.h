@@ -14,6 +14,17 @@
  *   - There is no CPU fallback: every step of the search runs in CUDA kernels; without a
  *     usable sm_100 device the calls return RIKI_ECUDA.
  *   - Infinity for a hitting level is 0xFF; finite levels are <= depth <= 254 (R8).
+ *   - Threading: every call on a graph handle holds that handle's lock, so one handle
+ *     serves concurrent callers (threads) safely -- their searches run one after the other
+ *     on the handle's device workspace (the GPU is saturated by one lock-step batch; use one
+ *     handle per device and batch the queries).  Different handles are independent.
+ *     riki_set_*_weights may be called between searches; it too takes the lock.
+ *   - Result order (Def. RPKSP, Eq. 6): ascending (S^r, S^c, v) with v the
+ *     caller's central node id (R23).  This departs from SPEC.md's RankedResult order
+ *     (S^r, edge-weight sum, v) in two ways, both documented readings: S^c is the secondary
+ *     key (central focus first: of two RPGs with equal S^r the one whose CG is tighter wins,
+ *     e.g. S^c = 2 / S^m = 4 before S^c = 4 / S^m = 2 at gamma = 0.5), and the paper's
+ *     weight-sum re-ranking is opt-in (tie_break = 1: (S^r, S^c, W, v)).
  */
 #ifndef RIKI_H
 #define RIKI_H
@@ -92,6 +103,13 @@ riki_status riki_set_label_weights(riki_graph *g, double alpha, double avg_hops)
 riki_status riki_set_activation_levels(riki_graph *g, const uint8_t *a);
 riki_status riki_get_activation_levels(const riki_graph *g, uint8_t *a);
 
+/* Debug / verification boundary for the coarsening's only transcendental step (R2):
+ * out[i] = the device's ln(n0 + i) exactly as the fine-weight kernel computes ln(cA + cB),
+ * for i < count (host out[count]; n0 >= 1).  A test compares it bit for bit with the
+ * oracle's libm log over the whole integer domain label counts can take.  Errors:
+ * RIKI_EINVAL, RIKI_ECUDA. */
+riki_status riki_debug_ln_table(int device, uint64_t n0, uint64_t count, double *out);
+
 /* ---------------------------------------------------------------------------------------
  * Search parameters (defaults in brackets; riki_params_default fills them).
  *   gamma      Eq. 6 weight [0.5, R22]
@@ -106,7 +124,10 @@ riki_status riki_get_activation_levels(const riki_graph *g, uint8_t *a);
  *              1 = keep failures, flagged ptc = 0; 2 = filter, PTC evaluated on G^m only;
  *              3 = filter, SPEC's exclusive form (V_C-resident marginal nodes never qualify)
  *   early_term 0 = exact bound (R21) [0]; 1 = the paper's literal inequality (Theorem
- *              earlyTermination P:375-378; unsafe in general, R21); 2 = none (exhaustive)
+ *              earlyTermination P:375-378): it reduces to S^c(kth) <= min S^c(unattached) and
+ *              is exact for gamma < 1, but at gamma = 1 it can stop before an equal-score CG
+ *              with a smaller id attaches (tests/golden/early_term_literal_gamma1.json);
+ *              2 = none (exhaustive)
  * ------------------------------------------------------------------------------------- */
 typedef struct {
     double gamma;
@@ -127,7 +148,9 @@ void riki_params_default(riki_params *p);
  * blocking, termination at >= w CGs) -> candidate CGs -> Alg. 2 recovery of each CG ->
  * marginal run (fresh H, stop rule for |M| >= 2, attach, RPG recovery + PTC, exact early
  * termination) -> top-k by (S^r, S^c, v).  p == NULL uses defaults.  cuda_stream == NULL
- * uses the library's stream; otherwise a cudaStream_t on the graph's device.
+ * uses the library's stream; otherwise a cudaStream_t on the graph's device: every kernel
+ * launch and copy of the search is issued on that stream, after the caller's earlier work
+ * on it; the call returns once the results are on the host (the stream is synchronised).
  * *out receives a host result set (count may be 0: success with no result).
  * Errors: RIKI_EEMPTY_CENTRAL, RIKI_EUNRESOLVED, RIKI_ENOWEIGHTS, RIKI_EDEPTH, RIKI_EINVAL,
  *         RIKI_ENOMEM (workspace overflow, message says which), RIKI_ECUDA.

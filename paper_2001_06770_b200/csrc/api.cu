@@ -32,6 +32,10 @@ template <class F> riki_status guard(F &&f) {
     }
 }
 
+// Every call on a graph handle holds its lock (include/riki.h, Threading): concurrent
+// searches on one handle run one after the other on its workspace.
+#define HANDLE_LOCK(g) std::lock_guard<std::recursive_mutex> handle_lock_((g)->mu)
+
 void need(bool c, const char *msg) {
     if (!c) RIKI_THROW(RIKI_EINVAL, msg);
 }
@@ -121,19 +125,19 @@ void riki_free_graph(riki_graph *g) {
 }
 
 riki_status riki_set_edge_weights(riki_graph *g, const double *w01, double alpha, double avg_hops) {
-    return guard([&] { need(g, "null graph"); CUDA_TRY(cudaSetDevice(g->device)); graph_set_edge_weights(g, w01, alpha, avg_hops); });
+    return guard([&] { need(g, "null graph"); CUDA_TRY(cudaSetDevice(g->device)); HANDLE_LOCK(g); graph_set_edge_weights(g, w01, alpha, avg_hops); });
 }
 riki_status riki_set_node_weights(riki_graph *g, const double *w01, double alpha, double avg_hops) {
-    return guard([&] { need(g, "null graph"); CUDA_TRY(cudaSetDevice(g->device)); graph_set_node_weights(g, w01, alpha, avg_hops); });
+    return guard([&] { need(g, "null graph"); CUDA_TRY(cudaSetDevice(g->device)); HANDLE_LOCK(g); graph_set_node_weights(g, w01, alpha, avg_hops); });
 }
 riki_status riki_set_label_weights(riki_graph *g, double alpha, double avg_hops) {
-    return guard([&] { need(g, "null graph"); CUDA_TRY(cudaSetDevice(g->device)); graph_set_label_weights(g, alpha, avg_hops); });
+    return guard([&] { need(g, "null graph"); CUDA_TRY(cudaSetDevice(g->device)); HANDLE_LOCK(g); graph_set_label_weights(g, alpha, avg_hops); });
 }
 riki_status riki_set_activation_levels(riki_graph *g, const uint8_t *a) {
-    return guard([&] { need(g, "null graph"); CUDA_TRY(cudaSetDevice(g->device)); graph_set_act(g, a); });
+    return guard([&] { need(g, "null graph"); CUDA_TRY(cudaSetDevice(g->device)); HANDLE_LOCK(g); graph_set_act(g, a); });
 }
 riki_status riki_get_activation_levels(const riki_graph *g, uint8_t *a) {
-    return guard([&] { need(g && a, "null argument"); CUDA_TRY(cudaSetDevice(g->device)); graph_get_act(g, a); });
+    return guard([&] { need(g && a, "null argument"); CUDA_TRY(cudaSetDevice(g->device)); HANDLE_LOCK(g); graph_get_act(g, a); });
 }
 
 riki_status riki_rpq_search(riki_graph *g, const uint32_t *central, uint32_t n_central, const uint32_t *marginal,
@@ -142,7 +146,7 @@ riki_status riki_rpq_search(riki_graph *g, const uint32_t *central, uint32_t n_c
     return guard([&] {
         need(g && out, "null argument");
         *out = nullptr;
-        CUDA_TRY(cudaSetDevice(g->device));
+        CUDA_TRY(cudaSetDevice(g->device)); HANDLE_LOCK(g);
         riki_params prm;
         riki_params_default(&prm);
         if (p) prm = *p;
@@ -159,7 +163,7 @@ riki_status riki_rpq_search_batch(riki_graph *g, uint32_t n_queries, const uint6
     return guard([&] {
         need(g && out, "null argument");
         need(n_queries == 0 || (c_ptr && m_ptr), "null pointer arrays");
-        CUDA_TRY(cudaSetDevice(g->device));
+        CUDA_TRY(cudaSetDevice(g->device)); HANDLE_LOCK(g);
         riki_params prm;
         riki_params_default(&prm);
         if (p) prm = *p;
@@ -181,7 +185,7 @@ riki_status riki_rpq_search_batch_device(riki_graph *g, uint32_t n_queries, cons
     return guard([&] {
         need(g, "null graph");
         need(n_queries > 0 && d_c_ptr && d_m_ptr && d_c_terms, "null device arrays");
-        CUDA_TRY(cudaSetDevice(g->device));
+        CUDA_TRY(cudaSetDevice(g->device)); HANDLE_LOCK(g);
         riki_params prm;
         riki_params_default(&prm);
         if (p) prm = *p;
@@ -192,7 +196,7 @@ riki_status riki_rpq_search_batch_device(riki_graph *g, uint32_t n_queries, cons
 riki_status riki_batch_fetch(riki_graph *g, uint32_t n_queries, riki_results **out) {
     return guard([&] {
         need(g && out, "null argument");
-        CUDA_TRY(cudaSetDevice(g->device));
+        CUDA_TRY(cudaSetDevice(g->device)); HANDLE_LOCK(g);
         std::vector<riki_results *> res;
         engine_fetch(g, n_queries, &res);
         for (uint32_t q = 0; q < n_queries; q++) out[q] = res[q];
@@ -288,26 +292,36 @@ riki_status riki_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t n
                                 uint8_t *H_out, uint8_t *block_out, uint64_t *relax_out, int32_t *L_end_out) {
     return guard([&] {
         need(g && terms, "null argument");
-        CUDA_TRY(cudaSetDevice(g->device));
+        CUDA_TRY(cudaSetDevice(g->device)); HANDLE_LOCK(g);
         engine_hitting_levels(g, terms, n_terms, depth, block_mode, H_out, block_out, relax_out, L_end_out);
     });
 }
 
+riki_status riki_debug_ln_table(int device, uint64_t n0, uint64_t count, double *out) {
+    return guard([&] {
+        need(out != nullptr || count == 0, "null output");
+        need(n0 >= 1, "ln is taken of counts >= 1");
+        check_device(device);
+        graph_debug_ln_table(device, n0, count, out);
+    });
+}
+
 riki_status riki_set_profiling(riki_graph *g, int on) {
-    return guard([&] { need(g, "null graph"); g->profiling = on != 0; });
+    return guard([&] { need(g, "null graph"); HANDLE_LOCK(g); g->profiling = on != 0; });
 }
 riki_status riki_get_stats(const riki_graph *g, riki_stats *o) {
-    return guard([&] { need(g && o, "null argument"); *o = g->stats; });
+    return guard([&] { need(g && o, "null argument"); HANDLE_LOCK(g); *o = g->stats; });
 }
 riki_status riki_reset_stats(riki_graph *g) {
-    return guard([&] { need(g, "null graph"); g->stats = riki_stats{}; });
+    return guard([&] { need(g, "null graph"); HANDLE_LOCK(g); g->stats = riki_stats{}; });
 }
 riki_status riki_set_debug(riki_graph *g, int on) {
-    return guard([&] { need(g, "null graph"); g->debug = on != 0; });
+    return guard([&] { need(g, "null graph"); HANDLE_LOCK(g); g->debug = on != 0; });
 }
 riki_status riki_set_direction(riki_graph *g, int mode) {
     return guard([&] {
         need(g, "null graph");
+        HANDLE_LOCK(g);
         need(mode == 0 || mode == 1, "direction mode must be 0 or 1");
         g->pull_on = mode == 1;
     });
@@ -315,6 +329,7 @@ riki_status riki_set_direction(riki_graph *g, int mode) {
 riki_status riki_set_joint(riki_graph *g, int on) {
     return guard([&] {
         need(g, "null graph");
+        HANDLE_LOCK(g);
         need(!(on && g->vp()), "joint traversal is not available in vertex-partitioned mode");
         g->joint_on = on != 0;
     });
@@ -327,7 +342,7 @@ riki_status riki_sample_avg_hops(riki_graph *g, uint32_t n_pairs, const uint32_t
         need(g, "null graph");
         need(n_pairs == 0 || (src && dst), "null pair arrays");
         need(max_hops >= 1, "max_hops must be >= 1");
-        CUDA_TRY(cudaSetDevice(g->device));
+        CUDA_TRY(cudaSetDevice(g->device)); HANDLE_LOCK(g);
         std::vector<uint32_t> dist(n_pairs);
         graph_sample_hops(g, n_pairs, src, dst, max_hops, dist.data());
         // exact integer moments, then one division each (order independent; R30)
@@ -356,6 +371,7 @@ riki_status riki_sample_avg_hops(riki_graph *g, uint32_t n_pairs, const uint32_t
 riki_status riki_set_arena_limit(riki_graph *g, uint64_t words) {
     return guard([&] {
         need(g, "null graph");
+        HANDLE_LOCK(g);
         need(words == 0 || words >= 4096, "arena limit must be 0 or >= 4096 words");
         g->arena_limit = words;
         g->slots_cap = 0;
@@ -371,7 +387,7 @@ riki_status riki_dist_unique_id(void *out128) {
 riki_status riki_dist_init(riki_graph *g, int nranks, int rank, const void *uid, int mode) {
     return guard([&] {
         need(g, "null graph");
-        CUDA_TRY(cudaSetDevice(g->device));
+        CUDA_TRY(cudaSetDevice(g->device)); HANDLE_LOCK(g);
         dist_init(g, nranks, rank, uid, mode);
     });
 }
@@ -402,6 +418,7 @@ riki_status riki_dist_info(const riki_graph *g, int *nranks, int *rank, int *mod
 riki_status riki_set_batch_slots(riki_graph *g, uint32_t slots) {
     return guard([&] {
         need(g, "null graph");
+        HANDLE_LOCK(g);
         need(slots <= 1024, "at most 1024 slots");
         g->batch_slots = slots;
         g->slots_cap = 0;

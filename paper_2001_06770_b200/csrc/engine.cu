@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <chrono>
@@ -321,12 +322,13 @@ template <class RowT> __global__ void k_seed(GraphDev g, WsDev w, int ph) {
 __global__ void k_plan(WsDev w, int ph, uint32_t l_arg, uint32_t pull_min) {
     const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
     __shared__ unsigned long long sc[MAX_SLOTS];
-    __shared__ uint32_t nact, npull;
+    __shared__ uint32_t nact, wpull[MAX_SLOTS / 32];
     __shared__ unsigned long long nenq;
     uint32_t s = threadIdx.x;
-    if (s == 0) { nact = 0; npull = 0; nenq = 0; }
+    if (s == 0) { nact = 0; nenq = 0; }
     __syncthreads();
     uint32_t items = 0;
+    bool pl = false;
     if (s < w.nslots) {
         SlotState &st = w.st[s];
         if (st.in_phase) {
@@ -352,10 +354,21 @@ __global__ void k_plan(WsDev w, int ph, uint32_t l_arg, uint32_t pull_min) {
                 uint64_t total = (uint64_t)w.V * st.T[ph];
                 uint64_t unvisited = total > st.reached ? total - st.reached : 0;
                 st.pull = pull_min == 0 || (items >= pull_min && (uint64_t)items * PULL_ALPHA > unvisited);
-                if (st.pull) w.pslots[atomicAdd(&npull, 1u)] = s;
+                pl = st.pull;
             }
         }
     }
+    // pull slots in ascending slot order (a deterministic compaction, so every rank of the
+    // vertex-partitioned mode maps exchange position p to the same slot)
+    const uint32_t pb = __ballot_sync(FULLMASK, pl);
+    if ((s & 31) == 0) wpull[s >> 5] = __popc(pb);
+    __syncthreads();
+    uint32_t pbefore = 0, npull = 0;
+    for (uint32_t i = 0; i < MAX_SLOTS / 32; i++) {
+        pbefore += i < (s >> 5) ? wpull[i] : 0;
+        npull += wpull[i];
+    }
+    if (pl) w.pslots[pbefore + __popc(pb & lanemask_lt())] = s;
     // block exclusive scan (Hillis-Steele) over MAX_SLOTS
     sc[s] = items;
     __syncthreads();
@@ -2489,8 +2502,10 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     CUDA_TRY(cudaMallocHost(&ws->h_ctr, 64 * sizeof(uint32_t)));
     CUDA_TRY(cudaEventCreate(&ws->ev0));
     CUDA_TRY(cudaEventCreate(&ws->ev1));
-    static bool attr_done = false;
-    if (!attr_done) {
+    // function attributes are per device: set them once on every device a graph lives on
+    static std::atomic<uint64_t> attr_done{0};
+    const uint64_t dbit = 1ull << (g->device & 63);
+    if (!(attr_done.load() & dbit)) {
 #define SET_EX_ATTR(K) CUDA_TRY(cudaFuncSetAttribute(K<uint32_t, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ex<1>())); \
         CUDA_TRY(cudaFuncSetAttribute(K<uint64_t, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ex<1>())); \
         CUDA_TRY(cudaFuncSetAttribute(K<uint16_t, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ex<1>()));
@@ -2505,7 +2520,7 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
         CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
         CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
         CUDA_TRY(cudaFuncSetAttribute(k_final_lists<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, SORT_SMEM * 4));
-        attr_done = true;
+        attr_done.fetch_or(dbit);
     }
 }
 
@@ -2989,9 +3004,11 @@ uint32_t auto_slots(riki_graph *g, uint32_t nq, uint32_t rb0, uint32_t rb1, uint
 }
 
 void collect_results(riki_graph *g, Workspace *ws, uint32_t n_active, const std::vector<uint32_t> &qidx,
-                     std::vector<riki_results *> *out) {
-    cudaStream_t s = g->stream;
+                     std::vector<riki_results *> *out, cudaStream_t s) {
     const uint32_t ns = ws->cur ? ws->cur : ws->slots;
+    if (n_active > ns || qidx.size() < n_active)
+        RIKI_THROW(RIKI_EINVAL, "results of " + std::to_string(n_active) + " queries requested from a batch of " +
+                                    std::to_string(ns) + " slots");
     std::vector<SlotState> st(ns);
     std::vector<OutHdr> hdr((size_t)ns * ws->kmax);
     unsigned long long used = 0;
@@ -3054,6 +3071,11 @@ std::string err_text(uint32_t e) {
 // Grows capacities and re-runs when a workspace overflow is reported.
 // Returns false when the batch needs more recovery arena than 32-bit offsets address: the
 // caller re-runs it in smaller chunks (caps.slots halved).
+// shape of a batch the remembered chunk size applies to (depth, row widths, k)
+uint64_t slots_cap_key(const Caps &c, uint32_t depth) {
+    return (uint64_t)depth << 40 | (uint64_t)c.rb[0] << 32 | (uint64_t)c.rb[1] << 24 | c.kmax;
+}
+
 bool run_with_retry(riki_graph *g, Launch &L, uint32_t depth, Caps &caps, uint32_t n_active,
                     const std::function<void()> &upload, std::vector<SlotState> *st_out) {
     for (int attempt = 0;; attempt++) {
@@ -3078,8 +3100,12 @@ bool run_with_retry(riki_graph *g, Launch &L, uint32_t depth, Caps &caps, uint32
             const uint64_t amax = g->arena_limit ? std::min<uint64_t>(g->arena_limit, ARENA_MAX_WORDS) : ARENA_MAX_WORDS;
             if (caps.arena >= amax) {
                 if (n_active <= 1) RIKI_THROW(RIKI_ENOMEM, "recovery arena exceeds 2^32 words for one query");
+                const bool full_chunk = n_active >= caps.slots;  // not a short tail chunk
                 caps.slots = std::max(1u, n_active / 2);
-                g->slots_cap = caps.slots;  // remembered: later batches start at this chunk size
+                if (full_chunk) {  // remembered for later batches of the same shape only
+                    g->slots_cap = caps.slots;
+                    g->slots_cap_key = slots_cap_key(caps, depth);
+                }
                 return false;
             }
             caps.arena = std::min<uint64_t>(caps.arena * 4, amax);
@@ -3151,14 +3177,16 @@ static void check_common(riki_graph *g, uint32_t k, uint32_t depth, const riki_p
     if (p.beam_w && p.beam_w < k) RIKI_THROW(RIKI_EINVAL, "beam width must be >= k (P:309)");
 }
 
-static Caps initial_caps(riki_graph *g, uint32_t nq, uint32_t k, uint32_t rb0, uint32_t rb1, uint32_t want_hint = 0) {
+static Caps initial_caps(riki_graph *g, uint32_t nq, uint32_t k, uint32_t rb0, uint32_t rb1, uint32_t depth,
+                         uint32_t want_hint = 0) {
     Caps c;
     c.rb[0] = rb0;
     c.rb[1] = rb1;
     c.slots = auto_slots(g, nq, rb0, rb1, want_hint);
-    if (g->slots_cap) c.slots = std::min(c.slots, g->slots_cap);  // a batch this wide overflowed the arena
     c.capc = std::min<uint32_t>(16384, next_pow2(g->V + 1));
     c.kmax = std::max<uint32_t>(k, g->ws ? g->ws->kmax : 1);
+    // a full-width batch of this shape overflowed the arena before: start at its chunk size
+    if (g->slots_cap && g->slots_cap_key == slots_cap_key(c, depth)) c.slots = std::min(c.slots, g->slots_cap);
     c.arena = std::max<uint64_t>(64ull << 20, g->ws ? g->ws->arena_cap : 0);
     if (g->arena_limit) c.arena = std::min<uint64_t>(c.arena, g->arena_limit);
     c.out = std::max<uint64_t>(16ull << 20, g->ws ? g->ws->out_cap : 0);
@@ -3176,18 +3204,14 @@ void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, ui
     Tracer tr;
     uint32_t maxc0 = 0, maxm0 = 0;
     for (const QueryIn &q : qs) { maxc0 = std::max(maxc0, q.nc); maxm0 = std::max(maxm0, q.nm); }
-    Caps caps = initial_caps(g, (uint32_t)qs.size(), k, row_bytes(maxc0), row_bytes(std::max(maxm0, 1u)));
+    Caps caps = initial_caps(g, (uint32_t)qs.size(), k, row_bytes(maxc0), row_bytes(std::max(maxm0, 1u)), depth);
     tr("initial_caps");
+    // every launch and copy of the search is issued on the caller's stream when one is given
+    // (ordered after the caller's earlier work on it), else on the library stream
     Launch L{g, stream ? stream : g->stream};
-    if (stream) {
-        // run on the library stream, ordered after the caller's stream
-        cudaEvent_t e;
-        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        CUDA_TRY(cudaEventRecord(e, stream));
-        CUDA_TRY(cudaStreamWaitEvent(g->stream, e, 0));
-        cudaEventDestroy(e);
-        L.s = g->stream;
-    }
+    if (g->ws) g->ws->last_n = 0;  // the workspace is reused: a pending device batch is gone
+    for (riki_results *r : g->dev_stash) delete r;
+    g->dev_stash.clear();
     uint32_t maxc = 0, maxm = 0;
     for (const QueryIn &q : qs) { maxc = std::max(maxc, q.nc); maxm = std::max(maxm, q.nm); }
     SlotState tmpl = make_template(k, depth, p);
@@ -3227,7 +3251,7 @@ void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, ui
             tr("before run");
             if (!run_with_retry(g, L, depth, caps, n, upload, &stv)) continue;  // smaller chunk
             tr("run_with_retry");
-            collect_results(g, g->ws, n, qidx, &res);
+            collect_results(g, g->ws, n, qidx, &res, L.s);
             tr("collect_results");
             add_stats(g, g->ws, L, n);
             tr("add_stats");
@@ -3258,7 +3282,7 @@ void engine_search_device(riki_graph *g, uint32_t nq, const uint64_t *d_cptr, co
     if (maxc > RIKI_MAX_TERMS || maxm > RIKI_MAX_TERMS) RIKI_THROW(RIKI_EINVAL, "at most 8 terms per keyword class");
     tr("ptr D2H");
     // the whole batch in flight when it fits the device memory (auto_slots), else chunks
-    Caps caps = initial_caps(g, nq, k, row_bytes(std::max(maxc, 1u)), row_bytes(std::max(maxm, 1u)),
+    Caps caps = initial_caps(g, nq, k, row_bytes(std::max(maxc, 1u)), row_bytes(std::max(maxm, 1u)), depth,
                              std::max(g->batch_slots, std::min<uint32_t>(nq, MAX_SLOTS)));
     tr("initial_caps");
     ensure_workspace(g, caps);
@@ -3295,7 +3319,7 @@ void engine_search_device(riki_graph *g, uint32_t nq, const uint64_t *d_cptr, co
             g->dev_stash.resize(nq, nullptr);
             std::vector<uint32_t> qidx(n);
             for (uint32_t i = 0; i < n; i++) qidx[i] = q0 + i;
-            collect_results(g, g->ws, n, qidx, &g->dev_stash);
+            collect_results(g, g->ws, n, qidx, &g->dev_stash, L.s);
         }
         add_stats(g, g->ws, L, n);
         q0 += n;
@@ -3309,12 +3333,14 @@ void engine_fetch(riki_graph *g, uint32_t nq, std::vector<riki_results *> *out) 
     if (!g->dev_stash.empty()) {  // the batch ran in chunks: results were collected per chunk
         *out = std::move(g->dev_stash);
         g->dev_stash.clear();
+        g->ws->last_n = 0;
         return;
     }
     out->assign(nq, nullptr);
     std::vector<uint32_t> qidx(nq);
     for (uint32_t i = 0; i < nq; i++) qidx[i] = i;
-    collect_results(g, g->ws, nq, qidx, out);
+    collect_results(g, g->ws, nq, qidx, out, g->stream);
+    g->ws->last_n = 0;  // fetched once: a second fetch is an error, not a stale read
 }
 
 void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uint32_t depth, int block_mode,
@@ -3328,7 +3354,10 @@ void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uin
     q.nc = T;
     for (uint32_t j = 0; j < T; j++) q.c[j] = terms[j];
     check_query_host(g, q);
-    Caps caps = initial_caps(g, 1, 1, row_bytes(T), 2);
+    Caps caps = initial_caps(g, 1, 1, row_bytes(T), 2, depth);
+    if (g->ws) g->ws->last_n = 0;  // the workspace is reused: a pending device batch is gone
+    for (riki_results *r : g->dev_stash) delete r;
+    g->dev_stash.clear();
     for (int attempt = 0;; attempt++) {  // grows the frontier queues on E_QUEUE (see run_with_retry)
     ensure_workspace(g, caps);
     Workspace *ws = g->ws;

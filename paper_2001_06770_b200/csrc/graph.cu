@@ -94,10 +94,19 @@ __global__ void k_run_length(const uint64_t *key, const uint32_t *eid, uint64_t 
     }
 }
 
-// P:193 raw weight = ln(count_out + count_in); stored as double
+// P:193 raw weight = ln(count_out + count_in) of the integer count (R2: natural log); the
+// oracle takes glibc's log of the same integer, and riki_debug_ln_table exposes this exact
+// function so a test compares the two over the whole integer domain the counts can take.
+__device__ __forceinline__ double raw_ln(uint64_t n) { return log((double)n); }
+
 __global__ void k_raw_weight(const uint32_t *co, const uint32_t *ci, uint64_t n, double *raw) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        raw[i] = log((double)(co[i] + ci[i]));
+        raw[i] = raw_ln((uint64_t)co[i] + ci[i]);
+}
+
+__global__ void k_ln_table(uint64_t n0, uint64_t count, double *out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = raw_ln(n0 + i);
 }
 
 // P:194 min-max rescale; degenerate max == min -> 0 (R2)
@@ -520,4 +529,16 @@ void graph_get_act(const riki_graph *g, uint8_t *a) {
     if (!g->has_act) RIKI_THROW(RIKI_ENOWEIGHTS, "activation levels not set");
     if (g->E) CUDA_TRY(cudaMemcpyAsync(a, g->d_act_e, g->E, cudaMemcpyDeviceToHost, g->stream));
     sync_check(g->stream);
+}
+
+void graph_debug_ln_table(int device, uint64_t n0, uint64_t count, double *out_host) {
+    CUDA_TRY(cudaSetDevice(device));
+    double *d = nullptr;
+    if (count == 0) return;
+    CUDA_TRY(cudaMalloc(&d, count * sizeof(double)));
+    k_ln_table<<<grid_for(count), 256>>>(n0, count, d);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(out_host, d, count * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) RIKI_THROW(RIKI_ECUDA, std::string("ln table: ") + cudaGetErrorString(e));
 }

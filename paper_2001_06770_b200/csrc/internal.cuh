@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "../../include/riki.h"
@@ -93,7 +94,12 @@ struct riki_graph {
     DistState *dist = nullptr;  // set by riki_dist_init
     std::vector<riki_results *> dev_stash;
     uint64_t arena_limit = 0;  // riki_set_arena_limit (tests): 0 = the 32-bit offset limit
-    uint32_t slots_cap = 0;    // chunk size learnt from an arena-limited batch (0 = none)  // device batch run in chunks: results collected per chunk
+    uint32_t slots_cap = 0;    // chunk size learnt from an arena-limited full-width batch (0 = none)
+    uint64_t slots_cap_key = 0;  // ... and the batch shape it applies to (depth, row widths, k)
+    // Serialises every call on this handle (riki_rpq_search*, fetch, hitting levels, weights,
+    // dist): the workspace, its cached CUDA graphs and the device-batch stash are per handle,
+    // so concurrent callers on one graph run one after the other (include/riki.h, Threading).
+    mutable std::recursive_mutex mu;
     bool vp() const { return dist && dist->mode == 1; }
 
     GraphDev dev() const {
@@ -117,6 +123,7 @@ void graph_set_node_weights(riki_graph *g, const double *w01, double alpha, doub
 void graph_set_label_weights(riki_graph *g, double alpha, double avg);
 void graph_set_act(riki_graph *g, const uint8_t *a);
 void graph_get_act(const riki_graph *g, uint8_t *a);
+void graph_debug_ln_table(int device, uint64_t n0, uint64_t count, double *out_host);
 
 // engine.cu
 struct QueryIn {

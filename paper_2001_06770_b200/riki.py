@@ -120,6 +120,7 @@ def load():
         "riki_dist_init": (i32, [P, i32, i32, P, i32]),
         "riki_dist_partition": (i32, [P, u32, u32, P]),
         "riki_dist_info": (i32, [P, P, P, P, P, P, P]),
+        "riki_debug_ln_table": (i32, [i32, u64, u64, P]),
         "riki_last_error": (C.c_char_p, []),
         "riki_version": (C.c_char_p, []),
     }
@@ -129,6 +130,14 @@ def load():
         f.argtypes = args
     _lib = lib
     return lib
+
+
+def debug_ln_table(n0: int, count: int, device: int = 0) -> np.ndarray:
+    """The device's ln(n) for n in [n0, n0 + count), as the fine-weight kernel computes it
+    (riki_debug_ln_table)."""
+    out = np.empty(count, np.float64)
+    _check(load().riki_debug_ln_table(device, n0, count, _p(out)))
+    return out
 
 
 def dist_unique_id() -> bytes:
@@ -356,13 +365,15 @@ class Graph:
         return H, b, int(rel.value), int(L.value)
 
     # -- search
-    def search(self, central, marginal, k, depth, **kw) -> Result:
+    def search(self, central, marginal, k, depth, stream=None, **kw) -> Result:
+        """stream: a cudaStream_t handle (e.g. torch.cuda.Stream().cuda_stream) the search is
+        issued on, or None for the library stream."""
         c = np.ascontiguousarray(central, np.uint32)
         m = np.ascontiguousarray(marginal, np.uint32)
         prm = params(**kw)
         h = C.c_void_p()
-        _check(self.lib.riki_rpq_search(self.h, _p(c), len(c), _p(m), len(m), k, depth, C.byref(prm), None,
-                                        C.byref(h)))
+        _check(self.lib.riki_rpq_search(self.h, _p(c), len(c), _p(m), len(m), k, depth, C.byref(prm),
+                                        C.c_void_p(stream) if stream else None, C.byref(h)))
         return _take_results(self.lib, h, len(c), len(m))
 
     @staticmethod

@@ -98,11 +98,24 @@ def _chung_lu_weights(rng, n, exponent):
     return w / w.sum()
 
 
+def _searchsorted_right(cdf, x):
+    """np.searchsorted(cdf, x, side="right"), identical result; torch's CPU kernel runs it on
+    every host core (the 30M-node configs draw 75M endpoints per side)."""
+    if len(x) >= 1 << 12:
+        try:
+            import torch
+            return torch.searchsorted(torch.from_numpy(np.ascontiguousarray(cdf)),
+                                      torch.from_numpy(np.ascontiguousarray(x)), right=True).numpy()
+        except ImportError:
+            pass
+    return np.searchsorted(cdf, x, side="right")
+
+
 def _sample(rng, p, size):
     # inverse-CDF sampling (equivalent in law to an alias table), deterministic per seed
     cdf = np.cumsum(p)
     cdf[-1] = 1.0
-    return np.searchsorted(cdf, rng.random(size), side="right").astype(np.int64)
+    return _searchsorted_right(cdf, rng.random(size)).astype(np.int64)
 
 
 def make_graph(n_nodes: int, n_edges: int, n_labels: int, seed: int, *, in_exp: float = 2.1,
@@ -169,7 +182,7 @@ def make_postings(n_nodes: int, n_terms: int, lo: int, hi: int, seed: int, degre
             if cdf is None:
                 draw = rng.integers(0, n_nodes, 2 * s + 8)
             else:
-                draw = np.searchsorted(cdf, rng.random(2 * s + 8), side="right")
+                draw = _searchsorted_right(cdf, rng.random(2 * s + 8))
             nodes = np.unique(np.concatenate([nodes, draw]))
             if len(nodes) >= s:
                 break

@@ -62,3 +62,30 @@ def test_fails_loudly_without_device():
         P.Graph(3, np.array([0, 1], np.uint32), np.array([1, 0], np.uint32), None,
                 np.array([0, 1], np.uint64), np.array([0], np.uint32))
     assert e.value.name == "RIKI_ECUDA"
+
+
+def _build_c_client(tmp_path):
+    """tests/c/abi_smoke.c compiled and linked against libriki.so with the plain C compiler and
+    include/riki.h only (no C++ or CUDA headers): the boundary is a C ABI."""
+    B.build()
+    exe = str(tmp_path / "abi_smoke")
+    libdir = os.path.dirname(P.riki.LIB_PATH)
+    subprocess.check_call(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "c", "abi_smoke.c"), "-o", exe, "-L", libdir, "-lriki",
+                           "-Wl,-rpath," + libdir])
+    return exe
+
+
+def test_plain_c_client_compiles_and_links(tmp_path):
+    exe = _build_c_client(tmp_path)
+    assert os.path.exists(exe)
+    out = subprocess.check_output(["nm", "-u", exe], text=True)
+    assert "riki_rpq_search" in out and "riki_load_graph" in out
+
+
+@pytest.mark.gpu
+def test_plain_c_client_runs(tmp_path):
+    exe = _build_c_client(tmp_path)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "ABI_SMOKE_OK" in r.stdout
