@@ -59,6 +59,7 @@ def _load():
         "orc_res_count": (u32, [P]),
         "orc_res_ncand": (u32, [P]),
         "orc_res_levels": (None, [P, P, P, P, P, P, P]),
+        "orc_res_times": (None, [P, P, P]),
         "orc_res_cand": (None, [P, u32, P, P, P, P, P, P, P, P, P]),
         "orc_res_cand_lists": (None, [P, u32, P, P, P]),
         "orc_res_get": (None, [P, u32, P, P, P, P, P, P, P, P, P]),
@@ -242,6 +243,9 @@ def search(g: Graph, central_nodes, marginal_nodes, k: int, depth: int, gamma: f
         na, nf = C.c_uint32(), C.c_uint32()
         lib.orc_res_levels(r, C.byref(Lc), C.byref(Lm), C.byref(rc), C.byref(rm), C.byref(na), C.byref(nf))
         out = SearchResult([], [], Lc.value, Lm.value, rc.value, rm.value, na.value, nf.value)
+        tc, tm = C.c_double(), C.c_double()
+        lib.orc_res_times(r, C.byref(tc), C.byref(tm))
+        out.extra["t_central"], out.extra["t_marginal"] = tc.value, tm.value
         u32, u64, i32, dbl = C.c_uint32, C.c_uint64, C.c_int, C.c_double
         for i in range(lib.orc_res_count(r)):
             ci, v, sc, sm, sr, ptc = u32(), u32(), u32(), u32(), dbl(), i32()

@@ -25,8 +25,10 @@
  * Parity status: every function is pinned by tests/test_oracle_*.py (worked
  * examples, closed forms, brute force); see DESIGN.md §4 for the pin list.
  */
+#define _POSIX_C_SOURCE 199309L
 #include <math.h>
 #include <stdint.h>
+#include <time.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -75,39 +77,47 @@ static void sort_unique_u64(vu64 *v) {
  * over out-edges of v_i and in-edges of v_j; both counts include e_ij (R3);
  * the label class is (label, inverse flag) as the caller encodes it in cls[].
  * rescale to [0,1] by min-max; all zero when max = min (R2). */
+typedef struct { uint64_t key, e; } keyed_edge;
+static int cmp_keyed(const void *x, const void *y) {
+    const keyed_edge *a = x, *b = y;
+    if (a->key != b->key) return a->key < b->key ? -1 : 1;
+    return a->e < b->e ? -1 : a->e > b->e;
+}
+
+/* cnt[e] = number of edges e' with node[e'] == node[e] and cls[e'] == cls[e]: bucket the
+ * edges by node (counting sort), sort each bucket's (class, e) pairs, and give every run of
+ * equal classes its length. */
+static int count_node_class(uint32_t V, uint64_t E, const uint32_t *node, const uint32_t *cls, uint64_t *cnt) {
+    uint64_t *ptr = calloc((uint64_t)V + 2, sizeof(uint64_t));
+    keyed_edge *b = malloc((E ? E : 1) * sizeof(keyed_edge));
+    if (!ptr || !b) { free(ptr); free(b); return -2; }
+    for (uint64_t e = 0; e < E; e++) ptr[node[e] + 2]++;
+    for (uint64_t v = 0; v < V; v++) ptr[v + 2] += ptr[v + 1];
+    for (uint64_t e = 0; e < E; e++) { keyed_edge *x = &b[ptr[node[e] + 1]++]; x->key = cls[e]; x->e = e; }
+    for (uint64_t v = 0; v < V; v++) {
+        uint64_t lo = ptr[v], hi = ptr[v + 1];
+        qsort(b + lo, hi - lo, sizeof(keyed_edge), cmp_keyed);
+        for (uint64_t r = lo; r < hi;) {
+            uint64_t x = r;
+            while (x < hi && b[x].key == b[r].key) x++;
+            for (uint64_t t = r; t < x; t++) cnt[b[t].e] = x - r;
+            r = x;
+        }
+    }
+    free(ptr); free(b);
+    return 0;
+}
+
 int orc_fine_weights(uint32_t V, uint64_t E, const uint32_t *src, const uint32_t *dst,
                      const uint32_t *cls, double *w01) {
-    /* count (node, class) pairs by sorting keys: plain and obviously correct */
-    uint64_t *ko = malloc((E ? E : 1) * sizeof(uint64_t) * 2);
-    uint64_t *ki = ko + E;
     double *raw = w01;
-    if (!ko) return -2;
-    (void)V;
-    for (uint64_t e = 0; e < E; e++) {
-        ko[e] = ((uint64_t)src[e] << 32) | cls[e];
-        ki[e] = ((uint64_t)dst[e] << 32) | cls[e];
-    }
-    uint64_t *so = malloc((E ? E : 1) * sizeof(uint64_t) * 2);
-    uint64_t *si = so + E;
-    memcpy(so, ko, E * sizeof(uint64_t));
-    memcpy(si, ki, E * sizeof(uint64_t));
-    qsort(so, E, sizeof(uint64_t), cmp_u64);
-    qsort(si, E, sizeof(uint64_t), cmp_u64);
-    for (uint64_t e = 0; e < E; e++) {
-        /* count of key in sorted array = upper_bound - lower_bound */
-        uint64_t cnt[2];
-        const uint64_t *arr[2] = {so, si};
-        uint64_t key[2] = {ko[e], ki[e]};
-        for (int s = 0; s < 2; s++) {
-            uint64_t lo = 0, hi = E;
-            while (lo < hi) { uint64_t m = (lo + hi) / 2; if (arr[s][m] < key[s]) lo = m + 1; else hi = m; }
-            uint64_t lb = lo; hi = E;
-            while (lo < hi) { uint64_t m = (lo + hi) / 2; if (arr[s][m] <= key[s]) lo = m + 1; else hi = m; }
-            cnt[s] = lo - lb;
-        }
-        raw[e] = log((double)(cnt[0] + cnt[1]));
-    }
-    free(ko); free(so);
+    uint64_t *co = malloc((E ? E : 1) * sizeof(uint64_t)), *ci = malloc((E ? E : 1) * sizeof(uint64_t));
+    if (!co || !ci) { free(co); free(ci); return -2; }
+    /* |{e_ix : l(e_ix) = l(e_ij)}|: out-edges of the source with the edge's class;
+     * |{e_xj : l(e_xj) = l(e_ij)}|: in-edges of the target with the edge's class */
+    if (count_node_class(V, E, src, cls, co) || count_node_class(V, E, dst, cls, ci)) { free(co); free(ci); return -2; }
+    for (uint64_t e = 0; e < E; e++) raw[e] = log((double)(co[e] + ci[e]));
+    free(co); free(ci);
     if (E == 0) return 0;
     double mn = raw[0], mx = raw[0];
     for (uint64_t e = 1; e < E; e++) { if (raw[e] < mn) mn = raw[e]; if (raw[e] > mx) mx = raw[e]; }
@@ -446,7 +456,15 @@ typedef struct orc_result {
     int Lc, Lm;                        /* terminating levels (-1 if the run did not happen) */
     uint64_t relax_c, relax_m;
     uint32_t n_attached, n_ptc_fail;
+    double t_central, t_marginal;      /* seconds (steady clock): run 1 + CG recovery, then run 2 */
 } orc_result;
+
+/* steady clock for the phase split of the timing protocol (Fig. 5 analogue) */
+static double now_s(void) {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
+}
 
 static int key_less(const cand_t *a, const cand_t *b, int tie) {
     /* (S^r, S^c, v) ascending (R23); tie_break 1: (S^r, S^c, W, v) -- P:293 "break the ties
@@ -499,6 +517,7 @@ orc_result *orc_search(const orc_graph *g,
     orc_result *r = calloc(1, sizeof(orc_result));
     r->nc = nc; r->nm = nm; r->k = k; r->V = g->V; r->Lc = -1; r->Lm = -1;
     scratch_t s; s.seen = calloc(g->V + 1, 4); s.stamp = 0;
+    const double t0 = now_s();
 
     /* ---- first run: central keywords -> candidate CGs ---- */
     phase_t pc;
@@ -564,6 +583,8 @@ orc_result *orc_search(const orc_graph *g,
     }
 
     uint32_t *kb = calloc(k + 1, 4), nkb = 0;
+    const double t1 = now_s();
+    r->t_central = t1 - t0;
     if (nm == 0) {
         /* M = empty is a classic keyword search: top-k CGs by (S^c, v) */
         for (uint32_t i = 0; i < ncand; i++) {
@@ -650,6 +671,7 @@ orc_result *orc_search(const orc_graph *g,
         free(pm.F); free(pm.phi);
     }
     r->nres = nkb; r->res = kb;
+    r->t_marginal = now_s() - t1;
     r->Hc = pc.H; r->bc = pc.block; pc.H = NULL; pc.block = NULL;
     free(pc.F); free(pc.phi);
     free(s.seen);
@@ -669,6 +691,9 @@ void orc_result_free(orc_result *r) {
 
 /* ---- accessors (plain C types for ctypes) ---- */
 uint32_t orc_res_count(const orc_result *r) { return r->nres; }
+void orc_res_times(const orc_result *r, double *t_central, double *t_marginal) {
+    *t_central = r->t_central; *t_marginal = r->t_marginal;
+}
 uint32_t orc_res_ncand(const orc_result *r) { return r->ncand; }
 void orc_res_levels(const orc_result *r, int *Lc, int *Lm, uint64_t *relax_c, uint64_t *relax_m,
                     uint32_t *n_attached, uint32_t *n_ptc_fail) {
