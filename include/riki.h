@@ -254,6 +254,13 @@ typedef struct {
     uint64_t levels;               /* lock-step level iterations (one host sync each)       */
     uint64_t retries;              /* batches re-run after a workspace capacity overflow    */
     uint64_t reallocs;             /* workspace (re)allocations                             */
+    /* expansion work counted on the device (every batch, profiling or not), the units of the
+       SURVEY §8(d) algorithmic-byte model of the expansion kernel: */
+    uint64_t exp_items;            /* frontier items (f, l) consumed, incl. duplicates/blocked */
+    uint64_t exp_items_work;       /* items with a non-empty due edge range: distinct (f, L) */
+    uint64_t exp_edges;            /* edge reads = distinct (e, L) pairs P_e                */
+    uint64_t exp_new_cells;        /* H cells written (inf -> l+1)                          */
+    uint64_t exp_enqueued;         /* next-frontier queue entries written                   */
 } riki_stats;
 riki_status riki_set_profiling(riki_graph *g, int on);
 riki_status riki_get_stats(const riki_graph *g, riki_stats *out);

@@ -33,7 +33,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + ".tmp%d" % os.getpid()
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-                               "-shared", "-o", tmp, _SRC, "-lm"])
+                               "-shared", "-o", tmp, _SRC, "-lquadmath", "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -47,6 +47,7 @@ def _load():
     sig = {
         "orc_fine_weights": (i32, [u32, u64, P, P, P, P]),
         "orc_coarsen": (i32, [dbl, dbl, dbl]),
+        "orc_ln_count": (dbl, [u64]),
         "orc_coarsen_all": (None, [u64, P, dbl, dbl, P]),
         "orc_bound": (None, [i32, dbl, dbl, P, P]),
         "orc_path_score": (i32, [P, i32]),
@@ -96,6 +97,11 @@ def fine_weights(n_nodes: int, src, dst, cls) -> np.ndarray:
     if rc:
         raise MemoryError("oracle fine_weights")
     return out
+
+
+def ln_count(n: int) -> float:
+    """R31: ln of an integer count, correctly rounded to fp64 (P:193's log)."""
+    return _load().orc_ln_count(n)
 
 
 def coarsen(w: float, alpha: float, avg_hops: float) -> int:

@@ -27,6 +27,7 @@
  */
 #define _POSIX_C_SOURCE 199309L
 #include <math.h>
+#include <quadmath.h>
 #include <stdint.h>
 #include <time.h>
 #include <stdlib.h>
@@ -74,7 +75,8 @@ static void sort_unique_u64(vu64 *v) {
 /* ------------------------------------------------------------------ */
 
 /* w_ij = log(|{e_ix : l(e_ix) = l(e_ij)}| + |{e_xj : l(e_xj) = l(e_ij)}|)
- * over out-edges of v_i and in-edges of v_j; both counts include e_ij (R3);
+ * over out-edges of v_i and in-edges of v_j; both counts include e_ij (R3); log is the
+ * natural log (R2), its fp64 value correctly rounded (R31, orc_ln_count);
  * the label class is (label, inverse flag) as the caller encodes it in cls[].
  * rescale to [0,1] by min-max; all zero when max = min (R2). */
 typedef struct { uint64_t key, e; } keyed_edge;
@@ -108,6 +110,11 @@ static int count_node_class(uint32_t V, uint64_t E, const uint32_t *node, const 
     return 0;
 }
 
+/* R31: the fp64 value of ln n for an integer n >= 1, correctly rounded: binary128 logq is
+ * accurate to ~2^-112, so one rounding to 53 bits gives the nearest double (ln n is never
+ * exactly a rounding midpoint for n > 1).  glibc's log is within ~0.52 ulp and is not. */
+double orc_ln_count(uint64_t n) { return (double)logq((__float128)n); }
+
 int orc_fine_weights(uint32_t V, uint64_t E, const uint32_t *src, const uint32_t *dst,
                      const uint32_t *cls, double *w01) {
     double *raw = w01;
@@ -116,8 +123,19 @@ int orc_fine_weights(uint32_t V, uint64_t E, const uint32_t *src, const uint32_t
     /* |{e_ix : l(e_ix) = l(e_ij)}|: out-edges of the source with the edge's class;
      * |{e_xj : l(e_xj) = l(e_ij)}|: in-edges of the target with the edge's class */
     if (count_node_class(V, E, src, cls, co) || count_node_class(V, E, dst, cls, ci)) { free(co); free(ci); return -2; }
-    for (uint64_t e = 0; e < E; e++) raw[e] = log((double)(co[e] + ci[e]));
-    free(co); free(ci);
+    /* R31: ln of the integer count, correctly rounded to fp64 -- evaluated in binary128
+     * (113-bit) arithmetic and rounded once; memoised per distinct count */
+    uint64_t cmax = 0;
+    for (uint64_t e = 0; e < E; e++) if (co[e] + ci[e] > cmax) cmax = co[e] + ci[e];
+    double *lnc = malloc((cmax + 1) * sizeof(double));
+    uint8_t *have = calloc(cmax + 1, 1);
+    if (!lnc || !have) { free(co); free(ci); free(lnc); free(have); return -2; }
+    for (uint64_t e = 0; e < E; e++) {
+        uint64_t n = co[e] + ci[e];
+        if (!have[n]) { lnc[n] = orc_ln_count(n); have[n] = 1; }
+        raw[e] = lnc[n];
+    }
+    free(co); free(ci); free(lnc); free(have);
     if (E == 0) return 0;
     double mn = raw[0], mx = raw[0];
     for (uint64_t e = 1; e < E; e++) { if (raw[e] < mn) mn = raw[e]; if (raw[e] > mx) mx = raw[e]; }

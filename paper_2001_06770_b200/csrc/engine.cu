@@ -58,7 +58,7 @@ enum Ctr { C_NHEAVY = 0, C_NNEWATT, C_NOVF, C_ACTIVE, C_TOTAL, C_NCAND_TOTAL, C_
 // level argument of the per-level kernels: a value, or LV_DEVICE = read the device level
 // counter ctr[C_LEVEL] (the whole-run CUDA graph with a device-side while loop)
 constexpr uint32_t LV_DEVICE = 0xFFFFFFFFu;
-enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_PULLNODES, P_PULLEDGES,
+enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_PULLNODES, P_PULLEDGES, P_ITEMS_WORK,
             // recovery diagnostics (compiled in with -DREC_STATS=1)
             P_R_BUILDS = 8, P_R_BEDGES, P_R_BCYC, P_R_WAITS, P_R_WCYC, P_R_CANDS, P_R_CANDCYC, P_R_CANDMAX, P_R_BMAX,
             P_R_ITEMS, P_R_WARPMAX, P_R_H0,  // P_R_H0..+5: candidate-time histogram
@@ -617,7 +617,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
     RowT *const Hb = (RowT *)w.H[ph];  // per-slot layout (HGRP groups; never joint here)
     const size_t V = w.V;
     OwnF<RowT> *const own = s_own[threadIdx.x >> 5];
-    uint32_t p_edges = 0, p_cells = 0;  // items and queue entries are counted by k_plan
+    uint32_t p_edges = 0, p_cells = 0, p_work = 0;  // items and queue entries are counted by k_plan
 
     for (IdxT base = (IdxT)gw * 32; base < total; base += (IdxT)nw * 32) {
         const IdxT item = base + lane;
@@ -655,6 +655,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
                     eq0 = eqlo;
                     len = hi - lo;
                     relaxn = (hi - rb) * R::ones(newc) + (hi - eqlo) * R::ones(oldc);
+                    p_work += len > 0;
 #if EXP_STATS
                     atomicAdd(&w.prof[len ? P_X_WORK : P_X_IDLE], 1ull);
 #endif
@@ -770,9 +771,11 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
     }
     p_edges = warp_sum(p_edges);
     p_cells = warp_sum(p_cells);
+    p_work = warp_sum(p_work);
     if (lane == 0 && (p_edges | p_cells)) {
         atomicAdd(&w.prof[P_EDGES], (unsigned long long)p_edges);
         atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
+        atomicAdd(&w.prof[P_ITEMS_WORK], (unsigned long long)p_work);
     }
 }
 
@@ -3140,6 +3143,11 @@ void add_stats(riki_graph *g, Workspace *ws, Launch &L, uint32_t nq) {
                              prof[P_PULLNODES] * (8 + rb) + prof[P_PULLEDGES] * (5 + rb);
     g->stats.kernel_launches += L.launches;
     g->stats.queries += nq;
+    g->stats.exp_items += prof[P_ITEMS];
+    g->stats.exp_items_work += prof[P_ITEMS_WORK];
+    g->stats.exp_edges += prof[P_EDGES] + prof[P_PULLEDGES];
+    g->stats.exp_new_cells += prof[P_NEWCELLS];
+    g->stats.exp_enqueued += prof[P_ENQ];
     for (int i = 0; i < 4; i++) g->stats.section_ms[i] += L.sec_ms[i];
     g->stats.levels += L.levels;
     L.sec_ms[0] = L.sec_ms[1] = L.sec_ms[2] = L.sec_ms[3] = 0;

@@ -94,10 +94,59 @@ __global__ void k_run_length(const uint64_t *key, const uint32_t *eid, uint64_t 
     }
 }
 
-// P:193 raw weight = ln(count_out + count_in) of the integer count (R2: natural log); the
-// oracle takes glibc's log of the same integer, and riki_debug_ln_table exposes this exact
-// function so a test compares the two over the whole integer domain the counts can take.
-__device__ __forceinline__ double raw_ln(uint64_t n) { return log((double)n); }
+// P:193 raw weight = ln(count_out + count_in) of the integer count (R2: natural log), as the
+// CORRECTLY ROUNDED fp64 value of ln n (R31), so that it has one definition independent of any
+// math library: CUDA's log() is within 1 ulp and glibc's within ~0.52 ulp, and they disagree
+// on ~1 in 10^5 integers (riki_debug_ln_table + tests/test_gpu_boundary.py).  Computed in
+// double-double arithmetic (~2^-100 relative): n = 2^k * m, m in [sqrt(1/2), sqrt(2)),
+// ln n = k ln 2 + 2 atanh(z), z = (m - 1)/(m + 1), |z| < 0.172, atanh by its series to z^49;
+// the final hi + lo rounds to nearest.  Every operation is an explicit _rn intrinsic (no FMA
+// contraction may touch the error-free transforms).
+struct dd { double hi, lo; };
+__device__ __forceinline__ dd dd_two_sum(double a, double b) {
+    const double s = __dadd_rn(a, b), bb = __dsub_rn(s, a);
+    return {s, __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb))};
+}
+__device__ __forceinline__ dd dd_fast(double a, double b) {  // |a| >= |b|
+    const double s = __dadd_rn(a, b);
+    return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+    dd s = dd_two_sum(a.hi, b.hi), t = dd_two_sum(a.lo, b.lo);
+    s.lo = __dadd_rn(s.lo, t.hi);
+    s = dd_fast(s.hi, s.lo);
+    s.lo = __dadd_rn(s.lo, t.lo);
+    return dd_fast(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+    const double p = __dmul_rn(a.hi, b.hi);
+    double e = __fma_rn(a.hi, b.hi, -p);
+    e = __dadd_rn(e, __dadd_rn(__dmul_rn(a.hi, b.lo), __dmul_rn(a.lo, b.hi)));
+    return dd_fast(p, e);
+}
+__device__ __forceinline__ dd dd_neg(dd a) { return {-a.hi, -a.lo}; }
+__device__ __forceinline__ dd dd_div(dd a, dd b) {  // three correction steps
+    const double q1 = __ddiv_rn(a.hi, b.hi);
+    dd r = dd_add(a, dd_neg(dd_mul({q1, 0.0}, b)));
+    const double q2 = __ddiv_rn(r.hi, b.hi);
+    r = dd_add(r, dd_neg(dd_mul({q2, 0.0}, b)));
+    const double q3 = __ddiv_rn(r.hi, b.hi);
+    return dd_add(dd_fast(q1, q2), {q3, 0.0});
+}
+__device__ __noinline__ double raw_ln(uint64_t n) {
+    if (n <= 1) return 0.0;
+    int k = 0;
+    double m = frexp((double)n, &k);  // n < 2^53: exact; m in [0.5, 1)
+    if (m < 0.70710678118654752440) { m = __dmul_rn(m, 2.0); k -= 1; }
+    const dd z = dd_div({__dsub_rn(m, 1.0), 0.0}, {__dadd_rn(m, 1.0), 0.0});  // m -+ 1 exact
+    const dd z2 = dd_mul(z, z);
+    dd s = {0.0, 0.0};
+    for (int i = 24; i >= 0; i--) s = dd_add(dd_mul(s, z2), dd_div({1.0, 0.0}, {(double)(2 * i + 1), 0.0}));
+    const dd lnm = dd_mul(dd_mul(s, z), {2.0, 0.0});
+    const dd LN2 = {6.93147180559945286227e-01, 2.31904681384629955842e-17};
+    const dd r = dd_add(dd_mul({(double)k, 0.0}, LN2), lnm);
+    return __dadd_rn(r.hi, r.lo);
+}
 
 __global__ void k_raw_weight(const uint32_t *co, const uint32_t *ci, uint64_t n, double *raw) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)

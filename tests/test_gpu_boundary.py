@@ -26,30 +26,33 @@ def P():
 def _host_ln(tmp):
     so = os.path.join(tmp, "libln.so")
     subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
-                           os.path.join(ROOT, "tests", "c", "ln_table.c"), "-o", so, "-lm"])
+                           os.path.join(ROOT, "tests", "c", "ln_table.c"), "-o", so, "-lquadmath", "-lm"])
     lib = C.CDLL(so)
     lib.host_ln_table.argtypes = [C.c_uint64, C.c_uint64, C.c_void_p]
     lib.host_ln_table.restype = None
     return lib
 
 
-def test_coarsening_ln_matches_libm_exhaustively(P, tmp_path):
-    # P:193 takes ln of the integer cA + cB.  Both counts are at most the node's degree, so the
-    # domain is [2, 2 * max degree]; [1, 2^27) covers every graph with max degree < 2^26 (67M;
-    # config 4/5's largest hub has ~2M).  Device and host values must agree bit for bit: the
-    # min-max rescale and Eq. 1-3 are correctly rounded, so this makes the activations exact.
+def test_coarsening_ln_correctly_rounded_exhaustively(P, tmp_path):
+    # P:193 takes ln of the integer cA + cB; R31 fixes its fp64 value as the correctly rounded
+    # one.  Both counts are at most the node's degree, so the domain is [2, 2 * max degree];
+    # [1, 2^27) covers every graph with max degree < 2^26 (67M; config 4/5's largest hub has
+    # ~2M).  The device's double-double ln must equal binary128 logq rounded once, bit for bit
+    # (CUDA's own log() differs on ~1e-5 of these integers, glibc's log on ~3e-5).
     lib = _host_ln(str(tmp_path))
     chunk = 1 << 24
     host = np.empty(chunk, np.float64)
-    bad = 0
     for n0 in range(1, 1 << 27, chunk):
         cnt = min(chunk, (1 << 27) - n0)
         dev = P.riki.debug_ln_table(n0, cnt)
         lib.host_ln_table(n0, cnt, host.ctypes.data)
         d = np.nonzero(dev.view(np.uint64) != host[:cnt].view(np.uint64))[0]
-        bad += len(d)
         assert len(d) == 0, f"ln differs at n = {(n0 + d[:5]).tolist()}"
-    assert bad == 0
+    # where glibc's log is not correctly rounded the device still is (exact decimal reference)
+    from decimal import Decimal, getcontext
+    getcontext().prec = 60
+    for n in (9170, 136837, 141614, 147674, 277862, 330034, 351497):
+        assert P.riki.debug_ln_table(n, 1)[0] == float(Decimal(n).ln())
 
 
 def _c1_graph(P):

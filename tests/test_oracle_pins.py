@@ -52,6 +52,19 @@ def test_coarsen_bound_roundtrip_and_invariants():
     assert (np.diff(a.astype(int)) >= 0).all()
 
 
+def test_ln_count_correctly_rounded():
+    # R31: P:193's log of an integer count is the fp64 value nearest to ln n.  Pinned by an
+    # exact decimal evaluation (60 digits, then Python's correctly rounded str -> float), on
+    # random integers and on integers where the C library's log is off by one ulp
+    from decimal import Decimal, getcontext
+    getcontext().prec = 60
+    rng = np.random.default_rng(31)
+    ns = [1, 2, 3, 10, 9170, 136837, 141614, 147674, 277862, 278555, 330034, 351497, 372772, 394915]
+    ns += [int(x) for x in rng.integers(2, 1 << 32, 3000)]
+    for n in ns:
+        assert O.ln_count(n) == float(Decimal(n).ln()), n
+
+
 def test_fine_weights_hand_fixtures():
     # lone edge -> log 2; 3 same-label out-edges into single-in targets -> log 4;
     # uniform graph -> all 0 (degenerate rescale, R2).
