@@ -63,7 +63,9 @@ enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_PULLNODES, P_PUL
             P_R_BUILDS = 8, P_R_BEDGES, P_R_BCYC, P_R_WAITS, P_R_WCYC, P_R_CANDS, P_R_CANDCYC, P_R_CANDMAX, P_R_BMAX,
             P_R_ITEMS, P_R_WARPMAX, P_R_H0,  // P_R_H0..+5: candidate-time histogram
             // expansion item diagnostics (compiled in with -DEXP_STATS=1)
-            P_X_DUP = 24, P_X_BLOCKED, P_X_IDLE, P_X_WORK, P_NPROF = 32 };
+            P_X_DUP = 24, P_X_BLOCKED, P_X_IDLE, P_X_WORK,
+            // recovery tier diagnostics (REC_STATS): candidates per tier, big-tier sizes
+            P_R_T1 = 32, P_R_T2, P_R_T2NODES, P_R_T2EDGES, P_R_T2MAXE, P_R_T1RPG, P_R_T2RPG, P_NPROF = 40 };
 #ifndef EXP_STATS
 #define EXP_STATS 0
 #endif
@@ -1748,6 +1750,9 @@ template <class RowC, int TIER> __global__ void __launch_bounds__(tier_threads<T
             uint2 x = w.ovf[item];
             bool ovf = false;
             extract_cg<GroupCTA, RowC>(G_, g, w, x.x, x.y, b, sh, &ovf);
+#if REC_STATS
+            if (G_.rank() == 0) atomicAdd(&w.prof[P_R_T1], 1ull);
+#endif
             if (ovf && G_.rank() == 0) { sh.dirty = 1; push_overflow(w, 1, x); }
             G_.sync();
             ex_reset(G_, b, sh);
@@ -1766,6 +1771,9 @@ template <class RowC> __global__ void __launch_bounds__(256) k_extract_cg_big(Gr
         uint2 sc = w.ovf2[i];
         bool ovf = false;
         extract_cg<GroupCTA, RowC>(G_, g, w, sc.x, sc.y, b, sh, &ovf);
+#if REC_STATS
+        if (G_.rank() == 0) atomicAdd(&w.prof[P_R_T2], 1ull);
+#endif
         if (ovf && G_.rank() == 0) { sh.dirty = 1; atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT); }
         G_.sync();
         ex_reset(G_, b, sh);
@@ -1981,6 +1989,9 @@ template <class RowM, int TIER> __global__ void __launch_bounds__(tier_threads<T
             uint2 sc = w.ovf[i];
             bool ovf = false;
             extract_rpg<GroupCTA, RowM>(G_, g, w, sc.x, sc.y, b, sh, &ovf);
+#if REC_STATS
+            if (G_.rank() == 0) atomicAdd(&w.prof[P_R_T1RPG], 1ull);
+#endif
             if (ovf && G_.rank() == 0) { sh.dirty = 1; push_overflow(w, 1, sc); }
             G_.sync();
             ex_reset(G_, b, sh);
@@ -1999,6 +2010,14 @@ template <class RowM> __global__ void __launch_bounds__(256) k_extract_rpg_big(G
         uint2 sc = w.ovf2[i];
         bool ovf = false;
         extract_rpg<GroupCTA, RowM>(G_, g, w, sc.x, sc.y, b, sh, &ovf);
+#if REC_STATS
+        if (G_.rank() == 0) {
+            atomicAdd(&w.prof[P_R_T2RPG], 1ull);
+            atomicAdd(&w.prof[P_R_T2NODES], (unsigned long long)sh.nu);
+            atomicAdd(&w.prof[P_R_T2EDGES], (unsigned long long)sh.nedges);
+            atomicMax(&w.prof[P_R_T2MAXE], (unsigned long long)sh.nedges);
+        }
+#endif
         if (ovf && G_.rank() == 0) { sh.dirty = 1; atomicOr(&w.st[sc.x].err, (uint32_t)E_EXTRACT); }
         G_.sync();
         ex_reset(G_, b, sh);
@@ -3135,6 +3154,9 @@ void add_stats(riki_graph *g, Workspace *ws, Launch &L, uint32_t nq) {
             prof[P_R_BUILDS], prof[P_R_BEDGES], prof[P_R_BMAX], prof[P_R_BCYC], prof[P_R_WAITS], prof[P_R_WCYC],
             prof[P_R_ITEMS], prof[P_R_CANDS], prof[P_R_CANDCYC], prof[P_R_CANDMAX], prof[P_R_WARPMAX],
             prof[P_R_H0], prof[P_R_H0 + 1], prof[P_R_H0 + 2], prof[P_R_H0 + 3], prof[P_R_H0 + 4], prof[P_R_H0 + 5]);
+    fprintf(stderr, "[riki-rec] tiers: cg t1 %llu big %llu | rpg t1 %llu big %llu (nodes %llu edges %llu max edges %llu)\n",
+            prof[P_R_T1], prof[P_R_T2], prof[P_R_T1RPG], prof[P_R_T2RPG], prof[P_R_T2NODES], prof[P_R_T2EDGES],
+            prof[P_R_T2MAXE]);
 #endif
     uint64_t rb = ws->last_rb[0];  // bytes per H row (approximation when phases differ)
     g->stats.expand_launches += L.expand_launches;

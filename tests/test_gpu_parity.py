@@ -502,30 +502,3 @@ def test_joint_traversal_c2_sampled(P):
     for i in (0, 99, 199):
         _cmp_results(res[i], _oracle_run(og, kg.posting, qs.central[i], qs.marginal[i], qs.k, qs.depth,
                                          want_matrices=False))
-
-
-@pytest.mark.slow
-@pytest.mark.skipif(not __import__("os").environ.get("RIKI_TEST_C4"), reason="config 4 (30M nodes / 150M edges) takes "
-                    "~10 min of CPU for generation + oracle; set RIKI_TEST_C4=1 (log kept in profiles/)")
-def test_search_c4_wikidata_scale_depth_sweep(P):
-    import time
-    t0 = time.time()
-    kg = synth.make_kg(4)
-    qs = synth.config_queries(kg, 4, 200)  # the bench's batch: 200 x 30M > 2^32 -> 64-bit item loop
-    g = P.Graph(kg.n_nodes, kg.src, kg.dst, kg.label_class, kg.term_ptr, kg.postings)
-    g.set_label_weights(0.5, kg.avg_hops)
-    a = O.coarsen_all(O.fine_weights(kg.n_nodes, kg.src, kg.dst, kg.label_class), 0.5, kg.avg_hops)
-    assert (g.activation_levels() == a).all()
-    og = O.Graph(kg.n_nodes, kg.src, kg.dst, a)
-    print(f"c4 setup {time.time() - t0:.0f}s")
-    for depth in (4, 8, 20):
-        res = g.search_batch(qs.central, qs.marginal, qs.k, depth)
-        for i in (0, 1, 177):
-            t = time.time()
-            ro = _oracle_run(og, kg.posting, qs.central[i], qs.marginal[i], qs.k, depth, want_matrices=False)
-            _cmp_results(res[i], ro)
-            assert res[i].stats["relax_marginal"] == ro.relax_m and res[i].stats["L_marginal"] == ro.Lm
-            print(f"c4 depth {depth} query {i}: {len(ro.rpgs)} RPGs, oracle {time.time() - t:.1f}s, identical")
-    H, blk, rel, L = g.hitting_levels(np.array(qs.central[0], np.uint32), 20, 1)
-    Ho, bo, Lo, relo = O.phase(og, [kg.posting(t) for t in qs.central[0]], 20, 1)
-    assert (H == Ho).all() and (blk == bo).all() and rel == relo
