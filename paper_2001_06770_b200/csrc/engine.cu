@@ -16,6 +16,8 @@
 // (identification at level l+1, R10).  Lock-free by Theorem lockfree.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_segmented_radix_sort.cuh>
+
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
@@ -1253,10 +1255,22 @@ __device__ void cta_sort_u64(uint64_t *keys, uint32_t n, uint64_t *smem, uint32_
     }
 }
 
+// Segments of the candidate-key sort: slot s's keys CK(s)[0, ncand) (empty for slots that
+// are inactive or failed).
+// Offsets are relative to the first slot of s's sort group (G slots: int-sized item counts).
+__global__ void k_cand_segments(WsDev w, int *begin, int *end, uint32_t G) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= w.nslots) return;
+    const SlotState &st = w.st[s];
+    begin[s] = (int)((size_t)(s % G) * w.capc);
+    end[s] = begin[s] + ((st.active && !st.err) ? (int)min(st.ncand, w.capc) : 0);
+}
+
 // Candidate CGs: all CGs identified by the terminating level, ties kept (R13), ordered
-// by (S^c, v); beam_mode 1 truncates to the first w.
-__global__ void k_cand_sort(GraphDev g, WsDev w) {
-    extern __shared__ uint64_t sm64[];
+// by (S^c, v); beam_mode 1 truncates to the first w.  `sorted` holds every slot's keys
+// already sorted (segmented radix sort of CK, keys (S^c << 32 | caller id)); they are copied
+// back to CK(s) while the candidate records are built.
+__global__ void k_cand_sort(GraphDev g, WsDev w, const uint64_t *sorted) {
     uint32_t s = blockIdx.x;
     SlotState &st = w.st[s];
     if (!st.active || st.err) {
@@ -1264,13 +1278,14 @@ __global__ void k_cand_sort(GraphDev g, WsDev w) {
         return;
     }
     uint32_t n = min(st.ncand, w.capc);
-    cta_sort_u64(w.CK(s), n, sm64, 4096);
+    const uint64_t *src = sorted + (size_t)s * w.capc;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) w.CK(s)[i] = src[i];
     // beam_mode 1 with the tie-break (R29) truncates by (S^c, W(CG), v) after recovery
     const bool beam_tie = st.beam_mode == 1 && st.tie_break;
     uint32_t kept = st.beam_mode == 1 && !beam_tie ? min(n, st.w) : n;
     uint32_t nex = st.T[1] == 0 && !st.tie_break ? min(kept, st.k) : kept;
     for (uint32_t i = threadIdx.x; i < nex; i += blockDim.x) {
-        uint64_t key = w.CK(s)[i];
+        uint64_t key = src[i];
         Cand c;
         memset(&c, 0, sizeof(c));
         c.ext = (uint32_t)key;
@@ -1580,6 +1595,13 @@ template <class G> __device__ __forceinline__ void ex_init(const G &G_, const Ex
     G_.sync();
     ex_reset(G_, b, sh);
 }
+// Global-scratch tier: its V-sized tables are EMPTY on entry (filled with 0xFF when the
+// workspace is allocated, and every use leaves them clean: ex_reset clears the inserted
+// entries, or everything after an overflow), so no O(V) clear per launch.
+template <class G> __device__ __forceinline__ void ex_init_clean(const G &G_, ExShared &sh) {
+    if (G_.rank() == 0) { sh.nu = 0; sh.nk = 0; sh.nedges = 0; sh.ovf = 0; sh.dirty = 0; }
+    G_.sync();
+}
 
 // CG of candidate (s, c): union over central keywords of the recovered SP(c_j, v~).
 // Writes nodes, edge ids and V_C (nodes holding a central keyword) to the arena.
@@ -1766,7 +1788,7 @@ template <class RowC> __global__ void __launch_bounds__(256) k_extract_cg_big(Gr
     uint32_t n = min(w.ctr[C_NOVF2], w.ovf_cap);
     if (blockIdx.x >= n) return;
     ExBuf b = big_buf(w, blockIdx.x, sh);
-    ex_init(G_, b, sh);
+    ex_init_clean(G_, sh);
     for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
         uint2 sc = w.ovf2[i];
         bool ovf = false;
@@ -2005,7 +2027,7 @@ template <class RowM> __global__ void __launch_bounds__(256) k_extract_rpg_big(G
     uint32_t n = min(w.ctr[C_NOVF2], w.ovf_cap);
     if (blockIdx.x >= n) return;
     ExBuf b = big_buf(w, blockIdx.x, sh);
-    ex_init(G_, b, sh);
+    ex_init_clean(G_, sh);
     for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
         uint2 sc = w.ovf2[i];
         bool ovf = false;
@@ -2356,7 +2378,11 @@ struct Workspace {
     uint32_t *q = nullptr, *bm = nullptr, *jq = nullptr, *jbm = nullptr, *coffs = nullptr, *pslots = nullptr, *ctr = nullptr, *arena = nullptr,
              *big = nullptr, *resid = nullptr, *out = nullptr;
     uint4 *mtab = nullptr;
-    uint64_t *ck = nullptr;
+    uint64_t *ck = nullptr, *ck2 = nullptr;  // candidate keys; ck2 = sorted copy (segmented radix sort)
+    int *seg_b = nullptr, *seg_e = nullptr;
+    void *sort_tmp = nullptr;
+    size_t sort_tmp_bytes = 0;
+    uint32_t sort_group = 1;  // slots per segmented-sort call (item counts stay int-sized)
     Cand *cd = nullptr;
     u128 *rk = nullptr;
     SlotState *st = nullptr;
@@ -2494,6 +2520,14 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     ws->jbm = ws->alloc<uint32_t>(2 * (size_t)ws->W);
     CUDA_TRY(cudaMemset(ws->jbm, 0, 2 * (size_t)ws->W * 4));
     ws->ck = ws->alloc<uint64_t>(S * c.capc);
+    ws->ck2 = ws->alloc<uint64_t>(S * c.capc);
+    ws->seg_b = ws->alloc<int>(S + 1);
+    ws->seg_e = ws->alloc<int>(S + 1);
+    ws->sort_group = (uint32_t)std::max<size_t>(1, std::min<size_t>(S, (1ull << 30) / c.capc));
+    CUDA_TRY(cub::DeviceSegmentedRadixSort::SortKeys(nullptr, ws->sort_tmp_bytes, (const unsigned long long *)ws->ck,
+                                                     (unsigned long long *)ws->ck2, (int)(ws->sort_group * (size_t)c.capc),
+                                                     (int)ws->sort_group, ws->seg_b, ws->seg_e, 0, 40));
+    ws->sort_tmp = ws->alloc<uint8_t>(ws->sort_tmp_bytes);
     ws->cd = ws->alloc<Cand>(S * c.capc);
     ws->rk = ws->alloc<u128>(S * c.capc);
     ws->st = ws->alloc<SlotState>(S);
@@ -2516,6 +2550,7 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     ws->big_words = cu * 3 + 4ull * (V + 1) + cu / 4 + (V + 1) / 4 + 32 + std::max<uint64_t>(std::min<uint64_t>(g->E, 1ull << 26), 1u << 20);
     ws->mtab = ws->alloc<uint4>(S * 16 * MAPCAP);
     ws->big = ws->alloc<uint32_t>(ws->big_words * ws->big_ctas);
+    CUDA_TRY(cudaMemset(ws->big, 0xFF, ws->big_words * ws->big_ctas * 4));  // EMPTY tables (ex_init_clean)
     ws->hdr = ws->alloc<OutHdr>(S * c.kmax);
     ws->resid = ws->alloc<uint32_t>(S * c.kmax);
     ws->tie = ws->alloc<uint2>(S * c.capc);
@@ -2889,8 +2924,23 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     run_phase<RowC, RowC>(L, gd, ws, 0, -1, depth + 1, 0);
     L.mark(0);
     // ---- candidate CGs + recovery
-    k_cand_sort<<<wd.nslots, 1024, 4096 * 8, s>>>(gd, wd);
-    L.check(__LINE__);
+    {   // (S^c, v) order of every slot's candidates: one segmented radix sort over the slots
+        // (keys: level < 2^8 above a 32-bit caller id), then the candidate records
+        const uint32_t G = ws->sort_group;
+        k_cand_segments<<<(wd.nslots + 127) / 128, 128, 0, s>>>(wd, ws->seg_b, ws->seg_e, G);
+        L.check(__LINE__);
+        for (uint32_t s0 = 0; s0 < wd.nslots; s0 += G) {
+            const uint32_t ng = std::min(G, wd.nslots - s0);
+            size_t tb = ws->sort_tmp_bytes;
+            CUDA_TRY(cub::DeviceSegmentedRadixSort::SortKeys(
+                ws->sort_tmp, tb, (const unsigned long long *)ws->ck + (size_t)s0 * ws->capc,
+                (unsigned long long *)ws->ck2 + (size_t)s0 * ws->capc, (int)((size_t)ng * ws->capc), (int)ng,
+                ws->seg_b + s0, ws->seg_e + s0, 0, 40, s));
+            L.launches += 2;
+        }
+        k_cand_sort<<<wd.nslots, 1024, 0, s>>>(gd, wd, ws->ck2);
+        L.check(__LINE__);
+    }
     k_scan_cands<<<1, MAX_SLOTS, 0, s>>>(wd);
     L.check(__LINE__);
     CUDA_TRY(cudaMemcpyAsync(ws->h_ctr, ws->ctr, C_NCTR * 4, cudaMemcpyDeviceToHost, s));

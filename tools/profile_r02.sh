@@ -9,6 +9,8 @@ T=$1; C=${2:-5}
 export PATH=/usr/local/cuda/bin:$PATH
 mkdir -p gpurun_out
 B="python bench.py --config $C --steps 1 --warmup 1 --quick --no-cpu"
+# plain launches (kernels inside the CUDA-graph level loops are not listed one by one)
+export RIKI_NO_GRAPHS=1
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -c 6000 --csv --log-file gpurun_out/${T}_c${C}_all_dram.csv $B > gpurun_out/${T}_c${C}_dram.log 2>&1
 echo dram_done
@@ -28,10 +30,10 @@ for r in rows:
 exp = [i for i in ids if name[i].startswith("void <unnamed>::k_expand") or "k_expand<" in name[i]]
 light = [i for i in exp if "k_expand_heavy" not in name[i]]
 best = max(light, key=lambda i: dur.get(i, 0))
-print(light.index(best))
+print(exp.index(best))
 PY
 )
 echo "full capture: k_expand launch ordinal $SKIP"
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"k_expand<" -s $SKIP -c 1 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_expand -s $SKIP -c 1 \
     -o gpurun_out/${T}_c${C}_expand_full $B > gpurun_out/${T}_c${C}_full.log 2>&1
 echo profile_done
