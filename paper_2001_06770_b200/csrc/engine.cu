@@ -151,6 +151,9 @@ struct WsDev {
     unsigned long long *arena_used, arena_cap;
     uint2 *newatt, *ovf, *ovf2;
     uint32_t ovf_cap;
+    uint8_t *cst;  // per (slot, candidate): 0 unattached, 1 attached and pending RPG recovery,
+                   // 2 recovered, 3 excluded from the top-k (never recovered); bounded mode
+    uint32_t bounded;  // run 2 recovers RPGs in waves, only for candidates that can enter the top-k
     uint32_t *big;
     unsigned long long big_words;
     uint4 *mtab;
@@ -171,6 +174,7 @@ struct WsDev {
     __device__ __forceinline__ uint64_t *CK(uint32_t s) const { return ck + (size_t)s * capc; }
     __device__ __forceinline__ Cand *CD(uint32_t s) const { return cd + (size_t)s * capc; }
     __device__ __forceinline__ u128 *RK(uint32_t s) const { return rk + (size_t)s * capc; }
+    __device__ __forceinline__ uint8_t *CST(uint32_t s) const { return cst + (size_t)s * capc; }
 };
 
 template <class RowT> __device__ __forceinline__ RowT used_mask(uint32_t T) {
@@ -587,6 +591,12 @@ __device__ __forceinline__ void gate_range_in(const GraphDev &g, const uint4 &d,
 #ifndef EXP_MINB
 #define EXP_MINB 8
 #endif
+// 64-bit rows (5-8 keywords) need more registers: at 8 blocks (32 registers) the u64 loop
+// spills to local memory in its hot path (ncu r02e: LDL + short-scoreboard stalls).
+#ifndef EXP_MINB64
+#define EXP_MINB64 6
+#endif
+template <class RowT> struct ExpMinB { static constexpr int v = sizeof(RowT) == 8 ? EXP_MINB64 : EXP_MINB; };
 // Item fields of one non-empty active range, compacted per warp in shared memory for the
 // edge walk: edge index e = delta + idx, and edges with idx >= thr also carry the old columns.
 template <class RowT> struct alignas(16) OwnF {
@@ -598,7 +608,7 @@ template <class RowT> struct alignas(16) OwnF {
 // (slots x queue capacity >= 2^32, e.g. 200 queries on a 30M-node graph); the common
 // case keeps the 32-bit loop.
 template <class RowT, bool WIDE>
-__global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, int ph, uint32_t l_arg) {
+__global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, WsDev w, int ph, uint32_t l_arg) {
     typedef Row<RowT> R;
     const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
     typedef typename std::conditional<WIDE, unsigned long long, uint32_t>::type IdxT;
@@ -787,7 +797,7 @@ __global__ void __launch_bounds__(256, EXP_MINB) k_expand(GraphDev g, WsDev w, i
 #ifndef HEAVY_UNROLL
 #define HEAVY_UNROLL 2
 #endif
-template <class RowT> __global__ void __launch_bounds__(256, EXP_MINB) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l_arg) {
+template <class RowT> __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l_arg) {
     const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
     typedef Row<RowT> R;
     const uint32_t lane = lane_id();
@@ -1294,6 +1304,7 @@ __global__ void k_cand_sort(GraphDev g, WsDev w, const uint64_t *sorted) {
         c.sr = (double)c.sc;
         c.ptc = 1;
         w.CD(s)[i] = c;
+        w.CST(s)[i] = 0;
     }
     if (threadIdx.x == 0) {
         st.ncand_kept = kept;
@@ -1831,8 +1842,12 @@ template <class RowM> __global__ void __launch_bounds__(256) k_attach(WsDev w) {
             for (uint32_t i = 0; i < RIKI_MAX_TERMS; i++) cd.mdist[i] = i < st.T[1] ? R::byte(mn, i) : 0;
             cd.attached = 1;
             atomicAdd(&st.n_attached, 1u);
-            uint32_t p = atomicAdd(&w.ctr[C_NNEWATT], 1u);
-            w.newatt[p] = make_uint2(s, c);
+            if (w.bounded) {
+                w.CST(s)[c] = 1;  // its RPG is recovered by a k_rpg_select wave if it can enter the top-k
+            } else {
+                uint32_t p = atomicAdd(&w.ctr[C_NNEWATT], 1u);
+                w.newatt[p] = make_uint2(s, c);
+            }
         }
     }
 }
@@ -2063,6 +2078,64 @@ __device__ void cta_sort_u128(u128 *keys, uint32_t n, u128 *smem, uint32_t smem_
         __syncthreads();
     } else {
         cta_bitonic_sort(keys, n);
+    }
+}
+
+// Bounded RPG recovery (run 2, wave `last` = 0 or 1).  The answer is the k smallest keys
+// (S^r, S^c, v) of the PTC-passing RPGs, and the k-th key of the results found so far (R)
+// only decreases, so a candidate whose key is not below it can never enter the top-k: its
+// RPG is not recovered (R21's argument for attached candidates).  The candidates attached at
+// level l all have S^m = l, so their key order is their (S^c, v) order = candidate order.
+// Wave 0 takes, per slot, the first k pending candidates (in order) that can still enter;
+// wave 1 (after their PTC) takes every remaining one that still can.  One CTA per slot; the
+// selected (slot, candidate) pairs go to the recovery tiers through the newatt list.  With the
+// weight-sum tie-break (R29) every attached candidate is recovered (its key needs W).
+__global__ void __launch_bounds__(256) k_rpg_select(WsDev w, uint32_t l_arg, int last) {
+    const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
+    extern __shared__ __align__(16) u128 sm128[];
+    __shared__ uint32_t taken, wcount[8];
+    const uint32_t s = blockIdx.x;
+    SlotState &st = w.st[s];
+    if (!st.in_phase) return;
+    uint32_t nR = min(st.nR, w.capc);
+    if (last && nR != st.nR_sorted) {  // R gained the previous wave's results
+        cta_sort_u128(w.RK(s), nR, sm128, U128_SORT_KEYS);
+        if (threadIdx.x == 0) st.nR_sorted = nR;
+    }
+    const bool full = nR >= st.k && !st.tie_break;
+    const u128 kth = full ? w.RK(s)[st.k - 1] : (u128)0;
+    const uint32_t limit = last || st.tie_break ? 0xFFFFFFFFu : st.k;
+    if (threadIdx.x == 0) taken = 0;
+    __syncthreads();
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint8_t *cst = w.CST(s);
+    for (uint32_t c0 = 0; c0 < st.n_extract; c0 += blockDim.x) {
+        const uint32_t c = c0 + threadIdx.x;
+        bool pend = false;
+        if (c < st.n_extract && cst[c] == 1) {
+            const Cand &cd = w.CD(s)[c];
+            if (cd.sm != l || (full && !(rkey(cd.sr, cd.sc, cd.ext) < kth))) cst[c] = 3;  // can never enter
+            else pend = true;
+        }
+        const uint32_t b = __ballot_sync(FULLMASK, pend);
+        if (lane == 0) wcount[wid] = __popc(b);
+        __syncthreads();
+        uint32_t before = taken;
+        for (uint32_t i = 0; i < wid; i++) before += wcount[i];
+        const uint32_t rank = before + __popc(b & lanemask_lt());
+        if (pend && rank < limit) {
+            cst[c] = 2;
+            const uint32_t p = atomicAdd(&w.ctr[C_NNEWATT], 1u);
+            w.newatt[p] = make_uint2(s, c);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+            for (uint32_t i = 0; i < blockDim.x / 32; i++) t += wcount[i];
+            taken += t;
+        }
+        __syncthreads();
+        if (taken >= limit) break;
     }
 }
 
@@ -2389,6 +2462,8 @@ struct Workspace {
     uint4 *heavy = nullptr;
     unsigned long long *prof = nullptr, *arena_used = nullptr, *out_used = nullptr;
     uint2 *newatt = nullptr, *ovf = nullptr, *ovf2 = nullptr, *tie = nullptr;
+    uint8_t *cst = nullptr;
+    uint32_t bounded = 0;
     OutHdr *hdr = nullptr;
     uint32_t *h_ctr = nullptr;  // pinned
     uint64_t bytes = 0;
@@ -2453,7 +2528,7 @@ struct Workspace {
         d.q = q; d.qcap = qcap; d.bm = bm; d.jq = jq; d.jbm = jbm; d.ck = ck; d.cd = cd; d.rk = rk; d.offs = offs; d.coffs = coffs; d.pslots = pslots; d.track_reached = track_reached;
         d.heavy = heavy; d.heavy_cap = heavy_cap; d.ctr = ctr; d.prof = prof;
         d.arena = arena; d.arena_used = arena_used; d.arena_cap = arena_cap;
-        d.newatt = newatt; d.ovf = ovf; d.ovf2 = ovf2; d.ovf_cap = ovf_cap;
+        d.newatt = newatt; d.ovf = ovf; d.ovf2 = ovf2; d.ovf_cap = ovf_cap; d.cst = cst; d.bounded = bounded;
         d.big = big; d.big_words = big_words; d.mtab = mtab;
         d.hdr = hdr; d.tie = tie; d.resid = resid; d.out = out; d.out_used = out_used; d.out_cap = out_cap;
         return d;
@@ -2542,6 +2617,7 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     ws->arena = ws->alloc<uint32_t>(c.arena);
     ws->arena_used = ws->alloc<unsigned long long>(1);
     ws->newatt = ws->alloc<uint2>(S * c.capc);
+    ws->cst = ws->alloc<uint8_t>(S * c.capc);
     ws->ovf_cap = (uint32_t)(S * c.capc);
     ws->ovf = ws->alloc<uint2>(ws->ovf_cap);
     ws->ovf2 = ws->alloc<uint2>(ws->ovf_cap);
@@ -2570,6 +2646,7 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
         SET_EX_ATTR(k_extract_rpg)
 #undef SET_EX_ATTR
         CUDA_TRY(cudaFuncSetAttribute(k_decide_m, cudaFuncAttributeMaxDynamicSharedMemorySize, U128_SORT_KEYS * 16));
+        CUDA_TRY(cudaFuncSetAttribute(k_rpg_select, cudaFuncAttributeMaxDynamicSharedMemorySize, U128_SORT_KEYS * 16));
         CUDA_TRY(cudaFuncSetAttribute(k_final_select, cudaFuncAttributeMaxDynamicSharedMemorySize, U128_SORT_KEYS * 16));
         CUDA_TRY(cudaFuncSetAttribute(k_tie_select, cudaFuncAttributeMaxDynamicSharedMemorySize, U128_SORT_KEYS * 16));
         CUDA_TRY(cudaFuncSetAttribute(k_beam_tie, cudaFuncAttributeMaxDynamicSharedMemorySize, U128_SORT_KEYS * 16));
@@ -2714,12 +2791,25 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             if (total_cands) {
                 k_attach<RowT><<<attach_blocks, 256, 0, s>>>(wd);
                 L.check(__LINE__);
-                k_extract_rpg<RowT, 0><<<rpg0_blocks, tier_threads<0>(), smem_ex<0>(), s>>>(gd, wd);
-                L.check(__LINE__);
-                k_extract_rpg<RowT, 1><<<rpg1_blocks, 256, smem_ex<1>(), s>>>(gd, wd);
-                L.check(__LINE__);
-                k_extract_rpg_big<RowT><<<ws->big_ctas, 256, 0, s>>>(gd, wd);
-                L.check(__LINE__);
+                auto recover = [&]() {
+                    k_extract_rpg<RowT, 0><<<rpg0_blocks, tier_threads<0>(), smem_ex<0>(), s>>>(gd, wd);
+                    L.check(__LINE__);
+                    k_extract_rpg<RowT, 1><<<rpg1_blocks, 256, smem_ex<1>(), s>>>(gd, wd);
+                    L.check(__LINE__);
+                    k_extract_rpg_big<RowT><<<ws->big_ctas, 256, 0, s>>>(gd, wd);
+                    L.check(__LINE__);
+                };
+                if (wd.bounded) {  // two waves of bounded RPG recovery (k_rpg_select)
+                    for (int wave = 0; wave < 2; wave++) {
+                        k_reset_level_ctrs<<<1, 1, 0, s>>>(wd);
+                        L.check(__LINE__);
+                        k_rpg_select<<<wd.nslots, 256, U128_SORT_KEYS * 16, s>>>(wd, l, wave);
+                        L.check(__LINE__);
+                        recover();
+                    }
+                } else {
+                    recover();
+                }
             }
             k_decide_m<<<wd.nslots, 256, U128_SORT_KEYS * 16, s>>>(wd, l);
             L.check(__LINE__);
@@ -2966,6 +3056,7 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     if (L.g->profiling) CUDA_TRY(cudaStreamSynchronize(s));
     L.mark(1);
     // ---- run 2: marginal keywords
+    ws->bounded = getenv("RIKI_EAGER_RPG") ? 0 : 1;  // RIKI_EAGER_RPG=1 recovers every attached RPG (A/B, tests)
     run_phase<RowM, RowC>(L, gd, ws, 1, -1, depth + 1, total_cands);
     L.mark(2);
     // ---- top-k and packing

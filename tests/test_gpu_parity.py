@@ -243,7 +243,40 @@ def test_search_random_small(P, seed):
         assert r.candidates == [(c.sc, c.v) for c in ro.candidates]
         assert r.stats["L_central"] == ro.Lc and r.stats["L_marginal"] == ro.Lm
         assert r.stats["relax_central"] == ro.relax_c and r.stats["relax_marginal"] == ro.relax_m
-        assert r.stats["n_attached"] == ro.n_attached and r.stats["n_ptc_fail"] == ro.n_ptc_fail
+        # the GPU recovers an attached candidate's RPG (and checks its PTC) only if the candidate
+        # can still enter the top-k (bounded recovery); the oracle checks every attached one
+        assert r.stats["n_attached"] == ro.n_attached and r.stats["n_ptc_fail"] <= ro.n_ptc_fail
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_bounded_rpg_recovery_equals_eager(P, seed, monkeypatch):
+    # bounded recovery (only candidates that can still enter the top-k get their RPG and PTC)
+    # returns exactly what eager recovery of every attached candidate returns; eager recovery
+    # also reproduces the oracle's PTC-failure count
+    rng = np.random.default_rng(15000 + seed)
+    V, src, dst, act, _ = random_instance(rng, 20, 120, deg=2.6, amax=3)
+    nterm = 8
+    post = [np.unique(rng.integers(0, V, int(rng.integers(1, 5)))).astype(np.uint32) for _ in range(nterm)]
+    g = _dev_graph(P, V, src, dst, act, post)
+    og = O.Graph(V, src, dst, act)
+    Cs, Ms = [], []
+    for _ in range(16):
+        nc, nm = int(rng.integers(1, 3)), int(rng.integers(1, 4))
+        tt = rng.choice(nterm, nc + nm, replace=False)
+        Cs.append(tt[:nc].tolist())
+        Ms.append(tt[nc:].tolist())
+    k = int(rng.choice([1, 2, 4]))
+    kw = dict(ptc_mode=int(rng.choice([0, 1, 2])))
+    bounded = g.search_batch(Cs, Ms, k, 20, **kw)
+    monkeypatch.setenv("RIKI_EAGER_RPG", "1")
+    eager = g.search_batch(Cs, Ms, k, 20, **kw)
+    for i, (a, b) in enumerate(zip(bounded, eager)):
+        _cmp_results(a, b)
+        ro = _oracle_run(og, lambda t: post[t], Cs[i], Ms[i], k, 20, **kw)
+        _cmp_results(a, ro)
+        assert b.stats["n_ptc_fail"] == ro.n_ptc_fail and b.stats["n_attached"] == ro.n_attached
+        assert a.stats["n_ptc_fail"] <= b.stats["n_ptc_fail"]
+        assert (a.stats["L_marginal"], a.stats["relax_marginal"]) == (b.stats["L_marginal"], b.stats["relax_marginal"])
 
 
 def test_search_batch_c1_all_queries(P):
