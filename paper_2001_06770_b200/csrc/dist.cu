@@ -23,6 +23,8 @@ struct NcclApi {
     ncclResult_t (*get_unique_id)(ncclUniqueId *) = nullptr;
     ncclResult_t (*comm_init_rank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*all_gather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*all_reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
     ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
     const char *(*error_string)(ncclResult_t) = nullptr;
 };
@@ -43,9 +45,11 @@ const NcclApi &nccl() {
     api.get_unique_id = (decltype(api.get_unique_id))dlsym(h, "ncclGetUniqueId");
     api.comm_init_rank = (decltype(api.comm_init_rank))dlsym(h, "ncclCommInitRank");
     api.all_gather = (decltype(api.all_gather))dlsym(h, "ncclAllGather");
+    api.all_reduce = (decltype(api.all_reduce))dlsym(h, "ncclAllReduce");
     api.comm_destroy = (decltype(api.comm_destroy))dlsym(h, "ncclCommDestroy");
     api.error_string = (decltype(api.error_string))dlsym(h, "ncclGetErrorString");
-    if (!api.get_unique_id || !api.comm_init_rank || !api.all_gather || !api.comm_destroy || !api.error_string) {
+    if (!api.get_unique_id || !api.comm_init_rank || !api.all_gather || !api.all_reduce || !api.comm_destroy ||
+        !api.error_string) {
         api.all_gather = nullptr;
         RIKI_THROW(RIKI_ENCCL, "libnccl.so.2 lacks a required symbol");
     }
@@ -98,6 +102,7 @@ void dist_init(riki_graph *g, int nranks, int rank, const void *uid, int mode) {
     d->nranks = nranks;
     d->rank = rank;
     d->mode = mode;
+    d->push = getenv("RIKI_VP_PULL") == nullptr;  // push (fused exchange) unless the pull variant is asked for
     try {
         if (mode == 1) {
             d->simulated = uid == nullptr && nranks > 1;
@@ -157,9 +162,111 @@ void dist_allgather(riki_graph *g, uint32_t *x, size_t chunk_words, cudaStream_t
              "ncclAllGather");
 }
 
+// ---------------------------------------------------------------- vertex-partitioned push
+// Real multi-rank runs: every rank owns three slices (levels rotate through them mod 3) in
+// one allocation whose CUDA IPC handle is all-gathered once, so a rank's expansion kernel ORs
+// bits straight into the owner's slice over NVLink (peer stores, no staging).  Level t:
+//   push kernels (remote atomicOr into slice t mod 3)  ->  barrier (1-int all-reduce: every
+//   rank's kernel has finished, so its remote writes are complete)  ->  all-gather of the
+//   owned slices  ->  the owner clears slice (t + 2) mod 3 (written two levels on; any rank
+//   reaching that level has passed this level's all-gather, which follows this clear).
+// Simulated partitions and a single rank: one buffer [nranks][slice], cleared per level, and
+// the exchange is the identity.
+static void push_free(DistState *d) {
+    for (size_t r = 0; r < d->peer_bases.size(); r++)
+        if (d->peer_bases[r] && (int)r != d->rank) cudaIpcCloseMemHandle(d->peer_bases[r]);
+    d->peer_bases.clear();
+    if (d->d_slices) cudaFree(d->d_slices);
+    if (d->d_gather) cudaFree(d->d_gather);
+    if (d->d_xs) cudaFree(d->d_xs);
+    if (d->d_one) cudaFree(d->d_one);
+    d->d_slices = d->d_gather = nullptr;
+    d->d_xs = nullptr;
+    d->d_one = nullptr;
+    d->slice_words = 0;
+}
+
+static bool push_real(const DistState *d) { return d->comm != nullptr && d->nranks > 1; }
+
+void dist_push_setup(riki_graph *g, uint32_t slots) {
+    DistState *d = g->dist;
+    const size_t need = (size_t)std::max<uint32_t>(slots, 1) * 8 * d->wc;
+    if (need <= d->slice_words) return;
+    push_free(d);  // (collective in real mode: every rank grows at the same batch, same slots)
+    const int P = d->nranks;
+    auto alloc = [](void **p, size_t bytes, const char *what) {
+        if (cudaMalloc(p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            RIKI_THROW(RIKI_ENOMEM, std::string("vertex-partitioned push: ") + what);
+        }
+    };
+    std::vector<uint32_t *> xs(3 * (size_t)P);
+    if (!push_real(d)) {
+        alloc((void **)&d->d_slices, need * 4 * P, "slices");
+        CUDA_TRY(cudaMemset(d->d_slices, 0, need * 4 * P));
+        for (int k = 0; k < 3; k++)
+            for (int r = 0; r < P; r++) xs[(size_t)k * P + r] = d->d_slices + need * r;
+    } else {
+        alloc((void **)&d->d_slices, need * 4 * 3, "own slices");
+        CUDA_TRY(cudaMemset(d->d_slices, 0, need * 4 * 3));
+        alloc((void **)&d->d_gather, need * 4 * P, "gather buffer");
+        alloc((void **)&d->d_one, 4 * (size_t)P, "barrier");
+        // all-gather the 64-byte IPC handles of every rank's slices, then map the peers'
+        cudaIpcMemHandle_t h;
+        CUDA_TRY(cudaIpcGetMemHandle(&h, d->d_slices));
+        uint8_t *dh = nullptr;
+        alloc((void **)&dh, sizeof(h) * P, "handle exchange");
+        CUDA_TRY(cudaMemcpy(dh + sizeof(h) * d->rank, &h, sizeof(h), cudaMemcpyHostToDevice));
+        nccl_try(nccl().all_gather(dh + sizeof(h) * d->rank, dh, sizeof(h), ncclUint8, (ncclComm_t)d->comm, 0),
+                 "ncclAllGather (IPC handles)");
+        std::vector<cudaIpcMemHandle_t> hs(P);
+        CUDA_TRY(cudaMemcpy(hs.data(), dh, sizeof(h) * P, cudaMemcpyDeviceToHost));  // (syncs the NCCL call)
+        cudaFree(dh);
+        d->peer_bases.assign(P, nullptr);
+        for (int r = 0; r < P; r++) {
+            if (r == d->rank) { d->peer_bases[r] = d->d_slices; continue; }
+            CUDA_TRY(cudaIpcOpenMemHandle(&d->peer_bases[r], hs[r], cudaIpcMemLazyEnablePeerAccess));
+        }
+        for (int k = 0; k < 3; k++)
+            for (int r = 0; r < P; r++) xs[(size_t)k * P + r] = (uint32_t *)d->peer_bases[r] + need * k;
+    }
+    alloc((void **)&d->d_xs, xs.size() * sizeof(uint32_t *), "pointer table");
+    CUDA_TRY(cudaMemcpy(d->d_xs, xs.data(), xs.size() * sizeof(uint32_t *), cudaMemcpyHostToDevice));
+    d->slice_words = need;
+    d->t = 0;
+    d->used[0] = d->used[1] = d->used[2] = 0;
+}
+
+uint32_t *const *dist_push_targets(riki_graph *g) {
+    DistState *d = g->dist;
+    return d->d_xs + (push_real(d) ? (size_t)(d->t % 3) * d->nranks : 0);
+}
+
+const uint32_t *dist_push_exchange(riki_graph *g, size_t chunk, cudaStream_t s, size_t *stride) {
+    DistState *d = g->dist;
+    d->exchanges++;
+    d->exchanged_bytes += chunk * 4 * (size_t)d->nranks;
+    if (!push_real(d)) {
+        *stride = d->slice_words;
+        return d->d_slices;
+    }
+    const uint32_t k = (uint32_t)(d->t % 3);
+    nccl_try(nccl().all_reduce(d->d_one, d->d_one, 1, ncclInt32, ncclSum, (ncclComm_t)d->comm, s), "ncclAllReduce (barrier)");
+    nccl_try(nccl().all_gather(d->d_slices + d->slice_words * k, d->d_gather, chunk * 4, ncclUint8, (ncclComm_t)d->comm, s),
+             "ncclAllGather (bit planes)");
+    const uint32_t k2 = (uint32_t)((d->t + 2) % 3);
+    if (d->used[k2]) CUDA_TRY(cudaMemsetAsync(d->d_slices + d->slice_words * k2, 0, d->used[k2] * 4, s));
+    d->used[k2] = 0;
+    d->used[k] = chunk;
+    d->t++;
+    *stride = chunk;
+    return d->d_gather;
+}
+
 void dist_free(riki_graph *g) {
     DistState *d = g->dist;
     if (!d) return;
+    push_free(d);
     if (d->comm) nccl().comm_destroy((ncclComm_t)d->comm);
     if (d->d_bounds) cudaFree(d->d_bounds);
     if (d->d_x) cudaFree(d->d_x);

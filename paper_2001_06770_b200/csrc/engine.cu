@@ -141,7 +141,7 @@ struct WsDev {
     Cand *cd;
     u128 *rk;
     unsigned long long *offs;  // frontier-item prefix over the slots (k_expand<.., WIDE> beyond 2^32)
-    uint32_t *coffs, *pslots;
+    uint32_t *coffs, *pslots, *ppos;  // pull / VP slots: position -> slot, slot -> position
     uint32_t track_reached;  // direction-optimising mode: count new nodes per slot
     uint4 *heavy;
     uint32_t heavy_cap;
@@ -377,6 +377,7 @@ __global__ void k_plan(WsDev w, int ph, uint32_t l_arg, uint32_t pull_min) {
         npull += wpull[i];
     }
     if (pl) w.pslots[pbefore + __popc(pb & lanemask_lt())] = s;
+    if (s < w.nslots) w.ppos[s] = pl ? pbefore + __popc(pb & lanemask_lt()) : EMPTY;
     // block exclusive scan (Hillis-Steele) over MAX_SLOTS
     sc[s] = items;
     __syncthreads();
@@ -589,7 +590,7 @@ __device__ __forceinline__ void gate_range_in(const GraphDev &g, const uint4 &d,
 #define EXP_UNROLL 3
 #endif
 #ifndef EXP_MINB
-#define EXP_MINB 8
+#define EXP_MINB 7  // 7 resident blocks (36 registers): measured +2.7 % at C5, equal at C2 (r02f A/B)
 #endif
 // 64-bit rows (5-8 keywords) need more registers: at 8 blocks (32 registers) the u64 loop
 // spills to local memory in its hot path (ncu r02e: LDL + short-scoreboard stalls).
@@ -604,11 +605,39 @@ template <class RowT> struct alignas(16) OwnF {
     RowT nw, od;
 };
 
+// Vertex-partitioned push: a rank walks the out-edges of the
+// frontier nodes it owns, [lo, hi), and instead of writing H it ORs each newly reachable
+// cell (n, j) into bit plane j of n's OWNER's exchange slice -- xs[owner] is that slice, in
+// peer memory over NVLink in a real multi-rank run (the fused exchange), or a region of one
+// buffer for simulated partitions.  Slice layout [pull position][plane][wc words] over the
+// owner's range.  H stays as it was at the start of the level on every rank until
+// k_vp_apply_words writes the all-gathered planes.  The item phase (relaxation counts,
+// retained entries) runs on every rank for every item (`side`), so the frontier queues, the
+// counts and the candidates are replicated without another collective.
+struct VpPush {
+    uint32_t lo, hi;          // this launch's owned source range
+    uint32_t nranks, wc, side;
+    const uint32_t *bounds;   // nranks + 1 owner bounds (multiples of 32)
+    uint32_t *const *xs;      // per owner: its exchange slice for this level
+};
+template <class RowT>
+__device__ __forceinline__ void vp_mark(const VpPush &vp, uint32_t p, uint32_t n, RowT need) {
+    constexpr uint32_t RB = sizeof(RowT);
+    uint32_t r = 0;
+    while (r + 1 < vp.nranks && n >= __ldg(vp.bounds + r + 1)) r++;
+    const uint32_t i = n - __ldg(vp.bounds + r);
+    uint32_t *x = vp.xs[r] + (size_t)p * RB * vp.wc + (i >> 5);
+#pragma unroll
+    for (uint32_t j = 0; j < RB; j++)
+        if ((need >> (8 * j)) & 0xFF) atomicOr(x + (size_t)j * vp.wc, 1u << (i & 31));
+}
+
 // WIDE: 64-bit frontier-item indices, for batches whose level can exceed 2^32 items
 // (slots x queue capacity >= 2^32, e.g. 200 queries on a 30M-node graph); the common
-// case keeps the 32-bit loop.
-template <class RowT, bool WIDE>
-__global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, WsDev w, int ph, uint32_t l_arg) {
+// case keeps the 32-bit loop.  VPX: the vertex-partitioned push (VpPush above).
+template <class RowT, bool WIDE, bool VPX = false>
+__global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, WsDev w, int ph, uint32_t l_arg,
+                                                                  VpPush vp = VpPush{}) {
     typedef Row<RowT> R;
     const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
     typedef typename std::conditional<WIDE, unsigned long long, uint32_t>::type IdxT;
@@ -673,7 +702,12 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, Ws
 #if EXP_STATS
                     atomicAdd(&w.prof[len ? P_X_WORK : P_X_IDLE], 1ull);
 #endif
-                    if (info & 4) len = 0;  // pull slot: relaxed bottom-up by k_pull
+                    if (VPX) {
+                        if (f < vp.lo || f >= vp.hi) len = 0;  // another rank walks this node's edges
+                        if (!vp.side) { relaxn = 0; retain = false; }  // counted and retained once
+                    } else if (info & 4) {
+                        len = 0;  // pull slot: relaxed bottom-up by k_pull
+                    }
                     p_edges += len;
                     if (len > HEAVY) {
                         uint32_t nch = (len + CHUNK - 1) / CHUNK;
@@ -755,7 +789,10 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, Ws
 #pragma unroll
             for (int u = 0; u < EXP_UNROLL; u++) {
                 Relax<RowT> r{false, false, 0};
-                if (ev[u]) {
+                if (VPX) {  // H is read-only during a partitioned level: mark the owner's bit planes
+                    const RowT need = mask[u] & R::eq(hn[u], R::splat(0xFF));
+                    if (ev[u] && need) vp_mark<RowT>(vp, w.ppos[o_s[u]], n[u], need);
+                } else if (ev[u]) {
                     r = relax<RowT>(HV<RowT>{Hb + (size_t)(o_s[u] / HGRP) * V * HGRP + o_s[u] % HGRP, (uint32_t)HGRP},
                                     n[u], hn[u], mask[u], l);
                     p_cells += r.cells;
@@ -797,7 +834,9 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, Ws
 #ifndef HEAVY_UNROLL
 #define HEAVY_UNROLL 2
 #endif
-template <class RowT> __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l_arg) {
+template <class RowT, bool VPX = false>
+__global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l_arg,
+                                                                       VpPush vp = VpPush{}) {
     const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
     typedef Row<RowT> R;
     const uint32_t lane = lane_id();
@@ -838,8 +877,13 @@ template <class RowT> __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k
                 Relax<RowT> r{false, false, 0};
                 if (e0 + 32 * u + lane < h.w) {
                     RowT mask = newc | (a[u] == l ? oldc : (RowT)0);
-                    r = relax<RowT>(Hs, n[u], hn[u], mask, l);
-                    p_cells += r.cells;
+                    if (VPX) {
+                        const RowT need = mask & R::eq(hn[u], R::splat(0xFF));
+                        if (need) vp_mark<RowT>(vp, w.ppos[s], n[u], need);
+                    } else {
+                        r = relax<RowT>(Hs, n[u], hn[u], mask, l);
+                        p_cells += r.cells;
+                    }
                 }
                 enq[u] = r.enq;
                 idn[u] = r.ident;
@@ -904,6 +948,60 @@ __global__ void __launch_bounds__(256) k_vp_apply(GraphDev g, WsDev w, int ph, u
         }
         frontier_push(w, enq, s, n, nxt);
         cand_push(g, w, id, s, n, l + 1);
+    }
+    p_cells = warp_sum(p_cells);
+    if (lane_id() == 0 && p_cells) atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
+}
+
+// Vertex-partitioned push, after the exchange: the planes of every rank's slice are applied
+// to the replicated H on every rank (H, next frontier and identification at l + 1 identical
+// everywhere).  Thread per 32-node word of a slice: warps whose words are all zero skip;
+// otherwise a warp-uniform loop over the 32 bit positions (frontier_push / cand_push are
+// warp collectives).  x: slice r of pull position p, plane j at x + r*stride + (p*RB + j)*wc.
+template <class RowT>
+__global__ void __launch_bounds__(256) k_vp_apply_words(GraphDev g, WsDev w, int ph, uint32_t l, const uint32_t *x,
+                                                        size_t stride, uint32_t wc, uint32_t nranks,
+                                                        const uint32_t *bounds) {
+    typedef Row<RowT> R;
+    constexpr uint32_t RB = sizeof(RowT);
+    const uint32_t p = blockIdx.y, s = w.pslots[p];
+    const HV<RowT> H = w.Hs<RowT>(ph, s);
+    const bool collect = w.st[s].collect;
+    const uint32_t nxt = (l & 1) ^ 1;
+    const uint32_t total = nranks * wc;
+    uint32_t p_cells = 0;
+    for (uint32_t b = blockIdx.x * blockDim.x; b < total; b += gridDim.x * blockDim.x) {
+        const uint32_t t = b + threadIdx.x;
+        uint32_t pl[RB], any = 0, base = 0;
+        if (t < total) {
+            const uint32_t r = t / wc, wi = t % wc;
+            const uint32_t *xs = x + r * stride + (size_t)p * RB * wc + wi;
+#pragma unroll
+            for (uint32_t j = 0; j < RB; j++) any |= (pl[j] = __ldg(xs + (size_t)j * wc));
+            base = __ldg(bounds + r) + wi * 32;
+        } else {
+#pragma unroll
+            for (uint32_t j = 0; j < RB; j++) pl[j] = 0;
+        }
+        if (!__any_sync(FULLMASK, any != 0)) continue;
+        for (uint32_t bit = 0; bit < 32; bit++) {
+            bool enq = false, id = false;
+            const uint32_t n = base + bit;
+            if ((any >> bit) & 1u) {
+                RowT found = 0;
+#pragma unroll
+                for (uint32_t j = 0; j < RB; j++)
+                    if ((pl[j] >> bit) & 1u) found |= (RowT)0xFF << (8 * j);
+                const RowT Rn = R::load(H + n);  // found cells were infinite at the level start on every rank
+                const RowT nr = (Rn & ~found) | (found & R::splat(l + 1));
+                *(H + n) = nr;
+                enq = true;
+                id = collect && R::eq(nr, R::splat(0xFF)) == 0;
+                p_cells += R::ones(found);
+            }
+            frontier_push(w, enq, s, n, nxt);
+            cand_push(g, w, id, s, n, l + 1);
+        }
     }
     p_cells = warp_sum(p_cells);
     if (lane_id() == 0 && p_cells) atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
@@ -2448,7 +2546,7 @@ struct Workspace {
     uint8_t *H[2] = {nullptr, nullptr};
     uint32_t qcap = 0;  // entries per level queue
     unsigned long long *offs = nullptr;
-    uint32_t *q = nullptr, *bm = nullptr, *jq = nullptr, *jbm = nullptr, *coffs = nullptr, *pslots = nullptr, *ctr = nullptr, *arena = nullptr,
+    uint32_t *q = nullptr, *bm = nullptr, *jq = nullptr, *jbm = nullptr, *coffs = nullptr, *pslots = nullptr, *ppos = nullptr, *ctr = nullptr, *arena = nullptr,
              *big = nullptr, *resid = nullptr, *out = nullptr;
     uint4 *mtab = nullptr;
     uint64_t *ck = nullptr, *ck2 = nullptr;  // candidate keys; ck2 = sorted copy (segmented radix sort)
@@ -2525,7 +2623,7 @@ struct Workspace {
         memset(&d, 0, sizeof(d));  // padding too: the struct is part of CUDA-graph cache keys
         d.st = st; d.nslots = cur ? cur : slots; d.V = V; d.W = W; d.capc = capc; d.kmax = kmax;
         d.H[0] = H[0]; d.H[1] = H[1]; d.hnode = hnode; d.SP = SP; d.rb[0] = last_rb[0]; d.rb[1] = last_rb[1];
-        d.q = q; d.qcap = qcap; d.bm = bm; d.jq = jq; d.jbm = jbm; d.ck = ck; d.cd = cd; d.rk = rk; d.offs = offs; d.coffs = coffs; d.pslots = pslots; d.track_reached = track_reached;
+        d.q = q; d.qcap = qcap; d.bm = bm; d.jq = jq; d.jbm = jbm; d.ck = ck; d.cd = cd; d.rk = rk; d.offs = offs; d.coffs = coffs; d.pslots = pslots; d.ppos = ppos; d.track_reached = track_reached;
         d.heavy = heavy; d.heavy_cap = heavy_cap; d.ctr = ctr; d.prof = prof;
         d.arena = arena; d.arena_used = arena_used; d.arena_cap = arena_cap;
         d.newatt = newatt; d.ovf = ovf; d.ovf2 = ovf2; d.ovf_cap = ovf_cap; d.cst = cst; d.bounded = bounded;
@@ -2609,6 +2707,7 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     ws->offs = ws->alloc<unsigned long long>(S + 1);
     ws->coffs = ws->alloc<uint32_t>(S + 1);
     ws->pslots = ws->alloc<uint32_t>(S + 1);
+    ws->ppos = ws->alloc<uint32_t>(S + 1);
     uint64_t hc = (uint64_t)S * (g->E / CHUNK + g->E / HEAVY + 64);
     ws->heavy_cap = (uint32_t)std::min<uint64_t>(hc, 1u << 28);
     ws->heavy = ws->alloc<uint4>(ws->heavy_cap);
@@ -2736,6 +2835,42 @@ void vp_level(Launch &L, const GraphDev &gd, const WsDev &wd, int ph, uint32_t l
     const uint64_t total = (uint64_t)d->nranks * d->wc * 32;
     k_vp_apply<RowT><<<dim3((uint32_t)std::min<uint64_t>((total + 255) / 256, 148 * 8), npull), 256, 0, s>>>(
         gd, wd, ph, l, x, d->wc, d->nranks, d->d_bounds, npull);
+    L.check(__LINE__);
+}
+
+// One vertex-partitioned PUSH level (default VP mode): every rank walks the
+// out-edges of the frontier nodes it owns and ORs newly reachable cells into the owners' bit
+// planes (peer memory in a real run: the fused exchange), then the planes are made visible
+// to every rank and applied to the replicated H.  Per-rank edge work = the frontier's edges
+// owned by the rank; no pass over all V.
+template <class RowT>
+void vp_level_push(Launch &L, const GraphDev &gd, const WsDev &wd, int ph, uint32_t l, uint32_t npull, bool wide) {
+    DistState *d = L.g->dist;
+    cudaStream_t s = L.s;
+    dist_push_setup(L.g, wd.nslots);
+    const size_t chunk = (size_t)npull * sizeof(RowT) * d->wc;
+    const bool real = d->comm != nullptr && d->nranks > 1;
+    uint32_t *const *xs = dist_push_targets(L.g);
+    if (!real)  // the slices of this level start empty (a real run clears them in the exchange)
+        CUDA_TRY(cudaMemset2DAsync(d->d_slices, d->slice_words * 4, 0, chunk * 4, d->nranks, s));
+    for (int r = 0; r < d->nranks; r++) {
+        if (!d->simulated && r != d->rank) continue;
+        const VpPush vp{d->bounds[r], d->bounds[r + 1], (uint32_t)d->nranks, d->wc,
+                        (uint32_t)(d->simulated ? r == 0 : 1), d->d_bounds, xs};
+        if (wide)
+            k_expand<RowT, true, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l, vp);
+        else
+            k_expand<RowT, false, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l, vp);
+        L.check(__LINE__);
+    }
+    const VpPush vph{0, gd.V, (uint32_t)d->nranks, d->wc, 1, d->d_bounds, xs};
+    k_expand_heavy<RowT, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l, vph);
+    L.check(__LINE__);
+    size_t stride = 0;
+    const uint32_t *x = dist_push_exchange(L.g, chunk, s, &stride);
+    const uint32_t words = (uint32_t)d->nranks * d->wc;
+    k_vp_apply_words<RowT><<<dim3(std::min<uint32_t>((words + 255) / 256, 148 * 8), npull), 256, 0, s>>>(
+        gd, wd, ph, l, x, stride, d->wc, (uint32_t)d->nranks, d->d_bounds);
     L.check(__LINE__);
 }
 
@@ -2957,9 +3092,14 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
         }
         L.levels++;
         if (L.g->profiling) CUDA_TRY(cudaEventRecord(ws->event(L.nev++), s));
-        level_expand(l);
-        if (vp) {
+        if (vp && L.g->dist->push) {
+            if (uint32_t npull = ws->h_ctr[C_NPULL]) vp_level_push<RowT>(L, gd, wd, ph, l, npull, wide);
+        } else {
+            level_expand(l);
+        }
+        if (vp && !L.g->dist->push) {
             if (uint32_t npull = ws->h_ctr[C_NPULL]) vp_level<RowT>(L, gd, wd, ph, l, npull);
+        } else if (vp) {
         } else if (L.g->pull_on) {
             if (uint32_t npull = ws->h_ctr[C_NPULL]) {
                 uint32_t nbh = (gd.Vh + 7) / 8;
@@ -3056,7 +3196,12 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     if (L.g->profiling) CUDA_TRY(cudaStreamSynchronize(s));
     L.mark(1);
     // ---- run 2: marginal keywords
-    ws->bounded = getenv("RIKI_EAGER_RPG") ? 0 : 1;  // RIKI_EAGER_RPG=1 recovers every attached RPG (A/B, tests)
+    // Bounded recovery adds two selection waves (10 launches) per level and saves the RPG
+    // recovery of candidates that cannot enter the top-k: it pays off when the candidate sets
+    // are large against k (C5: ~300 k per query, +9 %; C2: ~47 k, -3 %: r02f A/B), hence the
+    // crossover below.  RIKI_EAGER_RPG=1 / RIKI_BOUNDED_RPG=1 force either mode (A/B, tests).
+    const uint64_t per_slot = total_cands / std::max<uint32_t>(wd.nslots, 1);
+    ws->bounded = getenv("RIKI_EAGER_RPG") ? 0 : getenv("RIKI_BOUNDED_RPG") ? 1 : per_slot > 100ull * ws->kmax;
     run_phase<RowM, RowC>(L, gd, ws, 1, -1, depth + 1, total_cands);
     L.mark(2);
     // ---- top-k and packing

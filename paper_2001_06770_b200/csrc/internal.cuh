@@ -30,6 +30,16 @@ struct DistState {
     uint32_t *d_x = nullptr;             // exchange buffer [rank][pull slot][plane][wc]
     size_t x_words = 0;
     uint64_t exchanges = 0, exchanged_bytes = 0;
+    // push mode (default): bit-plane slices every rank ORs into over peer memory (dist.cu)
+    bool push = true;
+    size_t slice_words = 0;        // words per slice: slots * 8 planes * wc
+    uint32_t *d_slices = nullptr;  // simulated: [nranks][slice_words]; real: own slices [3][slice_words]
+    uint32_t *d_gather = nullptr;  // real: all-gathered slices [nranks][chunk]
+    uint32_t **d_xs = nullptr;     // device pointer table: [3][nranks] slice of each owner per level mod 3
+    std::vector<void *> peer_bases;  // real: peers' d_slices opened through CUDA IPC (index = rank)
+    uint64_t t = 0;                // level counter of the push exchange (slices rotate mod 3)
+    size_t used[3] = {0, 0, 0};    // words written into own slice t mod 3
+    int *d_one = nullptr;          // barrier operand
 };
 
 // Device view of the resident graph (P:339 CSR).  Out-rows are sorted by activation
@@ -165,4 +175,9 @@ void dist_partition(const uint32_t *irow, uint32_t V, uint32_t nranks, uint32_t 
 uint32_t *dist_exchange_buffer(riki_graph *g, size_t chunk_words);  // [nranks][chunk_words], zeroed by the caller
 void dist_allgather(riki_graph *g, uint32_t *x, size_t chunk_words, cudaStream_t s);
 void dist_free(riki_graph *g);
+// vertex-partitioned push (dist.cu): slices sized for `slots` pull positions; per level t the
+// table of owners' slices to OR into, then the exchange that makes every rank's planes visible
+void dist_push_setup(riki_graph *g, uint32_t slots);
+uint32_t *const *dist_push_targets(riki_graph *g);
+const uint32_t *dist_push_exchange(riki_graph *g, size_t chunk_words, cudaStream_t s, size_t *stride);
 uint64_t engine_workspace_bytes(const riki_graph *g);

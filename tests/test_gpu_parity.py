@@ -267,7 +267,9 @@ def test_bounded_rpg_recovery_equals_eager(P, seed, monkeypatch):
         Ms.append(tt[nc:].tolist())
     k = int(rng.choice([1, 2, 4]))
     kw = dict(ptc_mode=int(rng.choice([0, 1, 2])))
+    monkeypatch.setenv("RIKI_BOUNDED_RPG", "1")  # (the library picks it by itself for large candidate sets)
     bounded = g.search_batch(Cs, Ms, k, 20, **kw)
+    monkeypatch.delenv("RIKI_BOUNDED_RPG")
     monkeypatch.setenv("RIKI_EAGER_RPG", "1")
     eager = g.search_batch(Cs, Ms, k, 20, **kw)
     for i, (a, b) in enumerate(zip(bounded, eager)):

@@ -6,8 +6,10 @@ over a world-size-2 gloo group.
 
 GPU (`-m gpu`): the partitioned path must give the oracle's H / block / relaxation counts and
 the oracle's search results bit for bit -- with nranks partitions simulated in one process
-(every partition's pull runs on the one GPU; the exchange is the identity), and through a real
-1-rank NCCL communicator (the in-place all-gather on the search stream)."""
+(every partition's push -- its owned frontier nodes' out-edges OR-ed into the owners' bit-plane
+slices, the fused exchange -- runs on the one GPU; the exchange is the identity), and through
+a real 1-rank NCCL communicator.  The earlier pull variant (RIKI_VP_PULL=1: every rank pulls
+its owned range, one all-gather per level) is checked the same way."""
 import os
 import socket
 
@@ -154,7 +156,10 @@ def _hub_graph(rng, V=3000, m=9000):
 @pytest.mark.gpu
 @pytest.mark.parametrize("seed", range(8))
 @pytest.mark.parametrize("nranks", [2, 3, 8])
-def test_vp_simulated_hitting_levels(P, seed, nranks):
+@pytest.mark.parametrize("variant", ["push", "pull"])
+def test_vp_simulated_hitting_levels(P, seed, nranks, variant, monkeypatch):
+    if variant == "pull":
+        monkeypatch.setenv("RIKI_VP_PULL", "1")  # read by riki_dist_init
     rng = np.random.default_rng(9100 + seed)
     if seed % 2:
         V, src, dst, act = _hub_graph(rng)
