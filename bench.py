@@ -231,8 +231,9 @@ def run_reference(args):
     qs = synth.config_queries(kg, args.config)
     per = step_size(args.config, spec, args.queries)
     cores = host_cores()
-    # each step: a bounded sample of the step's chunk, one query per host core
-    nref = args.ref_queries or cores
+    # each step: a bounded sample of the step's chunk (one query per thread; the oracle takes
+    # 5-40 s per config-5 query, so a step is about its slowest query)
+    nref = args.ref_queries or min(cores, 8 if args.config >= 4 else 2 * cores)
     og = oracle_graph(kg)
 
     def idx(s):
@@ -275,7 +276,7 @@ def main():
     ap.add_argument("--cpu-latency", type=int, default=0,
                     help="oracle queries run on one core for its p50/p99 latency (default 6 at C4/C5, else 16)")
     ap.add_argument("--ref-queries", type=int, default=0,
-                    help="oracle queries per step for --impl reference (0 = one per host core)")
+                    help="oracle queries per step for --impl reference (0 = 8 at C4/C5, else 2 per core)")
     ap.add_argument("--latency-queries", type=int, default=40)
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle (cpu_baseline and the parity gate)")
     ap.add_argument("--no-profile", action="store_true", help="skip the profiling pass (roofline)")

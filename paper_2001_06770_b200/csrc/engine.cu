@@ -433,6 +433,36 @@ __device__ __forceinline__ Relax<RowT> relax(const HV<RowT> &H, uint32_t n, RowT
     return r;
 }
 
+// The same relaxation for U edges of one lane at once: every atomic is issued before any of
+// their results is used, so a lane has U atomics in flight instead of one (ncu r02e: the
+// instructions after each atomicAnd carried the top stall samples).  EXP_BATCH_ATOM=0 keeps
+// the one-at-a-time relax() (A/B).
+#ifndef EXP_BATCH_ATOM
+#define EXP_BATCH_ATOM 1
+#endif
+template <class RowT, int U>
+__device__ __forceinline__ void relax_n(RowT *const (&row)[U], const RowT (&hn)[U], const RowT (&mask)[U],
+                                        const bool (&ev)[U], uint32_t l, bool (&enq)[U], bool (&idn)[U],
+                                        uint32_t &cells) {
+    typedef Row<RowT> R;
+    const RowT FF = R::splat(0xFF), L1 = R::splat(l + 1);
+    RowT need[U], andm[U], old[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        need[u] = ev[u] ? mask[u] & R::eq(hn[u], FF) : (RowT)0;
+        andm[u] = ~need[u] | (need[u] & L1);
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) old[u] = need[u] ? R::atomic_and(row[u], andm[u]) : (RowT)0;
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        const RowT changed = need[u] & R::eq(old[u], FF);
+        cells += R::ones(changed);
+        enq[u] = changed && R::eq(old[u], L1) == 0;
+        idn[u] = changed && R::eq(old[u] & andm[u], FF) == 0;
+    }
+}
+
 // Next frontier Q_{l+1}: a node is appended by the first writer of its row at level l (new
 // entry) or, if it keeps pending edges (Alg. 1 lines 9-11), by its own item (retained entry,
 // tag bit 31).  A retained entry whose row also carries l+1 is a duplicate and is skipped by
@@ -786,19 +816,27 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, Ws
             for (int u = 0; u < EXP_UNROLL; u++)
                 hn[u] = ev[u] ? R::load(Hb + ((size_t)(o_s[u] / HGRP) * V + n[u]) * HGRP + o_s[u] % HGRP) : (RowT)0;
             bool enq[EXP_UNROLL], idn[EXP_UNROLL];
+            if (!VPX && EXP_BATCH_ATOM) {
+                RowT *rowp[EXP_UNROLL];
 #pragma unroll
-            for (int u = 0; u < EXP_UNROLL; u++) {
-                Relax<RowT> r{false, false, 0};
-                if (VPX) {  // H is read-only during a partitioned level: mark the owner's bit planes
-                    const RowT need = mask[u] & R::eq(hn[u], R::splat(0xFF));
-                    if (ev[u] && need) vp_mark<RowT>(vp, w.ppos[o_s[u]], n[u], need);
-                } else if (ev[u]) {
-                    r = relax<RowT>(HV<RowT>{Hb + (size_t)(o_s[u] / HGRP) * V * HGRP + o_s[u] % HGRP, (uint32_t)HGRP},
-                                    n[u], hn[u], mask[u], l);
-                    p_cells += r.cells;
+                for (int u = 0; u < EXP_UNROLL; u++)
+                    rowp[u] = Hb + ((size_t)(o_s[u] / HGRP) * V + n[u]) * HGRP + o_s[u] % HGRP;
+                relax_n<RowT, EXP_UNROLL>(rowp, hn, mask, ev, l, enq, idn, p_cells);
+            } else {
+#pragma unroll
+                for (int u = 0; u < EXP_UNROLL; u++) {
+                    Relax<RowT> r{false, false, 0};
+                    if (VPX) {  // H is read-only during a partitioned level: mark the owner's bit planes
+                        const RowT need = mask[u] & R::eq(hn[u], R::splat(0xFF));
+                        if (ev[u] && need) vp_mark<RowT>(vp, w.ppos[o_s[u]], n[u], need);
+                    } else if (ev[u]) {
+                        r = relax<RowT>(HV<RowT>{Hb + (size_t)(o_s[u] / HGRP) * V * HGRP + o_s[u] % HGRP, (uint32_t)HGRP},
+                                        n[u], hn[u], mask[u], l);
+                        p_cells += r.cells;
+                    }
+                    enq[u] = r.enq;
+                    idn[u] = r.ident;
                 }
-                enq[u] = r.enq;
-                idn[u] = r.ident;
             }
             {
                 bool pw[EXP_UNROLL + 1];
@@ -872,6 +910,17 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand_heavy(GraphDev
             uint32_t ss[HEAVY_UNROLL];
 #pragma unroll
             for (int u = 0; u < HEAVY_UNROLL; u++) ss[u] = s;
+            if (!VPX && EXP_BATCH_ATOM) {
+                RowT *rowp[HEAVY_UNROLL], mk[HEAVY_UNROLL];
+                bool ev[HEAVY_UNROLL];
+#pragma unroll
+                for (int u = 0; u < HEAVY_UNROLL; u++) {
+                    ev[u] = e0 + 32 * u + lane < h.w;
+                    rowp[u] = Hs + n[u];
+                    mk[u] = newc | (a[u] == l ? oldc : (RowT)0);
+                }
+                relax_n<RowT, HEAVY_UNROLL>(rowp, hn, mk, ev, l, enq, idn, p_cells);
+            } else
 #pragma unroll
             for (int u = 0; u < HEAVY_UNROLL; u++) {
                 Relax<RowT> r{false, false, 0};
@@ -3254,14 +3303,16 @@ int row_bytes(uint32_t T) {
 #endif
 }
 
+// qmap (optional): the batch runs in row-width groups; slot s takes query qmap[q0 + s]
+// (positions q0 + s < nq of the grouped order), else query q0 + s.
 __global__ void k_slots_from_device(SlotState *st, uint32_t nslots, uint32_t q0, uint32_t nq, const uint64_t *cptr,
                                     const uint32_t *ct, const uint64_t *mptr, const uint32_t *mt, SlotState tmpl,
-                                    const uint64_t *tptr, uint32_t n_terms) {
+                                    const uint64_t *tptr, uint32_t n_terms, const uint32_t *qmap) {
     uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= nslots) return;
     SlotState x = tmpl;
-    uint32_t q = q0 + s;
-    x.active = q < nq;
+    x.active = q0 + s < nq;
+    const uint32_t q = x.active && qmap ? qmap[q0 + s] : q0 + s;
     if (x.active) {
         uint64_t cb = cptr[q], ce = cptr[q + 1], mb = mptr[q], me = mptr[q + 1];
         x.T[0] = (uint32_t)(ce - cb);
@@ -3528,22 +3579,38 @@ void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, ui
     if (g->ws) g->ws->last_n = 0;  // the workspace is reused: a pending device batch is gone
     for (riki_results *r : g->dev_stash) delete r;
     g->dev_stash.clear();
-    uint32_t maxc = 0, maxm = 0;
-    for (const QueryIn &q : qs) { maxc = std::max(maxc, q.nc); maxm = std::max(maxm, q.nm); }
     SlotState tmpl = make_template(k, depth, p);
     std::vector<riki_results *> &res = *out;
+    // row-width groups (see engine_search_device)
+    auto cls_of = [&](uint32_t q) {
+        return (uint32_t)row_bytes(std::max(qs[q].nc, 1u)) << 8 | (uint32_t)row_bytes(std::max(qs[q].nm, 1u));
+    };
+    const uint32_t nq = (uint32_t)qs.size();
+    std::vector<uint32_t> order(nq);
+    for (uint32_t q = 0; q < nq; q++) order[q] = q;
+    if (!getenv("RIKI_NO_ROW_GROUPS"))
+        std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cls_of(a) < cls_of(b); });
     try {
-        for (size_t q0 = 0; q0 < qs.size();) {
+        for (uint32_t q0 = 0; q0 < nq;) {
             ensure_workspace(g, caps);
             uint32_t slots = std::min(g->ws->slots, caps.slots);
-            uint32_t n = (uint32_t)std::min<size_t>(slots, qs.size() - q0);
+            // a chunk never mixes row widths (RIKI_NO_ROW_GROUPS: one group at the widest rows)
+            uint32_t n = std::min<uint32_t>(slots, nq - q0);
+            if (!getenv("RIKI_NO_ROW_GROUPS"))
+                for (uint32_t i = 1; i < n; i++)
+                    if (cls_of(order[q0 + i]) != cls_of(order[q0])) { n = i; break; }
+            uint32_t maxc = 0, maxm = 0;
+            for (uint32_t i = 0; i < n; i++) {
+                maxc = std::max(maxc, qs[order[q0 + i]].nc);
+                maxm = std::max(maxm, qs[order[q0 + i]].nm);
+            }
             std::vector<uint32_t> qidx(n);
-            for (uint32_t i = 0; i < n; i++) qidx[i] = (uint32_t)(q0 + i);
+            for (uint32_t i = 0; i < n; i++) qidx[i] = order[q0 + i];
             std::vector<SlotState> stv;
             auto upload = [&]() {
                 Workspace *ws = g->ws;
                 ws->last_rb[0] = row_bytes(maxc);
-                ws->last_rb[1] = row_bytes(maxm);
+                ws->last_rb[1] = row_bytes(std::max(maxm, 1u));
                 ws->tie_break = tmpl.tie_break;
                 ws->beam_tie = tmpl.tie_break && tmpl.beam_mode == 1;
                 ws->cur = n;
@@ -3551,15 +3618,11 @@ void engine_search(riki_graph *g, const std::vector<QueryIn> &qs, uint32_t k, ui
                 std::vector<SlotState> h(n, tmpl);
                 for (uint32_t i = 0; i < n; i++) {
                     SlotState &x = h[i];
-                    if (i < n) {
-                        const QueryIn &q = qs[q0 + i];
-                        x.active = 1;
-                        x.T[0] = q.nc; x.T[1] = q.nm;
-                        for (uint32_t j = 0; j < q.nc; j++) x.term[0][j] = q.c[j];
-                        for (uint32_t j = 0; j < q.nm; j++) x.term[1][j] = q.m[j];
-                    } else {
-                        x.active = 0; x.T[0] = x.T[1] = 0;
-                    }
+                    const QueryIn &q = qs[qidx[i]];
+                    x.active = 1;
+                    x.T[0] = q.nc; x.T[1] = q.nm;
+                    for (uint32_t j = 0; j < q.nc; j++) x.term[0][j] = q.c[j];
+                    for (uint32_t j = 0; j < q.nm; j++) x.term[1][j] = q.m[j];
                 }
                 CUDA_TRY(cudaMemcpyAsync(ws->st, h.data(), h.size() * sizeof(SlotState), cudaMemcpyHostToDevice, L.s));
                 CUDA_TRY(cudaMemsetAsync(ws->prof, 0, P_NPROF * 8, L.s));
@@ -3597,7 +3660,41 @@ void engine_search_device(riki_graph *g, uint32_t nq, const uint64_t *d_cptr, co
     }
     if (maxc > RIKI_MAX_TERMS || maxm > RIKI_MAX_TERMS) RIKI_THROW(RIKI_EINVAL, "at most 8 terms per keyword class");
     tr("ptr D2H");
-    // the whole batch in flight when it fits the device memory (auto_slots), else chunks
+    // Row-width groups: a lock-step batch uses one H row width per run (the widest query's),
+    // so a mixed batch (config 5: |M| = 2 / 4 / 6) runs as one sub-batch per (central, marginal)
+    // row width -- narrower rows for most queries: half the H bytes per relaxation and per
+    // reset, and fewer registers in the expansion.  Results are per query either way.
+    auto cls_of = [&](uint32_t q) {
+        return (uint32_t)row_bytes(std::max<uint32_t>((uint32_t)(cp[q + 1] - cp[q]), 1u)) << 8 |
+               (uint32_t)row_bytes(std::max<uint32_t>((uint32_t)(mp[q + 1] - mp[q]), 1u));
+    };
+    std::vector<uint32_t> order(nq);
+    for (uint32_t q = 0; q < nq; q++) order[q] = q;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cls_of(a) < cls_of(b); });
+    std::vector<std::pair<uint32_t, uint32_t>> groups;  // [begin, end) in `order`
+    for (uint32_t i = 0; i < nq;) {
+        uint32_t j = i + 1;
+        while (j < nq && cls_of(order[j]) == cls_of(order[i])) j++;
+        groups.push_back({i, j});
+        i = j;
+    }
+    if (getenv("RIKI_NO_ROW_GROUPS")) {  // A/B: one group at the widest rows
+        groups.assign(1, {0u, nq});
+        for (uint32_t q = 0; q < nq; q++) order[q] = q;
+    }
+    const bool grouped = groups.size() > 1;
+    if (grouped) {
+        if (g->qmap_cap < nq) {
+            if (g->d_qmap) cudaFree(g->d_qmap);
+            g->d_qmap = nullptr;
+            g->qmap_cap = 0;
+            CUDA_TRY(cudaMalloc(&g->d_qmap, (size_t)nq * 4));
+            g->qmap_cap = nq;
+        }
+        CUDA_TRY(cudaMemcpyAsync(g->d_qmap, order.data(), (size_t)nq * 4, cudaMemcpyHostToDevice, g->stream));
+    }
+    // the whole batch in flight when it fits the device memory (auto_slots), else chunks; the
+    // workspace is sized for the widest rows, each group uses its own width inside it
     Caps caps = initial_caps(g, nq, k, row_bytes(std::max(maxc, 1u)), row_bytes(std::max(maxm, 1u)), depth,
                              std::max(g->batch_slots, std::min<uint32_t>(nq, MAX_SLOTS)));
     tr("initial_caps");
@@ -3608,37 +3705,42 @@ void engine_search_device(riki_graph *g, uint32_t nq, const uint64_t *d_cptr, co
     std::vector<SlotState> stv;
     for (riki_results *r : g->dev_stash) delete r;
     g->dev_stash.clear();
-    bool chunked = false;
-    for (uint32_t q0 = 0; q0 < nq;) {
-        const uint32_t n = std::min<uint32_t>(std::min(caps.slots, g->ws->slots), nq - q0);
-        auto upload = [&]() {
-            Workspace *ws = g->ws;
-            ws->last_rb[0] = row_bytes(maxc);
-            ws->last_rb[1] = row_bytes(maxm);
-            ws->tie_break = tmpl.tie_break;
-            ws->beam_tie = tmpl.tie_break && tmpl.beam_mode == 1;
-            ws->cur = n;
-            set_layout(g, ws, n);
-            k_slots_from_device<<<(n + 127) / 128, 128, 0, L.s>>>(ws->st, n, q0, nq, d_cptr, d_cterms, d_mptr, d_mterms,
-                                                                  tmpl, g->d_tptr, g->n_terms);
-            L.check(__LINE__);
-            CUDA_TRY(cudaMemsetAsync(ws->prof, 0, P_NPROF * 8, L.s));
-        };
-        tr("ensure+setup");
-        if (!run_with_retry(g, L, depth, caps, n, upload, &stv)) {  // arena limit: smaller chunks
-            chunked = true;
-            continue;
+    bool chunked = grouped;
+    for (const auto &grp : groups) {
+        const uint32_t gc = grouped ? cls_of(order[grp.first]) >> 8 : row_bytes(std::max(maxc, 1u));
+        const uint32_t gm = grouped ? cls_of(order[grp.first]) & 0xFF : row_bytes(std::max(maxm, 1u));
+        for (uint32_t q0 = grp.first; q0 < grp.second;) {
+            const uint32_t n = std::min<uint32_t>(std::min(caps.slots, g->ws->slots), grp.second - q0);
+            auto upload = [&]() {
+                Workspace *ws = g->ws;
+                ws->last_rb[0] = gc;
+                ws->last_rb[1] = gm;
+                ws->tie_break = tmpl.tie_break;
+                ws->beam_tie = tmpl.tie_break && tmpl.beam_mode == 1;
+                ws->cur = n;
+                set_layout(g, ws, n);
+                k_slots_from_device<<<(n + 127) / 128, 128, 0, L.s>>>(ws->st, n, q0, grp.second, d_cptr, d_cterms, d_mptr,
+                                                                      d_mterms, tmpl, g->d_tptr, g->n_terms,
+                                                                      grouped ? g->d_qmap : nullptr);
+                L.check(__LINE__);
+                CUDA_TRY(cudaMemsetAsync(ws->prof, 0, P_NPROF * 8, L.s));
+            };
+            tr("ensure+setup");
+            if (!run_with_retry(g, L, depth, caps, n, upload, &stv)) {  // arena limit: smaller chunks
+                chunked = true;
+                continue;
+            }
+            tr("run_with_retry");
+            if (chunked || n < nq) {  // results of a chunk leave HBM before the next chunk runs
+                chunked = true;
+                g->dev_stash.resize(nq, nullptr);
+                std::vector<uint32_t> qidx(n);
+                for (uint32_t i = 0; i < n; i++) qidx[i] = order[q0 + i];
+                collect_results(g, g->ws, n, qidx, &g->dev_stash, L.s);
+            }
+            add_stats(g, g->ws, L, n);
+            q0 += n;
         }
-        tr("run_with_retry");
-        if (chunked || n < nq) {  // results of a chunk leave HBM before the next chunk runs
-            chunked = true;
-            g->dev_stash.resize(nq, nullptr);
-            std::vector<uint32_t> qidx(n);
-            for (uint32_t i = 0; i < n; i++) qidx[i] = q0 + i;
-            collect_results(g, g->ws, n, qidx, &g->dev_stash, L.s);
-        }
-        add_stats(g, g->ws, L, n);
-        q0 += n;
     }
     g->ws->last_n = nq;
     tr("add_stats");
@@ -3739,6 +3841,9 @@ void engine_hitting_levels(riki_graph *g, const uint32_t *terms, uint32_t T, uin
 void engine_free(riki_graph *g) {
     for (riki_results *r : g->dev_stash) delete r;
     g->dev_stash.clear();
+    if (g->d_qmap) cudaFree(g->d_qmap);
+    g->d_qmap = nullptr;
+    g->qmap_cap = 0;
     if (g->ws) {
         g->ws->release();
         delete g->ws;

@@ -103,6 +103,8 @@ struct riki_graph {
     riki_stats stats{};
     DistState *dist = nullptr;  // set by riki_dist_init
     std::vector<riki_results *> dev_stash;
+    uint32_t *d_qmap = nullptr;  // device batch: query order of the row-width groups
+    uint32_t qmap_cap = 0;
     uint64_t arena_limit = 0;  // riki_set_arena_limit (tests): 0 = the 32-bit offset limit
     uint32_t slots_cap = 0;    // chunk size learnt from an arena-limited full-width batch (0 = none)
     uint64_t slots_cap_key = 0;  // ... and the batch shape it applies to (depth, row widths, k)
