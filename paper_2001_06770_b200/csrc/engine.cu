@@ -438,7 +438,7 @@ __device__ __forceinline__ Relax<RowT> relax(const HV<RowT> &H, uint32_t n, RowT
 // instructions after each atomicAnd carried the top stall samples).  EXP_BATCH_ATOM=0 keeps
 // the one-at-a-time relax() (A/B).
 #ifndef EXP_BATCH_ATOM
-#define EXP_BATCH_ATOM 1
+#define EXP_BATCH_ATOM 0  // measured: -1.5 % at C2, equal at C5 (r02h A/B)
 #endif
 template <class RowT, int U>
 __device__ __forceinline__ void relax_n(RowT *const (&row)[U], const RowT (&hn)[U], const RowT (&mask)[U],
@@ -853,9 +853,16 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, Ws
                 frontier_push_n<EXP_UNROLL + 1, 1>(w, pw, ps, pe, nxt);
                 retain = false;
             }
+            {   // identification appends: skipped (one vote) when no lane completed a row
+                bool anyid = false;
 #pragma unroll
-            for (int u = 0; u < EXP_UNROLL; u++)
-                cand_push(g, w, idn[u] && ((s_info[o_s[u]] >> 1) & 1), o_s[u], n[u], l + 1);
+                for (int u = 0; u < EXP_UNROLL; u++) anyid |= idn[u];
+                if (__any_sync(FULLMASK, anyid)) {
+#pragma unroll
+                    for (int u = 0; u < EXP_UNROLL; u++)
+                        cand_push(g, w, idn[u] && ((s_info[o_s[u]] >> 1) & 1), o_s[u], n[u], l + 1);
+                }
+            }
         }
     }
     p_edges = warp_sum(p_edges);
@@ -938,8 +945,12 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand_heavy(GraphDev
                 idn[u] = r.ident;
             }
             frontier_push_n<HEAVY_UNROLL>(w, enq, ss, n, nxt);
+            bool anyid = false;
 #pragma unroll
-            for (int u = 0; u < HEAVY_UNROLL; u++) cand_push(g, w, idn[u] && collect, s, n[u], l + 1);
+            for (int u = 0; u < HEAVY_UNROLL; u++) anyid |= idn[u] && collect;
+            if (__any_sync(FULLMASK, anyid))
+#pragma unroll
+                for (int u = 0; u < HEAVY_UNROLL; u++) cand_push(g, w, idn[u] && collect, s, n[u], l + 1);
         }
     }
     p_cells = warp_sum(p_cells);
@@ -2984,7 +2995,9 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
                     L.check(__LINE__);
                 };
                 if (wd.bounded) {  // two waves of bounded RPG recovery (k_rpg_select)
-                    for (int wave = 0; wave < 2; wave++) {
+                    // RIKI_RPG_WAVES=1: a single flush wave (filter by the k-th key at the level start)
+                    static const int waves = getenv("RIKI_RPG_WAVES") && atoi(getenv("RIKI_RPG_WAVES")) == 1 ? 1 : 2;
+                    for (int wave = 2 - waves; wave < 2; wave++) {
                         k_reset_level_ctrs<<<1, 1, 0, s>>>(wd);
                         L.check(__LINE__);
                         k_rpg_select<<<wd.nslots, 256, U128_SORT_KEYS * 16, s>>>(wd, l, wave);
