@@ -329,7 +329,7 @@ template <class RowT> __global__ void k_seed(GraphDev g, WsDev w, int ph) {
 // pull_min: minimum frontier for bottom-up (0xFFFFFFFF disables it)
 __global__ void k_plan(WsDev w, int ph, uint32_t l_arg, uint32_t pull_min) {
     const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
-    __shared__ unsigned long long sc[MAX_SLOTS];
+    __shared__ unsigned long long sc[64];  // warp sums, then their inclusive prefix
     __shared__ uint32_t nact, wpull[MAX_SLOTS / 32];
     __shared__ unsigned long long nenq;
     uint32_t s = threadIdx.x;
@@ -378,24 +378,36 @@ __global__ void k_plan(WsDev w, int ph, uint32_t l_arg, uint32_t pull_min) {
     }
     if (pl) w.pslots[pbefore + __popc(pb & lanemask_lt())] = s;
     if (s < w.nslots) w.ppos[s] = pl ? pbefore + __popc(pb & lanemask_lt()) : EMPTY;
-    // block exclusive scan (Hillis-Steele) over MAX_SLOTS
-    sc[s] = items;
-    __syncthreads();
-    for (uint32_t o = 1; o < MAX_SLOTS; o <<= 1) {
-        unsigned long long v = s >= o ? sc[s - o] : 0;
-        __syncthreads();
-        sc[s] += v;
-        __syncthreads();
+    // block exclusive scan over MAX_SLOTS: warp shuffles, then one pass over the 32 warp sums
+    unsigned long long incl = items;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long v = __shfl_up_sync(FULLMASK, incl, o);
+        if ((s & 31) >= (uint32_t)o) incl += v;
     }
-    if (s < w.nslots) w.offs[s] = sc[s] - items;
+    if ((s & 31) == 31) sc[s >> 5] = incl;
+    __syncthreads();
+    if (s < 32) {
+        unsigned long long t = sc[s];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long v = __shfl_up_sync(FULLMASK, t, o);
+            if (s >= (uint32_t)o) t += v;
+        }
+        sc[32 + s] = t;  // inclusive prefix of the warp sums
+    }
+    __syncthreads();
+    incl += (s >> 5) ? sc[32 + (s >> 5) - 1] : 0ull;
+    const unsigned long long total_items = sc[32 + 31];
+    if (s < w.nslots) w.offs[s] = incl - items;
     if (s == 0) {
-        w.offs[w.nslots] = sc[MAX_SLOTS - 1];
+        w.offs[w.nslots] = total_items;
         w.ctr[C_ACTIVE] = nact;
-        w.ctr[C_TOTAL] = (uint32_t)min(sc[MAX_SLOTS - 1], 0xFFFFFFFFull);  // diagnostics
+        w.ctr[C_TOTAL] = (uint32_t)min(total_items, 0xFFFFFFFFull);  // diagnostics
         w.ctr[C_NHEAVY] = 0;
         w.ctr[C_NPULL] = npull;
         if (!w.hnode) {  // profiling counters of the per-slot expansion (k_expand counts edges/cells)
-            w.prof[P_ITEMS] += sc[MAX_SLOTS - 1];
+            w.prof[P_ITEMS] += total_items;
             w.prof[P_ENQ] += nenq;
         }
         // joint traversal: size of the union frontier of this level, reset the next one
@@ -620,7 +632,7 @@ __device__ __forceinline__ void gate_range_in(const GraphDev &g, const uint4 &d,
 #define EXP_UNROLL 3
 #endif
 #ifndef EXP_MINB
-#define EXP_MINB 7  // 7 resident blocks (36 registers): measured +2.7 % at C5, equal at C2 (r02f A/B)
+#define EXP_MINB 8  // 32 registers (7 blocks would give the same 32: allocation is in units of 8)
 #endif
 // 64-bit rows (5-8 keywords) need more registers: at 8 blocks (32 registers) the u64 loop
 // spills to local memory in its hot path (ncu r02e: LDL + short-scoreboard stalls).
