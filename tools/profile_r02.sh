@@ -14,6 +14,7 @@ export RIKI_NO_GRAPHS=1
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -c 6000 --csv --log-file gpurun_out/${T}_c${C}_all_dram.csv $B > gpurun_out/${T}_c${C}_dram.log 2>&1
 echo dram_done
+if [ "${FULL:-1}" = "0" ]; then exit 0; fi
 SKIP=$(python - "$T" "$C" <<'PY'
 import csv, sys
 rows = [r for r in csv.reader(open(f"gpurun_out/{sys.argv[1]}_c{sys.argv[2]}_all_dram.csv")) if len(r) > 10]
