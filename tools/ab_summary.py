@@ -18,6 +18,7 @@ NOTES = {
     "r02j_w1": "RIKI_RPG_WAVES=1 (one flush wave); at C2 also RIKI_BOUNDED_RPG=1",
     "r02k": "run-to-run noise: the same libraries repeated (vd, libriki, vd, libriki, ve)",
     "r02l": "EXP_UNROLL 4 (vu4) and HEAVY_UNROLL 4 (vhu4) against the default, each twice",
+    "r02q_nob": "the same library with RIKI_NO_BUCKETS=1 (the default path)",
     "r02q": "destination-bucketed relaxation (on by default for V >= 4M) vs RIKI_NO_BUCKETS=1 (r02q_nob), each twice; C2 unaffected",
     "r02n": "EXP_SMALL 4 (libriki.so: ranges of <= 4 due edges walked lane-locally) vs EXP_SMALL 0 (vs0), each twice",
 }
