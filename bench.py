@@ -390,22 +390,23 @@ def main():
         prof["step_ms"] = prof_ms
 
     # ---------------- e2e through the host C-ABI (H2D of queries, D2H of results inside)
-    h2d = d2h = 0
     res_by_chunk = {}
 
     def step_e2e(i):
-        nonlocal h2d, d2h
         ids, cs, ms, arrs = host_chunks[i % nchunks]
-        rr = g.search_batch(cs, ms, qs.k, qs.depth)
+        rr = g.search_batch(cs, ms, qs.k, qs.depth)  # H2D of the queries, D2H + export of every result
         if dist and not args.vp:  # replicated mode: every shard's results gathered to rank 0
             gather_results(rr, device=rdev)
         if i < nchunks:
             res_by_chunk[i % nchunks] = rr
-        h2d = sum(a.nbytes for a in arrs)
-        d2h = sum(4 * (len(x.nodes) + len(x.vc)) + 8 * len(x.edge_ids) + 64 for r in rr for x in r.rpgs)
         return len(ids)
 
     e2e_step_ms, nq_e2e = timed_pass(step_e2e)
+    # bytes moved per step (counted after the timed region from the tensors copied)
+    h2d = sum(a.nbytes for a in host_chunks[0][3])
+    rr0 = res_by_chunk[0]
+    d2h = int(rr0.hdr.nbytes + rr0.score.nbytes + rr0.nodes.nbytes + rr0.edges.nbytes + rr0.vc.nbytes +
+              rr0.cd.nbytes + rr0.md.nbytes + rr0.stats.nbytes + rr0.cnt.nbytes) if hasattr(rr0, "hdr") else 0
     e2e_ms = max_over_ranks(sum(e2e_step_ms), device=rdev)
     e2e_value = nq_e2e * units / (e2e_ms / 1000.0)
 
