@@ -505,6 +505,28 @@ def main():
             "qps_roofline_expansion_bytes": peak * 1e9 / qbytes * units if qbytes else None,
             "qps_frac_of_roofline": value / (peak * 1e9 / qbytes * units) if qbytes else None,
             "peak_source": peak_src}
+        # The expansion is bound by RANDOM row accesses, not by streaming bandwidth: every due edge
+        # reads its neighbour's H row at a random address and a productive one follows it with a
+        # dependent atomicAnd.  Ceiling for that mix, measured on this pool's B200s by
+        # tools/randbench.cu (uniformly random 4-byte accesses over 8 GiB; a miss fetches a full
+        # 128-byte line): T = (loads - atomics) / load rate + atomics / (load+atomic pair rate).
+        try:
+            rb = [json.loads(x) for x in open(os.path.join(ROOT, "profiles", "r02_randbench_b200.jsonl"))
+                  if x.startswith("{") and '"working_set_mib": 8192' in x]
+            r_load = next(x for x in rb if x["pattern"] in ("load", "load.cg"))["g_accesses_per_s"] * 1e9
+            r_pair = next(x for x in rb if x["pattern"] in ("load+atomicAnd", "load.cg+atomicAnd"))["g_accesses_per_s"] * 1e9 / 2
+            loads, atoms = prof["exp_edges"], prof.get("exp_atomics", 0)
+            t_ceil = (loads - atoms) / r_load + atoms / r_pair
+            line["random_access_roofline"] = {
+                "bound": "random 128-byte line fetches (HBM latency/concurrency), measured",
+                "load_rate_g_per_s": r_load / 1e9, "pair_rate_g_per_s": r_pair / 1e9,
+                "source": "profiles/r02_randbench_b200.jsonl (tools/randbench.cu, 8 GiB working set)",
+                "h_row_loads_per_step": loads / args.steps, "atomics_per_step": atoms / args.steps,
+                "ceiling_ms_per_step": t_ceil * 1e3 / args.steps, "expand_ms_per_step": exp_s * 1e3 / args.steps,
+                "frac": t_ceil / exp_s if exp_s > 0 else None,
+                "note": "frac > 1 is possible: hub rows hit in L2, the uniform-random ceiling assumes none do"}
+        except Exception as e:  # noqa: BLE001 -- reported, never fatal
+            line["random_access_roofline"] = {"error": str(e)}
         line["gpu_launches"] = int(prof["kernel_launches"])
         line["gpu_launches_note"] = "kernels launched for the timed steps' work, counted in the profiling pass " \
                                     "(the production pass replays the same kernels from CUDA graphs)"

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_segmented_radix_sort.cuh>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -66,6 +67,7 @@ enum Prof { P_ITEMS = 0, P_EDGES, P_NEWCELLS, P_ENQ, P_RELAX, P_PULLNODES, P_PUL
             P_R_ITEMS, P_R_WARPMAX, P_R_H0,  // P_R_H0..+5: candidate-time histogram
             // expansion item diagnostics (compiled in with -DEXP_STATS=1)
             P_X_DUP = 24, P_X_BLOCKED, P_X_IDLE, P_X_WORK,
+            P_ATOMS = 28,  // relaxation atomics issued by the expansion (random-access roofline)
             // recovery tier diagnostics (REC_STATS): candidates per tier, big-tier sizes
             P_R_T1 = 32, P_R_T2, P_R_T2NODES, P_R_T2EDGES, P_R_T2MAXE, P_R_T1RPG, P_R_T2RPG, P_NPROF = 40 };
 #ifndef EXP_STATS
@@ -421,8 +423,16 @@ __global__ void k_plan(WsDev w, int ph, uint32_t l_arg, uint32_t pull_min) {
 template <class RowT> struct Relax {
     bool enq;    // first writer of this row at this level -> next frontier
     bool ident;  // completed the row -> identified at level l+1
-    int cells;   // cells turned from inf to l+1 by this thread
+    int cells;   // cells turned from inf to l+1 by this thread, + ATOM_ONE if it issued the atomic
 };
+// relax() reports the atomic it issued as ATOM_ONE in `cells`; the expansion adds the cells to
+// a per-lane counter and the atomics, one ballot per unrolled edge, to a warp-uniform counter
+// (uniform registers: no pressure on the 32-register budget of the 8-blocks/SM kernels)
+constexpr int ATOM_ONE = 1 << 16;
+__device__ __forceinline__ void cnt_add(uint32_t &cells_acc, uint32_t &atoms_acc, int cells) {
+    cells_acc += cells & 0xFFFF;
+    atoms_acc += __popc(__ballot_sync(FULLMASK, cells >= ATOM_ONE));
+}
 
 // Relaxation of edge (f -> n) for the byte-columns in `mask` at level l (Alg. 1 lines 12-17),
 // given the (possibly stale) row hn read earlier: one atomicAnd writes l+1 into every selected
@@ -438,8 +448,9 @@ __device__ __forceinline__ Relax<RowT> relax(const HV<RowT> &H, uint32_t n, RowT
     RowT andm = ~need | (need & R::splat(l + 1));
     RowT old = R::atomic_and(H + n, andm);
     RowT changed = need & R::eq(old, FF);
+    r.cells = ATOM_ONE;
     if (!changed) return r;
-    r.cells = R::ones(changed);
+    r.cells += R::ones(changed);
     r.enq = R::eq(old, R::splat(l + 1)) == 0;  // no cell of n was written at this level before
     r.ident = R::eq(old & andm, FF) == 0;      // this write completed the row
     return r;
@@ -455,7 +466,7 @@ __device__ __forceinline__ Relax<RowT> relax(const HV<RowT> &H, uint32_t n, RowT
 template <class RowT, int U>
 __device__ __forceinline__ void relax_n(RowT *const (&row)[U], const RowT (&hn)[U], const RowT (&mask)[U],
                                         const bool (&ev)[U], uint32_t l, bool (&enq)[U], bool (&idn)[U],
-                                        uint32_t &cells) {
+                                        uint32_t &cells) {  // (A/B variant: atomics not counted)
     typedef Row<RowT> R;
     const RowT FF = R::splat(0xFF), L1 = R::splat(l + 1);
     RowT need[U], andm[U], old[U];
@@ -705,7 +716,7 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, Ws
     RowT *const Hb = (RowT *)w.H[ph];  // per-slot layout (HGRP groups; never joint here)
     const size_t V = w.V;
     OwnF<RowT> *const own = s_own[threadIdx.x >> 5];
-    uint32_t p_edges = 0, p_cells = 0, p_work = 0;  // items and queue entries are counted by k_plan
+    uint32_t p_edges = 0, p_cells = 0, p_work = 0, p_atoms = 0;  // items and queue entries: k_plan
 
     for (IdxT base = (IdxT)gw * 32; base < total; base += (IdxT)nw * 32) {
         const IdxT item = base + lane;
@@ -808,10 +819,8 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, Ws
 #pragma unroll
                 for (int u = 0; u < EXP_SMALL; u++) {
                     Relax<RowT> r{false, false, 0};
-                    if (ev[u]) {
-                        r = relax<RowT>(HV<RowT>{Hs_, (uint32_t)HGRP}, nn[u], hh[u], mk[u], l);
-                        p_cells += r.cells;
-                    }
+                    if (ev[u]) r = relax<RowT>(HV<RowT>{Hs_, (uint32_t)HGRP}, nn[u], hh[u], mk[u], l);
+                    cnt_add(p_cells, p_atoms, r.cells);
                     pw[u + 1] = r.enq;
                     ps[u + 1] = s;
                     pe[u + 1] = nn[u];
@@ -896,8 +905,8 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, Ws
                     } else if (ev[u]) {
                         r = relax<RowT>(HV<RowT>{Hb + (size_t)(o_s[u] / HGRP) * V * HGRP + o_s[u] % HGRP, (uint32_t)HGRP},
                                         n[u], hn[u], mask[u], l);
-                        p_cells += r.cells;
                     }
+                    if (!VPX) cnt_add(p_cells, p_atoms, r.cells);
                     enq[u] = r.enq;
                     idn[u] = r.ident;
                 }
@@ -932,9 +941,10 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, Ws
     p_edges = warp_sum(p_edges);
     p_cells = warp_sum(p_cells);
     p_work = warp_sum(p_work);
-    if (lane == 0 && (p_edges | p_cells)) {
+    if (lane == 0 && (p_edges | p_cells | p_atoms)) {
         atomicAdd(&w.prof[P_EDGES], (unsigned long long)p_edges);
         atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
+        atomicAdd(&w.prof[P_ATOMS], (unsigned long long)p_atoms);  // warp total already
         atomicAdd(&w.prof[P_ITEMS_WORK], (unsigned long long)p_work);
     }
 }
@@ -954,7 +964,7 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand_heavy(GraphDev
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     uint32_t nh = min(w.ctr[C_NHEAVY], w.heavy_cap);
     const RowT L = R::splat(l);
-    uint32_t p_cells = 0;
+    uint32_t p_cells = 0, p_atoms = 0;  // p_atoms: warp total (cnt_add)
     for (uint32_t it = gw; it < nh; it += nw) {
         uint4 h = w.heavy[it];
         uint32_t s = h.x;
@@ -1002,9 +1012,9 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand_heavy(GraphDev
                         if (need) vp_mark<RowT>(vp, w.ppos[s], n[u], need);
                     } else {
                         r = relax<RowT>(Hs, n[u], hn[u], mask, l);
-                        p_cells += r.cells;
                     }
                 }
+                if (!VPX) cnt_add(p_cells, p_atoms, r.cells);
                 enq[u] = r.enq;
                 idn[u] = r.ident;
             }
@@ -1018,7 +1028,10 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand_heavy(GraphDev
         }
     }
     p_cells = warp_sum(p_cells);
-    if (lane == 0 && p_cells) atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
+    if (lane == 0 && (p_cells | p_atoms)) {
+        atomicAdd(&w.prof[P_NEWCELLS], (unsigned long long)p_cells);
+        atomicAdd(&w.prof[P_ATOMS], (unsigned long long)p_atoms);
+    }
 }
 
 // Vertex-partitioned exchange slice: bit plane j of pull slot p holds, for each node of the
@@ -2778,6 +2791,23 @@ struct Tracer {  // RIKI_TRACE=<ms>: print the stage times of calls slower than 
     }
 };
 
+// NVTX ranges (header-only NVTX v3: no-ops unless a profiler such as Nsight Systems is attached):
+// one per section of a batch (central run, CG recovery, marginal run, finalize) and, in the
+// plain-launch path, one per level.  begin() closes the open range first.
+struct Nvtx {
+    bool open = false;
+    void begin(const char *m) {
+        end();
+        nvtxRangePushA(m);
+        open = true;
+    }
+    void end() {
+        if (open) nvtxRangePop();
+        open = false;
+    }
+    ~Nvtx() { end(); }
+};
+
 struct Caps {
     uint32_t slots, capc, kmax, qcap;
     uint64_t arena, out;
@@ -2845,6 +2875,7 @@ void ensure_workspace(riki_graph *g, const Caps &c) {
     ws->ovf = ws->alloc<uint2>(ws->ovf_cap);
     ws->ovf2 = ws->alloc<uint2>(ws->ovf_cap);
     ws->big_ctas = V <= (4u << 20) ? 8 : 2;
+    if (const char *e = getenv("RIKI_BIG_CTAS")) ws->big_ctas = std::max(1, atoi(e));  // A/B
     uint64_t cu = next_pow2(2 * V + 2);
     ws->big_words = cu * 3 + 4ull * (V + 1) + cu / 4 + (V + 1) / 4 + 32 + std::max<uint64_t>(std::min<uint64_t>(g->E, 1ull << 26), 1u << 20);
     ws->mtab = ws->alloc<uint4>(S * 16 * MAPCAP);
@@ -3210,6 +3241,12 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
             l += n - 1;
             continue;
         }
+        Nvtx lv;
+        {
+            char nm[48];
+            snprintf(nm, sizeof nm, "riki.run%d.level%u", ph + 1, l);
+            lv.begin(nm);
+        }
         level_pre(l);
         if (l % LEVEL_BATCH == LEVEL_BATCH - 1 || l == max_levels || pull) {
             CUDA_TRY(cudaMemcpyAsync(ws->h_ctr, ws->ctr, C_NCTR * 4, cudaMemcpyDeviceToHost, s));
@@ -3276,9 +3313,12 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
         CUDA_TRY(cudaMemset2DAsync((uint8_t *)ws->mtab + 8 * col, pitch, 0xFF, sizeof(RowM) * col, wd.nslots, s));
     }
     // ---- run 1: central keywords
+    Nvtx nv;
+    nv.begin("riki.central_run");
     L.t0 = std::chrono::steady_clock::now();
     run_phase<RowC, RowC>(L, gd, ws, 0, -1, depth + 1, 0);
     L.mark(0);
+    nv.begin("riki.cg_recovery");
     // ---- candidate CGs + recovery
     {   // (S^c, v) order of every slot's candidates: one segmented radix sort over the slots
         // (keys: level < 2^8 above a 32-bit caller id), then the candidate records
@@ -3326,10 +3366,12 @@ void run_batch_t(Launch &L, riki_graph *g, Workspace *ws, uint32_t depth) {
     // recovery of candidates that cannot enter the top-k: it pays off when the candidate sets
     // are large against k (C5: ~300 k per query, +9 %; C2: ~47 k, -3 %: r02f A/B), hence the
     // crossover below.  RIKI_EAGER_RPG=1 / RIKI_BOUNDED_RPG=1 force either mode (A/B, tests).
+    nv.begin("riki.marginal_run");
     const uint64_t per_slot = total_cands / std::max<uint32_t>(wd.nslots, 1);
     ws->bounded = getenv("RIKI_EAGER_RPG") ? 0 : getenv("RIKI_BOUNDED_RPG") ? 1 : per_slot > 100ull * ws->kmax;
     run_phase<RowM, RowC>(L, gd, ws, 1, -1, depth + 1, total_cands);
     L.mark(2);
+    nv.begin("riki.finalize");
     // ---- top-k and packing
     k_final_select<<<wd.nslots, 256, U128_SORT_KEYS * 16, s>>>(wd);
     L.check(__LINE__);
@@ -3583,6 +3625,7 @@ void add_stats(riki_graph *g, Workspace *ws, Launch &L, uint32_t nq) {
     g->stats.exp_items_work += prof[P_ITEMS_WORK];
     g->stats.exp_edges += prof[P_EDGES] + prof[P_PULLEDGES];
     g->stats.exp_new_cells += prof[P_NEWCELLS];
+    g->stats.exp_atomics += prof[P_ATOMS];
     g->stats.exp_enqueued += prof[P_ENQ];
     for (int i = 0; i < 4; i++) g->stats.section_ms[i] += L.sec_ms[i];
     g->stats.levels += L.levels;

@@ -65,7 +65,8 @@ class Stats(C.Structure):
                 ("relaxations", C.c_uint64), ("kernel_launches", C.c_uint64), ("queries", C.c_uint64),
                 ("section_ms", C.c_double * 4), ("levels", C.c_uint64), ("retries", C.c_uint64),
                 ("reallocs", C.c_uint64), ("exp_items", C.c_uint64), ("exp_items_work", C.c_uint64),
-                ("exp_edges", C.c_uint64), ("exp_new_cells", C.c_uint64), ("exp_enqueued", C.c_uint64)]
+                ("exp_edges", C.c_uint64), ("exp_new_cells", C.c_uint64), ("exp_enqueued", C.c_uint64),
+                ("exp_atomics", C.c_uint64)]
 
 
 def declared_symbols():
