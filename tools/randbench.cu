@@ -39,6 +39,7 @@ template <int MODE> __device__ __forceinline__ uint32_t ld(const uint32_t *p) {
     return v;
 }
 
+// modes >= 20: load variant (MODE - 20) followed by the dependent atomicAnd
 template <int MODE>  // 0 load, 1 atomicAnd, 2 load -> dependent atomicAnd, 3.. load variants (ld<MODE>)
 __global__ void __launch_bounds__(256) k_rand(uint32_t *a, uint64_t nwords, int iters, uint32_t *sink) {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -50,13 +51,13 @@ __global__ void __launch_bounds__(256) k_rand(uint32_t *a, uint64_t nwords, int 
         for (int c = 0; c < CH; c++) ix[c] = pick(nwords, t, it * CH + c);
         if (MODE == 0 || MODE >= 2) {
 #pragma unroll
-            for (int c = 0; c < CH; c++) v[c] = ld<MODE>(a + ix[c]);
+            for (int c = 0; c < CH; c++) v[c] = ld<(MODE >= 20 ? MODE - 20 : MODE)>(a + ix[c]);
         }
         if (MODE == 1) {
 #pragma unroll
             for (int c = 0; c < CH; c++) v[c] = atomicAnd(a + ix[c], ~(1u << ((it + c) & 31)));
         }
-        if (MODE == 2 || MODE == 11 || MODE == 13) {
+        if (MODE == 2 || MODE == 11 || MODE == 13 || MODE >= 20) {
 #pragma unroll
             for (int c = 0; c < CH; c++)
                 if (v[c]) v[c] = atomicAnd(a + ix[c], ~(1u << ((it + c) & 31)));
@@ -86,7 +87,8 @@ int main(int argc, char **argv) {
         uint32_t *a = nullptr;
         const uint64_t bytes = mb << 20;
         if (cudaMalloc(&a, bytes) != cudaSuccess) { printf("{\"error\": \"malloc %llu MiB\"}\n", (unsigned long long)mb); return 1; }
-        for (int mode = 0; mode < 14; mode++) {
+        for (int mode = 0; mode < 30; mode++) {
+            if (mode >= 14 && mode < 23) continue;
             cudaMemset(a, 0xFF, bytes);
             cudaEvent_t e0, e1;
             cudaEventCreate(&e0);
@@ -108,6 +110,13 @@ int main(int argc, char **argv) {
                 if (mode == 11) k_rand<11><<<blocks, threads>>>(a, bytes / 4, iters, sink);
                 if (mode == 12) k_rand<12><<<blocks, threads>>>(a, bytes / 4, iters, sink);
                 if (mode == 13) k_rand<13><<<blocks, threads>>>(a, bytes / 4, iters, sink);
+                if (mode == 23) k_rand<23><<<blocks, threads>>>(a, bytes / 4, iters, sink);
+                if (mode == 24) k_rand<24><<<blocks, threads>>>(a, bytes / 4, iters, sink);
+                if (mode == 25) k_rand<25><<<blocks, threads>>>(a, bytes / 4, iters, sink);
+                if (mode == 26) k_rand<26><<<blocks, threads>>>(a, bytes / 4, iters, sink);
+                if (mode == 27) k_rand<27><<<blocks, threads>>>(a, bytes / 4, iters, sink);
+                if (mode == 28) k_rand<28><<<blocks, threads>>>(a, bytes / 4, iters, sink);
+                if (mode == 29) k_rand<29><<<blocks, threads>>>(a, bytes / 4, iters, sink);
                 cudaEventRecord(e1);
                 cudaEventSynchronize(e1);
                 float ms = 0;
@@ -115,10 +124,13 @@ int main(int argc, char **argv) {
                 if (rep > 0 && ms < best) best = ms;  // first launch is a warm-up
             }
             cudaError_t err = cudaGetLastError();
-            const double acc = (double)blocks * threads * iters * CH * (mode == 2 || mode == 11 || mode == 13 ? 2 : 1);
+            const double acc = (double)blocks * threads * iters * CH * (mode == 2 || mode == 11 || mode == 13 || mode >= 20 ? 2 : 1);
             const char *name[] = {"load.cg", "atomicAnd", "load.cg+atomicAnd", "load.volatile", "load.nc", "load.cs",
                                   "load.lu", "load.ca", "load.L1::no_allocate", "load.L2::evict_first",
-                                  "atomicOr0", "atomicOr0+atomicAnd", "ld.relaxed.gpu", "ld.relaxed.gpu+atomicAnd"};
+                                  "atomicOr0", "atomicOr0+atomicAnd", "ld.relaxed.gpu", "ld.relaxed.gpu+atomicAnd",
+                                  "", "", "", "", "", "", "", "", "", "load.volatile+atomicAnd", "load.nc+atomicAnd",
+                                  "load.cs+atomicAnd", "load.lu+atomicAnd", "load.ca+atomicAnd",
+                                  "load.L1::no_allocate+atomicAnd", "load.L2::evict_first+atomicAnd"};
             printf("{\"pattern\": \"%s\", \"working_set_mib\": %llu, \"ms\": %.3f, \"g_accesses_per_s\": %.2f, "
                    "\"gb_s_at_32B\": %.0f, \"gb_s_at_64B\": %.0f, \"err\": \"%s\"}\n",
                    name[mode], (unsigned long long)mb, best, acc / best / 1e6, acc * 32 / best / 1e6,
