@@ -87,6 +87,30 @@ def test_hitting_levels_random(P, seed):
         assert L == Lo and rel == relo
 
 
+@pytest.mark.parametrize("seed", range(10))
+def test_expansion_counters_against_oracle(P, seed):
+    # the device counters behind the bench's SURVEY §8(d) byte model and random-access roofline:
+    # new cells = the oracle's finite non-seed cells of H exactly; every walked edge relaxes 1..T
+    # columns (P_e <= R <= T * P_e, R the oracle's relaxation count); every relaxation atomic
+    # turns 1..T cells (or loses a race) and follows one walked edge (cells / T <= atomics <= P_e)
+    rng = np.random.default_rng(3300 + seed)
+    V, src, dst, act, terms = random_instance(rng, 20, 300, deg=4.0, T_hi=8, post_hi=6)
+    g = _dev_graph(P, V, src, dst, act, terms)
+    og = O.Graph(V, src, dst, act)
+    T = len(terms)
+    for mode in (0, 1, 2):
+        g.reset_stats()
+        H, blk, rel, L = g.hitting_levels(np.arange(T, dtype=np.uint32), 20, mode)
+        Ho, bo, Lo, relo = O.phase(og, terms, 20, mode)
+        assert (H == Ho).all() and rel == relo
+        st = g.stats()
+        cells = int(((Ho > 0) & (Ho < INF)).sum())
+        assert st["exp_new_cells"] == cells, (st["exp_new_cells"], cells)
+        pe, atoms = st["exp_edges"], st["exp_atomics"]
+        assert pe <= relo <= T * pe, (pe, relo, T)
+        assert -(-cells // T) <= atoms <= pe, (cells, atoms, pe)
+
+
 @pytest.mark.parametrize("seed", range(12))
 def test_hitting_levels_long_rows_high_activations(P, seed):
     """Rows longer than 8 edges with activations past the gate offset table (a >= 16): the table
