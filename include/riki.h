@@ -262,7 +262,8 @@ typedef struct {
     uint64_t exp_new_cells;        /* H cells written (inf -> l+1)                          */
     uint64_t exp_enqueued;         /* next-frontier queue entries written                   */
     uint64_t exp_atomics;          /* relaxation atomics issued (rows read with a selected
-                                      inf cell): the random-access roofline's second term    */
+                                      inf cell): the random-access roofline's second term;
+                                      counted only with profiling on (riki_set_profiling)   */
 } riki_stats;
 riki_status riki_set_profiling(riki_graph *g, int on);
 riki_status riki_get_stats(const riki_graph *g, riki_stats *out);

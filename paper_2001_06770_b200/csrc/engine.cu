@@ -691,7 +691,9 @@ __device__ __forceinline__ void vp_mark(const VpPush &vp, uint32_t p, uint32_t n
 // WIDE: 64-bit frontier-item indices, for batches whose level can exceed 2^32 items
 // (slots x queue capacity >= 2^32, e.g. 200 queries on a 30M-node graph); the common
 // case keeps the 32-bit loop.  VPX: the vertex-partitioned push (VpPush above).
-template <class RowT, bool WIDE, bool VPX = false>
+// CNT: count the relaxation atomics (riki_stats.exp_atomics) -- the profiling-mode variant (the
+// per-edge ballot costs ~2 % at config 2, so the production path does not count them).
+template <class RowT, bool WIDE, bool VPX = false, bool CNT = false>
 __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, WsDev w, int ph, uint32_t l_arg,
                                                                   VpPush vp = VpPush{}) {
     typedef Row<RowT> R;
@@ -820,7 +822,8 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, Ws
                 for (int u = 0; u < EXP_SMALL; u++) {
                     Relax<RowT> r{false, false, 0};
                     if (ev[u]) r = relax<RowT>(HV<RowT>{Hs_, (uint32_t)HGRP}, nn[u], hh[u], mk[u], l);
-                    cnt_add(p_cells, p_atoms, r.cells);
+                    if (CNT) cnt_add(p_cells, p_atoms, r.cells);
+                    else p_cells += r.cells & 0xFFFF;
                     pw[u + 1] = r.enq;
                     ps[u + 1] = s;
                     pe[u + 1] = nn[u];
@@ -906,7 +909,8 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, Ws
                         r = relax<RowT>(HV<RowT>{Hb + (size_t)(o_s[u] / HGRP) * V * HGRP + o_s[u] % HGRP, (uint32_t)HGRP},
                                         n[u], hn[u], mask[u], l);
                     }
-                    if (!VPX) cnt_add(p_cells, p_atoms, r.cells);
+                    if (CNT) cnt_add(p_cells, p_atoms, r.cells);
+                    else p_cells += r.cells & 0xFFFF;
                     enq[u] = r.enq;
                     idn[u] = r.ident;
                 }
@@ -953,7 +957,7 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, Ws
 #ifndef HEAVY_UNROLL
 #define HEAVY_UNROLL 2
 #endif
-template <class RowT, bool VPX = false>
+template <class RowT, bool VPX = false, bool CNT = false>
 __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l_arg,
                                                                        VpPush vp = VpPush{}) {
     const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
@@ -1014,7 +1018,8 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand_heavy(GraphDev
                         r = relax<RowT>(Hs, n[u], hn[u], mask, l);
                     }
                 }
-                if (!VPX) cnt_add(p_cells, p_atoms, r.cells);
+                if (CNT) cnt_add(p_cells, p_atoms, r.cells);
+                else p_cells += r.cells & 0xFFFF;
                 enq[u] = r.enq;
                 idn[u] = r.ident;
             }
@@ -3117,6 +3122,14 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
                 k_jexpand<RowT, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
                 L.check(__LINE__);
             }
+        } else if (L.g->profiling) {  // the variants that also count the relaxation atomics
+            if (wide)
+                k_expand<RowT, true, false, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
+            else
+                k_expand<RowT, false, false, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
+            L.check(__LINE__);
+            k_expand_heavy<RowT, false, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
+            L.check(__LINE__);
         } else {
             if (wide)
                 k_expand<RowT, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);

@@ -96,6 +96,7 @@ def test_expansion_counters_against_oracle(P, seed):
     rng = np.random.default_rng(3300 + seed)
     V, src, dst, act, terms = random_instance(rng, 20, 300, deg=4.0, T_hi=8, post_hi=6)
     g = _dev_graph(P, V, src, dst, act, terms)
+    g.set_profiling(True)  # the atomics are counted by the profiling-mode kernels
     og = O.Graph(V, src, dst, act)
     T = len(terms)
     for mode in (0, 1, 2):
