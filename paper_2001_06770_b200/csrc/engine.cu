@@ -447,12 +447,13 @@ __device__ __forceinline__ Relax<RowT> relax(const HV<RowT> &H, uint32_t n, RowT
     if (!need) return r;
     RowT andm = ~need | (need & R::splat(l + 1));
     RowT old = R::atomic_and(H + n, andm);
-    RowT changed = need & R::eq(old, FF);
+    const RowT oldFF = R::eq(old, FF);
+    RowT changed = need & oldFF;
     r.cells = ATOM_ONE;
     if (!changed) return r;
     r.cells += R::ones(changed);
     r.enq = R::eq(old, R::splat(l + 1)) == 0;  // no cell of n was written at this level before
-    r.ident = R::eq(old & andm, FF) == 0;      // this write completed the row
+    r.ident = (oldFF & ~need) == 0;            // this write completed the row: every inf cell was in need
     return r;
 }
 
@@ -535,24 +536,28 @@ __device__ __forceinline__ void frontier_push(const WsDev &w, bool want, uint32_
 // U pushes per lane at once (the unrolled edges of one chunk, after NR leading retained
 // entries): when every pushing (lane, u) is in one slot, a single queue-counter atomic
 // covers them all.
+// su: the warp-uniform slot of every push when the caller knows it (all of the warp's items in
+// one slot), else EMPTY (then the slots are compared).
 template <int U, int NR = 0>
 __device__ __forceinline__ void frontier_push_n(const WsDev &w, const bool (&want)[U], const uint32_t (&s)[U],
-                                                const uint32_t (&entry)[U], uint32_t nxt) {
+                                                const uint32_t (&entry)[U], uint32_t nxt, uint32_t su = EMPTY) {
     uint32_t m[U], any = 0;
 #pragma unroll
     for (int u = 0; u < U; u++) any |= (m[u] = __ballot_sync(FULLMASK, want[u]));
     if (!any) return;
-    int u0 = 0;
-#pragma unroll
-    for (int u = U - 1; u >= 0; u--)
-        if (m[u]) u0 = u;
-    uint32_t s0 = 0;
-#pragma unroll
-    for (int u = 0; u < U; u++)
-        if (u == u0) s0 = __shfl_sync(FULLMASK, s[u], __ffs(m[u]) - 1);
+    uint32_t s0 = su;
     bool ok = true;
+    if (su == EMPTY) {
+        int u0 = 0;
 #pragma unroll
-    for (int u = 0; u < U; u++) ok &= !want[u] || s[u] == s0;
+        for (int u = U - 1; u >= 0; u--)
+            if (m[u]) u0 = u;
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            if (u == u0) s0 = __shfl_sync(FULLMASK, s[u], __ffs(m[u]) - 1);
+#pragma unroll
+        for (int u = 0; u < U; u++) ok &= !want[u] || s[u] == s0;
+    }
     if (__all_sync(FULLMASK, ok)) {
         uint32_t cnt = 0;
 #pragma unroll
@@ -574,8 +579,10 @@ __device__ __forceinline__ void frontier_push_n(const WsDev &w, const bool (&wan
         const uint32_t lt = lanemask_lt();
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            if (want[u]) Qd[base + __popc(m[u] & lt)] = entry[u];
-            base += __popc(m[u]);
+            if (m[u]) {  // warp-uniform: most unrolled edges push nothing
+                if (want[u]) Qd[base + __popc(m[u] & lt)] = entry[u];
+                base += __popc(m[u]);
+            }
         }
         return;
     }
@@ -927,7 +934,7 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, Ws
                     ps[u + 1] = o_s[u];
                     pe[u + 1] = n[u];
                 }
-                frontier_push_n<EXP_UNROLL + 1, 1>(w, pw, ps, pe, nxt);
+                frontier_push_n<EXP_UNROLL + 1, 1>(w, pw, ps, pe, nxt, sA == sB ? sA : EMPTY);
                 retain = false;
             }
             {   // identification appends: skipped (one vote) when no lane completed a row
@@ -1023,7 +1030,7 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand_heavy(GraphDev
                 enq[u] = r.enq;
                 idn[u] = r.ident;
             }
-            frontier_push_n<HEAVY_UNROLL>(w, enq, ss, n, nxt);
+            frontier_push_n<HEAVY_UNROLL>(w, enq, ss, n, nxt, s);  // one chunk: one slot
             bool anyid = false;
 #pragma unroll
             for (int u = 0; u < HEAVY_UNROLL; u++) anyid |= idn[u] && collect;
