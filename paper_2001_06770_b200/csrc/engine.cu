@@ -660,7 +660,15 @@ __device__ __forceinline__ void gate_range_in(const GraphDev &g, const uint4 &d,
 #ifndef EXP_MINB64
 #define EXP_MINB64 6
 #endif
-template <class RowT> struct ExpMinB { static constexpr int v = sizeof(RowT) == 8 ? EXP_MINB64 : EXP_MINB; };
+// BIG: graphs of >= EXP_BIG_V nodes, whose expansion waits on random HBM rows rather than on
+// issue: 6 blocks/SM (40 registers, no spills) for 16/32-bit rows, 5 for 64-bit rows
+// (measured: +1.3-1.7 % at config 5, -6 % at config 2 if used there)
+#ifndef EXP_BIG_V
+#define EXP_BIG_V (4u << 20)
+#endif
+template <class RowT, bool BIG = false> struct ExpMinB {
+    static constexpr int v = BIG ? (sizeof(RowT) == 8 ? 5 : 6) : (sizeof(RowT) == 8 ? EXP_MINB64 : EXP_MINB);
+};
 // Item fields of one non-empty active range, compacted per warp in shared memory for the
 // edge walk: edge index e = delta + idx, and edges with idx >= thr also carry the old columns.
 template <class RowT> struct alignas(16) OwnF {
@@ -700,8 +708,8 @@ __device__ __forceinline__ void vp_mark(const VpPush &vp, uint32_t p, uint32_t n
 // case keeps the 32-bit loop.  VPX: the vertex-partitioned push (VpPush above).
 // CNT: count the relaxation atomics (riki_stats.exp_atomics) -- the profiling-mode variant (the
 // per-edge ballot costs ~2 % at config 2, so the production path does not count them).
-template <class RowT, bool WIDE, bool VPX = false, bool CNT = false>
-__global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, WsDev w, int ph, uint32_t l_arg,
+template <class RowT, bool WIDE, bool VPX = false, bool CNT = false, bool BIG = false>
+__global__ void __launch_bounds__(256, (ExpMinB<RowT, BIG>::v)) k_expand(GraphDev g, WsDev w, int ph, uint32_t l_arg,
                                                                   VpPush vp = VpPush{}) {
     typedef Row<RowT> R;
     const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
@@ -964,8 +972,8 @@ __global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand(GraphDev g, Ws
 #ifndef HEAVY_UNROLL
 #define HEAVY_UNROLL 2
 #endif
-template <class RowT, bool VPX = false, bool CNT = false>
-__global__ void __launch_bounds__(256, ExpMinB<RowT>::v) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l_arg,
+template <class RowT, bool VPX = false, bool CNT = false, bool BIG = false>
+__global__ void __launch_bounds__(256, (ExpMinB<RowT, BIG>::v)) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l_arg,
                                                                        VpPush vp = VpPush{}) {
     const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
     typedef Row<RowT> R;
@@ -2976,6 +2984,19 @@ __global__ void k_loop_cond(WsDev w, cudaGraphConditionalHandle h, uint32_t max_
     cudaGraphSetConditional(h, go ? 1u : 0u);
 }
 
+// One level's push expansion (light items, then the heavy chunks), one wave of blocks each.
+template <class RowT, bool CNT, bool BIG>
+void expand_launch(Launch &L, const GraphDev &gd, const WsDev &wd, int ph, uint32_t l, bool wide) {
+    constexpr unsigned grid = 148 * ExpMinB<RowT, BIG>::v;
+    if (wide)
+        k_expand<RowT, true, false, CNT, BIG><<<grid, 256, 0, L.s>>>(gd, wd, ph, l);
+    else
+        k_expand<RowT, false, false, CNT, BIG><<<grid, 256, 0, L.s>>>(gd, wd, ph, l);
+    L.check(__LINE__);
+    k_expand_heavy<RowT, false, CNT, BIG><<<grid, 256, 0, L.s>>>(gd, wd, ph, l);
+    L.check(__LINE__);
+}
+
 // One vertex-partitioned level: pull over this rank's node range into its
 // slice of the bit-plane buffer (every range, in simulated mode), one in-place all-gather
 // on the search stream, then every rank applies all slices.  Identical H, blocks, frontiers
@@ -3129,22 +3150,15 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
                 k_jexpand<RowT, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
                 L.check(__LINE__);
             }
-        } else if (L.g->profiling) {  // the variants that also count the relaxation atomics
-            if (wide)
-                k_expand<RowT, true, false, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
-            else
-                k_expand<RowT, false, false, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
-            L.check(__LINE__);
-            k_expand_heavy<RowT, false, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
-            L.check(__LINE__);
-        } else {
-            if (wide)
-                k_expand<RowT, true><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
-            else
-                k_expand<RowT, false><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
-            L.check(__LINE__);
-            k_expand_heavy<RowT><<<148 * 8, 256, 0, s>>>(gd, wd, ph, l);
-            L.check(__LINE__);
+        } else {  // profiling: the variants that also count the relaxation atomics (CNT)
+            const bool big = ws->V >= EXP_BIG_V && !getenv("RIKI_NO_BIGOCC");
+            if (L.g->profiling) {
+                if (big) expand_launch<RowT, true, true>(L, gd, wd, ph, l, wide);
+                else expand_launch<RowT, true, false>(L, gd, wd, ph, l, wide);
+            } else {
+                if (big) expand_launch<RowT, false, true>(L, gd, wd, ph, l, wide);
+                else expand_launch<RowT, false, false>(L, gd, wd, ph, l, wide);
+            }
         }
     };
     if (use_graphs && !getenv("RIKI_CHUNK_GRAPHS")) {
