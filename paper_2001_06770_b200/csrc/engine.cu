@@ -666,8 +666,21 @@ __device__ __forceinline__ void gate_range_in(const GraphDev &g, const uint4 &d,
 #ifndef EXP_BIG_V
 #define EXP_BIG_V (4u << 20)
 #endif
+#ifndef EXP_MINB_BIG
+#define EXP_MINB_BIG 6
+#endif
+#ifndef EXP_MINB64_BIG
+#define EXP_MINB64_BIG 5
+#endif
+#ifndef EXP_UNROLL_BIG
+#define EXP_UNROLL_BIG 3
+#endif
+#ifndef HEAVY_UNROLL_BIG
+#define HEAVY_UNROLL_BIG 2
+#endif
 template <class RowT, bool BIG = false> struct ExpMinB {
-    static constexpr int v = BIG ? (sizeof(RowT) == 8 ? 5 : 6) : (sizeof(RowT) == 8 ? EXP_MINB64 : EXP_MINB);
+    static constexpr int v = BIG ? (sizeof(RowT) == 8 ? EXP_MINB64_BIG : EXP_MINB_BIG)
+                                 : (sizeof(RowT) == 8 ? EXP_MINB64 : EXP_MINB);
 };
 // Item fields of one non-empty active range, compacted per warp in shared memory for the
 // edge walk: edge index e = delta + idx, and edges with idx >= thr also carry the old columns.
@@ -711,6 +724,7 @@ __device__ __forceinline__ void vp_mark(const VpPush &vp, uint32_t p, uint32_t n
 template <class RowT, bool WIDE, bool VPX = false, bool CNT = false, bool BIG = false>
 __global__ void __launch_bounds__(256, (ExpMinB<RowT, BIG>::v)) k_expand(GraphDev g, WsDev w, int ph, uint32_t l_arg,
                                                                   VpPush vp = VpPush{}) {
+    constexpr int UNR = BIG ? EXP_UNROLL_BIG : EXP_UNROLL;
     typedef Row<RowT> R;
     const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
     typedef typename std::conditional<WIDE, unsigned long long, uint32_t>::type IdxT;
@@ -857,7 +871,7 @@ __global__ void __launch_bounds__(256, (ExpMinB<RowT, BIG>::v)) k_expand(GraphDe
             }
         }
 #endif
-        // Edge-parallel walk over the concatenated active ranges, EXP_UNROLL edges per lane in
+        // Edge-parallel walk over the concatenated active ranges, UNR (EXP_UNROLL, EXP_UNROLL_BIG) edges per lane in
         // flight.  The non-empty ranges are compacted into s_own (rank order = start order);
         // the owner of edge position p of a 32-wide chunk is found from the bit mask of range
         // starts inside the chunk (one OR-reduction) instead of a per-edge binary search.
@@ -884,12 +898,12 @@ __global__ void __launch_bounds__(256, (ExpMinB<RowT, BIG>::v)) k_expand(GraphDe
         }
         const uint32_t le_mask = lanemask_lt() | (1u << lane);
         int own_last = -1;
-        for (uint32_t eb = 0; eb < tot; eb += 32 * EXP_UNROLL) {
-            uint32_t n[EXP_UNROLL], o_s[EXP_UNROLL];
-            RowT mask[EXP_UNROLL], hn[EXP_UNROLL];
-            bool ev[EXP_UNROLL];
+        for (uint32_t eb = 0; eb < tot; eb += 32 * UNR) {
+            uint32_t n[UNR], o_s[UNR];
+            RowT mask[UNR], hn[UNR];
+            bool ev[UNR];
 #pragma unroll
-            for (int u = 0; u < EXP_UNROLL; u++) {
+            for (int u = 0; u < UNR; u++) {
                 const uint32_t cb = eb + 32 * u;
                 const uint32_t off = excl - cb;  // < 32 iff this lane's range starts in the chunk
                 const uint32_t M = __reduce_or_sync(FULLMASK, (len > 0 && off < 32) ? 1u << off : 0u);
@@ -904,18 +918,18 @@ __global__ void __launch_bounds__(256, (ExpMinB<RowT, BIG>::v)) k_expand(GraphDe
                 mask[u] = o.nw | (idx >= o.thr ? o.od : (RowT)0);  // [eqlo, hi) are the edges with a == l
             }
 #pragma unroll
-            for (int u = 0; u < EXP_UNROLL; u++)
+            for (int u = 0; u < UNR; u++)
                 hn[u] = ev[u] ? R::load(Hb + ((size_t)(o_s[u] / HGRP) * V + n[u]) * HGRP + o_s[u] % HGRP) : (RowT)0;
-            bool enq[EXP_UNROLL], idn[EXP_UNROLL];
+            bool enq[UNR], idn[UNR];
             if (!VPX && EXP_BATCH_ATOM) {
-                RowT *rowp[EXP_UNROLL];
+                RowT *rowp[UNR];
 #pragma unroll
-                for (int u = 0; u < EXP_UNROLL; u++)
+                for (int u = 0; u < UNR; u++)
                     rowp[u] = Hb + ((size_t)(o_s[u] / HGRP) * V + n[u]) * HGRP + o_s[u] % HGRP;
-                relax_n<RowT, EXP_UNROLL>(rowp, hn, mask, ev, l, enq, idn, p_cells);
+                relax_n<RowT, UNR>(rowp, hn, mask, ev, l, enq, idn, p_cells);
             } else {
 #pragma unroll
-                for (int u = 0; u < EXP_UNROLL; u++) {
+                for (int u = 0; u < UNR; u++) {
                     Relax<RowT> r{false, false, 0};
                     if (VPX) {  // H is read-only during a partitioned level: mark the owner's bit planes
                         const RowT need = mask[u] & R::eq(hn[u], R::splat(0xFF));
@@ -931,27 +945,27 @@ __global__ void __launch_bounds__(256, (ExpMinB<RowT, BIG>::v)) k_expand(GraphDe
                 }
             }
             {
-                bool pw[EXP_UNROLL + 1];
-                uint32_t ps[EXP_UNROLL + 1], pe[EXP_UNROLL + 1];
+                bool pw[UNR + 1];
+                uint32_t ps[UNR + 1], pe[UNR + 1];
                 pw[0] = retain;
                 ps[0] = s;
                 pe[0] = f | RETAINED;
 #pragma unroll
-                for (int u = 0; u < EXP_UNROLL; u++) {
+                for (int u = 0; u < UNR; u++) {
                     pw[u + 1] = enq[u];
                     ps[u + 1] = o_s[u];
                     pe[u + 1] = n[u];
                 }
-                frontier_push_n<EXP_UNROLL + 1, 1>(w, pw, ps, pe, nxt, sA == sB ? sA : EMPTY);
+                frontier_push_n<UNR + 1, 1>(w, pw, ps, pe, nxt, sA == sB ? sA : EMPTY);
                 retain = false;
             }
             {   // identification appends: skipped (one vote) when no lane completed a row
                 bool anyid = false;
 #pragma unroll
-                for (int u = 0; u < EXP_UNROLL; u++) anyid |= idn[u];
+                for (int u = 0; u < UNR; u++) anyid |= idn[u];
                 if (__any_sync(FULLMASK, anyid)) {
 #pragma unroll
-                    for (int u = 0; u < EXP_UNROLL; u++)
+                    for (int u = 0; u < UNR; u++)
                         cand_push(g, w, idn[u] && ((s_info[o_s[u]] >> 1) & 1), o_s[u], n[u], l + 1);
                 }
             }
@@ -975,6 +989,7 @@ __global__ void __launch_bounds__(256, (ExpMinB<RowT, BIG>::v)) k_expand(GraphDe
 template <class RowT, bool VPX = false, bool CNT = false, bool BIG = false>
 __global__ void __launch_bounds__(256, (ExpMinB<RowT, BIG>::v)) k_expand_heavy(GraphDev g, WsDev w, int ph, uint32_t l_arg,
                                                                        VpPush vp = VpPush{}) {
+    constexpr int HUNR = BIG ? HEAVY_UNROLL_BIG : HEAVY_UNROLL;
     const uint32_t l = l_arg == LV_DEVICE ? w.ctr[C_LEVEL] : l_arg;
     typedef Row<RowT> R;
     const uint32_t lane = lane_id();
@@ -995,34 +1010,34 @@ __global__ void __launch_bounds__(256, (ExpMinB<RowT, BIG>::v)) k_expand_heavy(G
         RowT Rf = R::load(Hs + h.y);  // values <= l are final; concurrent l+1 writes don't change the masks
         RowT newc = R::eq(Rf, L) & used, oldc = R::lt(Rf, L) & used;
         bool collect = st.collect;
-        for (uint32_t e0 = h.z; e0 < h.w; e0 += 32 * HEAVY_UNROLL) {
-            uint32_t n[HEAVY_UNROLL], a[HEAVY_UNROLL];
-            RowT hn[HEAVY_UNROLL];
+        for (uint32_t e0 = h.z; e0 < h.w; e0 += 32 * HUNR) {
+            uint32_t n[HUNR], a[HUNR];
+            RowT hn[HUNR];
 #pragma unroll
-            for (int u = 0; u < HEAVY_UNROLL; u++) {
+            for (int u = 0; u < HUNR; u++) {
                 uint32_t e = e0 + 32 * u + lane;
                 n[u] = e < h.w ? STREAM_LD(g.col + e) : 0;
                 a[u] = e < h.w ? __ldg(g.act + e) : 0xFF;
             }
 #pragma unroll
-            for (int u = 0; u < HEAVY_UNROLL; u++) hn[u] = (e0 + 32 * u + lane < h.w) ? R::load(Hs + n[u]) : (RowT)0;
-            bool enq[HEAVY_UNROLL], idn[HEAVY_UNROLL];
-            uint32_t ss[HEAVY_UNROLL];
+            for (int u = 0; u < HUNR; u++) hn[u] = (e0 + 32 * u + lane < h.w) ? R::load(Hs + n[u]) : (RowT)0;
+            bool enq[HUNR], idn[HUNR];
+            uint32_t ss[HUNR];
 #pragma unroll
-            for (int u = 0; u < HEAVY_UNROLL; u++) ss[u] = s;
+            for (int u = 0; u < HUNR; u++) ss[u] = s;
             if (!VPX && EXP_BATCH_ATOM) {
-                RowT *rowp[HEAVY_UNROLL], mk[HEAVY_UNROLL];
-                bool ev[HEAVY_UNROLL];
+                RowT *rowp[HUNR], mk[HUNR];
+                bool ev[HUNR];
 #pragma unroll
-                for (int u = 0; u < HEAVY_UNROLL; u++) {
+                for (int u = 0; u < HUNR; u++) {
                     ev[u] = e0 + 32 * u + lane < h.w;
                     rowp[u] = Hs + n[u];
                     mk[u] = newc | (a[u] == l ? oldc : (RowT)0);
                 }
-                relax_n<RowT, HEAVY_UNROLL>(rowp, hn, mk, ev, l, enq, idn, p_cells);
+                relax_n<RowT, HUNR>(rowp, hn, mk, ev, l, enq, idn, p_cells);
             } else
 #pragma unroll
-            for (int u = 0; u < HEAVY_UNROLL; u++) {
+            for (int u = 0; u < HUNR; u++) {
                 Relax<RowT> r{false, false, 0};
                 if (e0 + 32 * u + lane < h.w) {
                     RowT mask = newc | (a[u] == l ? oldc : (RowT)0);
@@ -1038,13 +1053,13 @@ __global__ void __launch_bounds__(256, (ExpMinB<RowT, BIG>::v)) k_expand_heavy(G
                 enq[u] = r.enq;
                 idn[u] = r.ident;
             }
-            frontier_push_n<HEAVY_UNROLL>(w, enq, ss, n, nxt, s);  // one chunk: one slot
+            frontier_push_n<HUNR>(w, enq, ss, n, nxt, s);  // one chunk: one slot
             bool anyid = false;
 #pragma unroll
-            for (int u = 0; u < HEAVY_UNROLL; u++) anyid |= idn[u] && collect;
+            for (int u = 0; u < HUNR; u++) anyid |= idn[u] && collect;
             if (__any_sync(FULLMASK, anyid))
 #pragma unroll
-                for (int u = 0; u < HEAVY_UNROLL; u++) cand_push(g, w, idn[u] && collect, s, n[u], l + 1);
+                for (int u = 0; u < HUNR; u++) cand_push(g, w, idn[u] && collect, s, n[u], l + 1);
         }
     }
     p_cells = warp_sum(p_cells);
