@@ -661,16 +661,17 @@ __device__ __forceinline__ void gate_range_in(const GraphDev &g, const uint4 &d,
 #define EXP_MINB64 6
 #endif
 // BIG: graphs of >= EXP_BIG_V nodes, whose expansion waits on random HBM rows rather than on
-// issue: 6 blocks/SM (40 registers, no spills) for 16/32-bit rows, 5 for 64-bit rows
-// (measured: +1.3-1.7 % at config 5, -6 % at config 2 if used there)
+// issue: 4 blocks/SM (no spills) for every row width -- fewer warps in flight thrash L2 less
+// (measured against 8/6 blocks: +5-8 % at config 5, +13 % at config 3; -6 % at config 2 if
+// used there; profiles/r02_ab_experiments.txt r02x-r02ab)
 #ifndef EXP_BIG_V
 #define EXP_BIG_V (4u << 20)
 #endif
 #ifndef EXP_MINB_BIG
-#define EXP_MINB_BIG 6
+#define EXP_MINB_BIG 4
 #endif
 #ifndef EXP_MINB64_BIG
-#define EXP_MINB64_BIG 5
+#define EXP_MINB64_BIG 4
 #endif
 #ifndef EXP_UNROLL_BIG
 #define EXP_UNROLL_BIG 3
