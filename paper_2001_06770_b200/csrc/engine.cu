@@ -3167,7 +3167,9 @@ void run_phase(Launch &L, const GraphDev &gd, Workspace *ws, int ph, int hitting
                 L.check(__LINE__);
             }
         } else {  // profiling: the variants that also count the relaxation atomics (CNT)
-            const bool big = ws->V >= EXP_BIG_V && !getenv("RIKI_NO_BIGOCC");
+            // (a batch: with a few queries in flight L2 is not thrashed, and a lone query's flood
+            // level wants every warp -- single-query p99 at config 5 was 71 ms at 4 blocks/SM)
+            const bool big = ws->V >= EXP_BIG_V && wd.nslots >= 8 && !getenv("RIKI_NO_BIGOCC");
             if (L.g->profiling) {
                 if (big) expand_launch<RowT, true, true>(L, gd, wd, ph, l, wide);
                 else expand_launch<RowT, true, false>(L, gd, wd, ph, l, wide);
