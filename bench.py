@@ -412,15 +412,10 @@ def main():
 
     # ---------------- single-query latency (one query in flight, host API incl. D2H)
     gc.collect()
-    # warm the single-slot path once per H row-width shape of the timed queries (each shape has its
-    # own CUDA graphs of the level loop: their one-time capture is not query latency)
-    def _rb(t):
-        return 2 if t <= 2 else 4 if t <= 4 else 8
+    # warm-up: the timed queries run once untimed -- one-time costs (the level-loop CUDA graphs of
+    # each H row-width shape, capacity growth of the single-slot workspace) are not query latency
     nlat = min(args.latency_queries, len(qs.central))
-    warm = {}
     for i in range(nlat):
-        warm.setdefault((_rb(len(qs.central[i])), _rb(len(qs.marginal[i]))), i)
-    for i in sorted(set(warm.values()) | {0, 1, 2}):
         g.search(qs.central[i], qs.marginal[i], qs.k, qs.depth)
     lat = []
     for i in range(nlat):
